@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 Laplace solve by PCG + geometric p-multigrid on B200.
+
+One step = one full Laplace solve (all SURVEY §8(a) rows: lift, PCG with one
+V-cycle per iteration -- Schwarz smoothing, transfers, P=1 coarse solve -- to
+rtol 1e-8 from phi_F = 0) of BASELINE.json config 3 (65,536 curvilinear
+prisms, p = 5, 4.2 M DOF), inputs resident in HBM.  Metric: Laplace solve
+MDOF/s (free DOF / solve time).  See DESIGN.md §"Measurement".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+N > 1 runs under torchrun: every rank solves its own copy (replicas; the
+partitioned solve is NEXT, DESIGN.md §"Multi-GPU").
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Laplace solve MDOF/s (p-MG, tol 1e-8) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="config3", choices=["config1", "config2", "config3"])
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def make_mesh(name):
+    from workloads import config1, config2, config3
+    return {"config1": config1, "config2": config2, "config3": config3}[name]()
+
+
+WORKLOAD = {
+    "config1": "config1: box [0,2]x[0,1]x[-1,0], 64 straight prisms, p=3",
+    "config2": "config2: wave channel [0,16]x[0,1], 2048 curved prisms, p=4",
+    "config3": "config3: 3D wave basin [0,32]^2, 8192 jittered triangles x 8 layers = 65,536 curved prisms, p=5",
+}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def oracle_sample(tol, budget_s=20.0):
+    """The oracle as it stands (PCG + p-MG of Alg 4.1/4.3 on the assembled
+    matrices, hierarchy setup excluded like the GPU's) on a bounded sample of
+    the config-3 workload: the same construction (jitter, 8 waves, p = 5,
+    same element size) on an 8x8-quad x 2-layer patch."""
+    import numpy as np
+    from oracle import pmg, sem
+    from workloads.configs import basin
+    m = basin("config3_sample", 5, 32.0 * 8 / 64, 8, 2, seed=3)
+    mg = pmg.PMG(m)
+    lev = mg.levels[0].level
+    phiD = m.phi(*lev.xyz.T)
+    A, b = sem.dirichlet_lift(lev, phiD)
+    times, info = [], None
+    t_end = time.perf_counter() + budget_s
+    while True:
+        t0 = time.perf_counter()
+        _, info = pmg.pcg(mg, b, rtol=tol)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= 50:
+            break
+    t = statistics.median(times)
+    nfree = len(lev.free)
+    try:
+        from threadpoolctl import threadpool_info
+        thr = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:
+        thr = 1
+    return dict(value=nfree / t / 1e6, unit="MDOF/s", cores=int(thr), kind="oracle",
+                sample=f"oracle PCG-p-MG solve (tol {tol:g}, levels {mg.schedule}) of a config-3-construction "
+                       f"patch: 8x8 quads x 2 layers = {m.n_elem} prisms, p=5, {nfree} free DOF; median of "
+                       f"{len(times)} solves ({info['iters']} iterations); host cores available "
+                       f"{len(os.sched_getaffinity(0))}",
+                t_solve_s=t, n_free=nfree, iters=info["iters"])
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    samples = []
+    for i in range(args.warmup + args.steps):
+        s = oracle_sample(args.tol, budget_s=0.0)
+        if i >= args.warmup:
+            samples.append(s)
+    v = statistics.median([s["value"] for s in samples])
+    ms = statistics.median([s["t_solve_s"] for s in samples]) * 1e3
+    cb = dict(samples[0])
+    cb["value"] = v
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "MDOF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD["config3"] + " (CPU oracle on a bounded sample, see cpu_baseline.sample)",
+                   "tol": args.tol},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": "MDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------------ GPU arm
+def schwarz_alg_bytes(s, level=0):
+    """Algorithmic bytes of one Schwarz sweep: the packed symmetric inverses
+    n_k(n_k+1)/2 * 8 B, the subdomain index lists, and one read of r, W, u and
+    one write of u per node (DESIGN.md §"Roofline")."""
+    return s._alg_schwarz_bytes
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2009_00705_b200 as lib
+    from paper_2009_00705_b200.metrics import schwarz_bytes_model, apply_bytes_model
+
+    m = make_mesh(args.config)
+    t0 = time.perf_counter()
+    s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
+                   verbose=int(os.environ.get("SEM_VERBOSE", "0")))
+    setup_s = time.perf_counter() - t0
+    info = s.info
+    xyz = s.node_xyz(0)
+    phiD_h = m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])
+    phiD = torch.from_numpy(phiD_h).cuda()
+    phi = s.empty(0)
+    stream = s.stream
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    reps = []
+    for _ in range(args.warmup):
+        _, rep = s.solve(phiD, args.tol, out=phi)
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    s.launches(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        _, rep = s.solve(phiD, args.tol, out=phi)
+        reps.append(rep)
+    ev1.record(stream)
+    barrier()
+    launches = s.launches()
+    ms_total = ev0.elapsed_time(ev1)
+    clocks = clk.stop()
+    if dist is not None:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    n_free = info["n_free"]
+    value = n_free * world / (ms_step * 1e-3) / 1e6
+
+    # ---- dominant kernel: Schwarz sweep on the finest level, timed alone on the solve's stream
+    res = {}
+    r0 = torch.randn(info["n_dof"], dtype=torch.float64, device="cuda")
+    u0 = s.empty(0)
+    nrep = 20
+    for _ in range(3):
+        s.schwarz(0, r0, u0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(nrep):
+        s.schwarz(0, r0, u0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_schwarz = e0.elapsed_time(e1) / nrep * 1e-3
+    sb = schwarz_bytes_model(s, m)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = peaks["hbm_gbs"]
+    ach = sb / t_schwarz / 1e9
+    roof = {"kernel": "k_schwarz (level 0, one sweep)", "bound": "hbm", "achieved": ach, "peak": peak,
+            "unit": "GB/s", "frac": ach / peak, "traffic": None, "alg_bytes_per_launch": sb,
+            "launch_us": t_schwarz * 1e6,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback"}
+    # ---- operator apply (north_star: >= 60 % of HBM)
+    for _ in range(3):
+        s.apply(r0, out=u0)
+    e0.record(stream)
+    for _ in range(nrep):
+        s.apply(r0, out=u0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_apply = e0.elapsed_time(e1) / nrep * 1e-3
+    ab = apply_bytes_model(s, m)
+    apply = {"kernel": "k_apply<5> (+memset)", "MDOF_s": info["n_dof"] / t_apply / 1e6, "us": t_apply * 1e6,
+             "achieved_GBs": ab / t_apply / 1e9, "frac": ab / t_apply / 1e9 / peak, "alg_bytes_per_launch": ab,
+             "flops_per_launch": s._apply_flops if hasattr(s, "_apply_flops") else None}
+    # ---- end to end through the public host API
+    e2e = None
+    if not args.no_e2e:
+        ph = torch.from_numpy(phiD_h).pin_memory()
+        out_h = torch.empty(info["n_dof"], dtype=torch.float64).pin_memory()
+        s.solve_host(ph, args.tol, out_h)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s.solve_host(ph, args.tol, out_h)
+        barrier()
+        t_e2e = (time.perf_counter() - t0) / args.steps
+        if dist is not None:
+            t = torch.tensor([t_e2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        e2e = {"value": n_free * world / t_e2e / 1e6, "unit": "MDOF/s",
+               "h2d_bytes_per_step": info["n_dof"] * 8, "d2h_bytes_per_step": info["n_dof"] * 8,
+               "ms_per_step": t_e2e * 1e3, "api": "laplace_solve_host (pinned host buffers)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = oracle_sample(args.tol)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    rep = reps[-1]
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "MDOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD[args.config], "p": m.p, "n_dof": info["n_dof"], "n_free": n_free,
+                       "n_elem": info["n_elem"], "levels": info["level_p"], "tol": args.tol, "nu": [3, 3],
+                       "smoother": "additive Schwarz, overlap 1, exact dense local inverses (eq 4.4-4.6)",
+                       "outer": "PCG (Alg 4.3)", "coarse": f"dense inverse, {info['coarse_n']} free P=1 DOF",
+                       "l2": "inputs larger than L2: each V-cycle streams "
+                             f"{sum(info['schwarz_bytes']) / 1e9:.1f} GB of Schwarz inverses",
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "setup_s": setup_s},
+            "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "q_mean": rep["q_mean"],
+            "roofline": roof, "apply": apply, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,215 @@
+/*
+ * sem_pmg.h — C ABI of the B200-native geometric p-multigrid Laplace solver
+ * (arXiv 2009.00705, Engsig-Karup et al.).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper); S:n = SPEC.md line n;
+ * On = reading n of DESIGN.md §"Readings" (= SURVEY.md §8(c) register).
+ *
+ * The problem (eq 2.2):   phi = phi~ on the free surface (Dirichlet),
+ *   laplace(phi) = 0 in the fluid, n.grad(phi) = 0 on bottom / walls / hull,
+ * discretised by continuous-Galerkin spectral elements on curvilinear prisms
+ * (eq 3.8) and solved by PCG (Alg 4.3) preconditioned
+ * with one geometric p-multigrid V-cycle (Alg 4.1): additive
+ * Schwarz smoother (eq 4.4-4.6), R = P^T (eq 4.3),
+ * exact P=1 coarse solve.
+ *
+ * General conventions
+ *  - All floating point is IEEE FP64.  Indices are int32.
+ *  - Vector arguments of the compute calls are DEVICE pointers (cudaMalloc or
+ *    torch CUDA tensors) of length n_dof(level) in the library's node
+ *    numbering, unless a name ends in _host.  They are caller-owned; the
+ *    library never frees or retains them beyond the call.
+ *  - Calls are asynchronous with respect to the host only where stated;
+ *    every compute call is enqueued on opts.stream (NULL = legacy default
+ *    stream) and the functions that return scalars synchronise that stream.
+ *  - Return value: 0 on success, a negative SEM_E* code otherwise;
+ *    sem_strerror() gives a message.  A failed call leaves the ctx usable
+ *    unless the code is SEM_ECUDA (sticky device error).
+ *  - A sem_ctx is not thread-safe: one ctx per device per thread.
+ *  - Reference prism: {r,s >= -1, r+s <= 0} x [-1,1]; bottom vertices v0,v1,v2
+ *    at (r,s) = (-1,-1),(1,-1),(-1,1), t = -1; top v3,v4,v5 above, t = +1.
+ *    Local node n = m + Nt*l: m indexes the triangle nodes (for j in 0..p, for
+ *    i in 0..p-j: barycentric (k=p-i-j, i, j) toward (v0, v1, v2)), l the
+ *    vertical LGL level.  Triangle nodes: Blyth-Pozrikidis (reading O1).
+ */
+#ifndef SEM_PMG_H
+#define SEM_PMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ---------------------- */
+#define SEM_OK            0
+#define SEM_EINVAL       -1   /* bad argument: p < 1 or > 8, bad tags, NULL    */
+#define SEM_EBADELEM     -2   /* detJ <= 0 at a cubature point         */
+#define SEM_ENOMEM       -3   /* device allocation failed (e.g. dense Schwarz) */
+#define SEM_ESINGULAR    -4   /* Schwarz block / coarse Cholesky failed*/
+#define SEM_ENOTCONV     -5   /* imax reached; phi holds the last iterate */
+#define SEM_EBREAKDOWN   -6   /* PCG p^T q <= 0                        */
+#define SEM_ECUDA        -7   /* CUDA runtime / cuSOLVER / cuBLAS error        */
+#define SEM_ENCCL        -8   /* reserved: multi-GPU communication error       */
+#define SEM_EUNSUPPORTED -9   /* option combination not built (see message)    */
+
+/* ---- face tags ----------------------------------------------- */
+#define SEM_FACE_INTERIOR  0
+#define SEM_FACE_DIRICHLET 1  /* free surface Gamma^FS: phi = phi~            */
+#define SEM_FACE_NEUMANN   2  /* bottom, walls, hull: n.grad phi = 0          */
+
+typedef struct sem_ctx sem_ctx;   /* opaque; owns all of its device memory */
+
+/* Prism mesh (host memory, caller-owned, copied during sem_setup). */
+typedef struct {
+  int32_t n_vert;
+  const double *xyz;          /* [n_vert][3] vertex coordinates                      */
+  int32_t n_prism;
+  const int32_t *prism;       /* [n_prism][6] v0 v1 v2 bottom (CCW seen from +z), v3 v4 v5 above them */
+  const uint8_t *face_tag;    /* [n_prism][5] faces (bot, top, q01, q12, q20), SEM_FACE_*            */
+  const double *node_xyz;     /* [n_prism][N(p)][3] curvilinear nodes of the finest order in the local
+                                 order above (the nodal element map), or NULL = straight-sided */
+} sem_mesh;
+
+typedef struct {
+  int nu1, nu2;               /* pre/post smoothing steps; default 3,3 (O20)          */
+  int overlap;                /* Schwarz overlap in nodes: 0 = block Jacobi, 1 (default),
+                                 -1 = refined ceil((P+1)/2) per level                        */
+  int literal_smoother;       /* 0 (default): post-smoothing with S^-T (reading O14, symmetric V-cycle);
+                                 1: W left-applied pre and post exactly as eq 4.4 prints it         */
+  int outer;                  /* 0 PCG (Alg 4.3, default), 1 PDC (Alg 4.2), 2 stand-alone MG        */
+  const int *levels;          /* explicit level orders, finest first, last = 1, or NULL
+                                 = P -> ceil((P+1)/2) with strict-decrease guard (O18)       */
+  int n_levels;
+  double atol;                /* absolute tolerance of the stop test, default 0              */
+  int imax;                   /* max outer iterations, default 200                                  */
+  void *stream;               /* cudaStream_t for every kernel; NULL = default stream               */
+  int device;                 /* CUDA device ordinal used by sem_setup (default: current device)    */
+  int verbose;                /* 1: setup timings to stderr                                         */
+} sem_opts;
+
+typedef struct {
+  int iters;                  /* outer iterations                                                   */
+  int vcycles;                /* V-cycles applied (iterations + 1 for PCG)           */
+  int converged;              /* 1 if ||r|| <= rtol ||f|| + atol (O21)                        */
+  double rel_res;             /* final ||r||_2 / ||f||_2 over free nodes                            */
+  double q_mean;              /* geometric mean of q = ||r^m||/||r^m-1|| (eq 4.7; O22)        */
+  double t_ms;                /* device time of the solve (CUDA events)                             */
+  double norm_f;              /* ||b_F||_2                                                           */
+  int n_hist;                 /* entries of res_hist used                                            */
+  double res_hist[256];       /* ||r^m||_2, m = 0..iters                                            */
+} sem_report;
+
+typedef struct {
+  int64_t n_dof;              /* nodes of the finest level (incl. Dirichlet)                        */
+  int64_t n_free;             /* free (non-Dirichlet) nodes of the finest level                     */
+  int64_t n_elem;             /* prisms                                                             */
+  int n_levels;               /* multigrid levels, finest first                                     */
+  int level_p[16];            /* polynomial order of each level                                     */
+  int64_t level_n_dof[16];    /* nodes per level                                                    */
+  int64_t level_n_free[16];
+  int64_t schwarz_bytes[16];  /* bytes of stored Schwarz inverses per level (0 on the coarsest)     */
+  int64_t schwarz_nk_sum[16]; /* sum over subdomains of n_k (free nodes per subdomain)              */
+  int64_t schwarz_packed[16]; /* sum over subdomains of n_k (n_k+1)/2 (packed symmetric entries)    */
+  int64_t coarse_n;           /* free nodes of the P=1 level (size of the dense coarse inverse)     */
+  int64_t device_bytes;       /* total device memory held by the ctx                                */
+  double setup_ms;            /* wall time of sem_setup                                             */
+} sem_info;
+
+/* Default options (values above). */
+void sem_default_opts(sem_opts *opts);
+
+/* Reference coordinates [N(p)][3] of the local prism nodes of order p in the
+ * library's local order (see the conventions above).  rst: host, caller-owned,
+ * 3*N(p) doubles, N(p) = (p+1)^2 (p+2)/2.  Returns SEM_EINVAL for p<1 or p>8. */
+int sem_reference_nodes(int p, double *rst);
+
+/* Build the solver for order p (1..8) on `mesh` (all level
+ * operators, smoothers and the coarse factor are formed once here and reused).
+ * Allocates device memory on the current device; *out receives the ctx.
+ * Errors: SEM_EINVAL, SEM_EBADELEM, SEM_ENOMEM, SEM_ESINGULAR, SEM_ECUDA. */
+int sem_setup(const sem_mesh *mesh, int p, const sem_opts *opts, sem_ctx **out);
+
+int sem_get_info(const sem_ctx *ctx, sem_info *info);
+
+/* Copy the coordinates of the level's global nodes, [n_dof(level)][3], into
+ * `xyz` (device pointer if on_device, else host).  Lets callers map the
+ * library numbering to theirs (parity tests map by coordinates). */
+int sem_node_xyz(const sem_ctx *ctx, int level, double *xyz, int on_device);
+
+/* Dirichlet mask of a level, [n_dof(level)] uint8 (1 = Dirichlet), device or host. */
+int sem_dirichlet_mask(const sem_ctx *ctx, int level, uint8_t *mask, int on_device);
+
+/* y = A u on `level` (0 = finest), A = -L of eq 3.8 (reading O3),
+ * matrix-free with gather-scatter of shared nodes.
+ * masked = 0: the raw Neumann stiffness (every row and column).
+ * masked = 1: the Dirichlet-eliminated operator: u is read on free nodes only
+ *             (Dirichlet entries treated as 0), y_free = (A_FF u_F),
+ *             y_Dirichlet = u_Dirichlet (identity rows).
+ * u, y: device, distinct. */
+int sem_apply_laplace(sem_ctx *ctx, const double *u, double *y, int level, int masked);
+
+/* z = V(r): one V-cycle of Alg 4.1 from a zero initial guess on the finest
+ * level (the preconditioner M^-1 of eq 4.1).  r is read on free nodes only;
+ * z has zeros on Dirichlet nodes.  r, z: device, distinct. */
+int pmg_vcycle(sem_ctx *ctx, const double *r, double *z);
+
+/* Solve the discrete Laplace problem (eq 2.2 / 3.8):
+ *   phi = dirichlet_phi on Dirichlet nodes; A_FF phi_F = b_F - A_FD phi_D,
+ * b = rhs (Neumann load vector, NULL = 0), by the outer iteration opts.outer
+ * until ||r||_2 <= tol*||b_F - A_FD phi_D||_2 + atol from phi_F = 0.
+ * dirichlet_phi is read on Dirichlet nodes only; phi (output) holds the
+ * solution including the Dirichlet values.  rep may be NULL.
+ * Returns SEM_ENOTCONV (phi = last iterate, rep->converged = 0) if imax is
+ * reached, SEM_EBREAKDOWN if p^T A p <= 0. */
+int laplace_solve(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
+                  double tol, double *phi, sem_report *rep);
+
+/* laplace_solve with HOST buffers (pinned recommended): copies rhs (if not
+ * NULL) and dirichlet_phi host->device, solves, copies phi device->host, all
+ * on opts.stream, and synchronises.  The end-to-end entry point. */
+int laplace_solve_host(sem_ctx *ctx, const double *rhs_host, const double *dirichlet_phi_host,
+                       double tol, double *phi_host, sem_report *rep);
+
+/* ---- diagnostic entry points: each one step of the V-cycle, for parity ---- */
+/* uf += P uc: prolongation from level+1 to level, uc read on free
+ * nodes of level+1; only free fine nodes are updated. */
+int sem_prolong(sem_ctx *ctx, int level, const double *uc, double *uf);
+/* rc = P^T rf (eq 4.3): restriction from level to level+1; rf read on free
+ * nodes; rc written on all nodes (0 on Dirichlet nodes). */
+int sem_restrict(sem_ctx *ctx, int level, const double *rf, double *rc);
+/* u += S^-1 r (transpose=0) or u += S^-T r (transpose=1): one additive Schwarz
+ * correction of eq 4.2/4.4 on `level` (not the coarsest); r read on free nodes. */
+int sem_schwarz(sem_ctx *ctx, int level, const double *r, double *u, int transpose);
+/* z = A_1^-1 r on the coarsest level (exact coarse solve); z = 0 on Dirichlet. */
+int sem_coarse_solve(sem_ctx *ctx, const double *r, double *z);
+
+/* Number of kernel launches the library enqueued since the last reset. */
+int64_t sem_launch_count(const sem_ctx *ctx, int reset);
+
+void sem_destroy(sem_ctx *ctx);
+
+/* ---- host-only diagnostics (no device needed; used by the CPU test tier) ---- */
+/* Global numbering of V^p on `mesh` exactly as sem_setup builds it.  Two-call
+ * pattern: pass NULL arrays to query sizes.  conn: [n_prism][N(p)] int32 node
+ * ids; dirichlet: [n_dof] (1 = node on a face tagged SEM_FACE_DIRICHLET);
+ * owner: [n_prism][N(p)] (1 = first element, in input order, holding the node). */
+int sem_host_numbering(const sem_mesh *mesh, int p, int64_t *n_dof, int64_t *n_free,
+                       int32_t *conn, uint8_t *dirichlet, uint8_t *owner);
+/* Schwarz subdomains of level order p with `overlap` (reading O15): off
+ * [n_prism+1], idx [total] sorted free node ids of each subdomain, W [n_dof]
+ * weights of eq 4.6 (0 on Dirichlet nodes).  Two-call pattern as above. */
+int sem_host_schwarz(const sem_mesh *mesh, int p, int overlap, int64_t *total, int64_t *off,
+                     int32_t *idx, double *W);
+/* Reference operator matrices of order p: B0, Br, Bs [(p+1)^2][Nt] (triangle
+ * basis / d/dr / d/ds at the collapsed cubature), Bt, Dt [p+1][p+1] (1D basis /
+ * derivative at vertical Gauss points), w [(p+1)^3] cubature weights. */
+int sem_host_reference(int p, double *B0, double *Br, double *Bs, double *Bt, double *Dt, double *w);
+const char *sem_strerror(int code);
+/* Message of the last error raised in this thread (more detail than sem_strerror). */
+const char *sem_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEM_PMG_H */

@@ -1,0 +1,304 @@
+"""ctypes marshalling for include/sem_pmg.h (names follow the C ABI)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsem_pmg.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build the CUDA library first "
+                      "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+_lib = C.CDLL(LIB_PATH)
+
+_dp = C.POINTER(C.c_double)
+
+
+class SemMesh(C.Structure):
+    _fields_ = [("n_vert", C.c_int32), ("xyz", _dp), ("n_prism", C.c_int32),
+                ("prism", C.POINTER(C.c_int32)), ("face_tag", C.POINTER(C.c_uint8)),
+                ("node_xyz", _dp)]
+
+
+class SemOpts(C.Structure):
+    _fields_ = [("nu1", C.c_int), ("nu2", C.c_int), ("overlap", C.c_int), ("literal_smoother", C.c_int),
+                ("outer", C.c_int), ("levels", C.POINTER(C.c_int)), ("n_levels", C.c_int),
+                ("atol", C.c_double), ("imax", C.c_int), ("stream", C.c_void_p), ("device", C.c_int),
+                ("verbose", C.c_int)]
+
+
+class SemReport(C.Structure):
+    _fields_ = [("iters", C.c_int), ("vcycles", C.c_int), ("converged", C.c_int), ("rel_res", C.c_double),
+                ("q_mean", C.c_double), ("t_ms", C.c_double), ("norm_f", C.c_double), ("n_hist", C.c_int),
+                ("res_hist", C.c_double * 256)]
+
+    def as_dict(self):
+        return dict(iters=self.iters, vcycles=self.vcycles, converged=bool(self.converged),
+                    rel_res=self.rel_res, q_mean=self.q_mean, t_ms=self.t_ms, norm_f=self.norm_f,
+                    res_hist=list(self.res_hist[: self.n_hist]))
+
+
+class SemInfo(C.Structure):
+    _fields_ = [("n_dof", C.c_int64), ("n_free", C.c_int64), ("n_elem", C.c_int64), ("n_levels", C.c_int),
+                ("level_p", C.c_int * 16), ("level_n_dof", C.c_int64 * 16), ("level_n_free", C.c_int64 * 16),
+                ("schwarz_bytes", C.c_int64 * 16), ("schwarz_nk_sum", C.c_int64 * 16),
+                ("schwarz_packed", C.c_int64 * 16), ("coarse_n", C.c_int64), ("device_bytes", C.c_int64),
+                ("setup_ms", C.c_double)]
+
+
+_vp = C.c_void_p
+_lib.sem_default_opts.argtypes = [C.POINTER(SemOpts)]
+_lib.sem_reference_nodes.argtypes = [C.c_int, _dp]
+_lib.sem_setup.argtypes = [C.POINTER(SemMesh), C.c_int, C.POINTER(SemOpts), C.POINTER(_vp)]
+_lib.sem_get_info.argtypes = [_vp, C.POINTER(SemInfo)]
+_lib.sem_node_xyz.argtypes = [_vp, C.c_int, _vp, C.c_int]
+_lib.sem_dirichlet_mask.argtypes = [_vp, C.c_int, _vp, C.c_int]
+_lib.sem_apply_laplace.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int]
+_lib.pmg_vcycle.argtypes = [_vp, _vp, _vp]
+_lib.laplace_solve.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
+_lib.laplace_solve_host.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
+_lib.sem_prolong.argtypes = [_vp, C.c_int, _vp, _vp]
+_lib.sem_restrict.argtypes = [_vp, C.c_int, _vp, _vp]
+_lib.sem_schwarz.argtypes = [_vp, C.c_int, _vp, _vp, C.c_int]
+_lib.sem_coarse_solve.argtypes = [_vp, _vp, _vp]
+_lib.sem_launch_count.argtypes = [_vp, C.c_int]
+_lib.sem_launch_count.restype = C.c_int64
+_lib.sem_destroy.argtypes = [_vp]
+_lib.sem_strerror.argtypes = [C.c_int]
+_lib.sem_strerror.restype = C.c_char_p
+_lib.sem_last_error.restype = C.c_char_p
+
+_lib.sem_host_numbering.argtypes = [C.POINTER(SemMesh), C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                    _vp, _vp, _vp]
+_lib.sem_host_schwarz.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.POINTER(C.c_int64), _vp, _vp, _vp]
+_lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+
+EXPORTS = ["sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+           "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
+           "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
+           "sem_destroy", "sem_strerror", "sem_last_error"]
+
+SEM_ENOTCONV = -5
+
+
+class SemError(RuntimeError):
+    def __init__(self, code, where):
+        self.code = code
+        super().__init__(f"{where}: {_lib.sem_strerror(code).decode()} ({_lib.sem_last_error().decode()})")
+
+
+def _check(code, where):
+    if code != 0:
+        raise SemError(code, where)
+
+
+def default_opts() -> dict:
+    o = SemOpts()
+    _lib.sem_default_opts(C.byref(o))
+    return {k: getattr(o, k) for k, _ in SemOpts._fields_ if k not in ("levels", "stream")}
+
+
+def reference_nodes(p: int) -> np.ndarray:
+    n = (p + 1) ** 2 * (p + 2) // 2
+    out = np.zeros((n, 3))
+    _check(_lib.sem_reference_nodes(p, out.ctypes.data_as(_dp)), "sem_reference_nodes")
+    return out
+
+
+def _mesh_struct(vertices, prisms, face_tag, node_xyz=None):
+    keep = [np.ascontiguousarray(vertices, dtype=np.float64), np.ascontiguousarray(prisms, dtype=np.int32),
+            np.ascontiguousarray(face_tag, dtype=np.uint8)]
+    m = SemMesh()
+    m.n_vert = keep[0].shape[0]
+    m.xyz = keep[0].ctypes.data_as(_dp)
+    m.n_prism = keep[1].shape[0]
+    m.prism = keep[1].ctypes.data_as(C.POINTER(C.c_int32))
+    m.face_tag = keep[2].ctypes.data_as(C.POINTER(C.c_uint8))
+    if node_xyz is not None:
+        keep.append(np.ascontiguousarray(node_xyz, dtype=np.float64))
+        m.node_xyz = keep[3].ctypes.data_as(_dp)
+    return m, keep
+
+
+def host_numbering(vertices, prisms, face_tag, p):
+    """sem_host_numbering: (conn [E][N], dirichlet [n] bool, owner [E][N] bool)."""
+    m, keep = _mesh_struct(vertices, prisms, face_tag)
+    n, nf = C.c_int64(), C.c_int64()
+    _check(_lib.sem_host_numbering(C.byref(m), p, C.byref(n), C.byref(nf), None, None, None), "sem_host_numbering")
+    E = keep[1].shape[0]
+    N = (p + 1) ** 2 * (p + 2) // 2
+    conn = np.zeros((E, N), dtype=np.int32)
+    dirm = np.zeros(n.value, dtype=np.uint8)
+    own = np.zeros((E, N), dtype=np.uint8)
+    _check(_lib.sem_host_numbering(C.byref(m), p, None, None, C.c_void_p(conn.ctypes.data),
+                                   C.c_void_p(dirm.ctypes.data), C.c_void_p(own.ctypes.data)), "sem_host_numbering")
+    return conn, dirm.astype(bool), own.astype(bool)
+
+
+def host_schwarz(vertices, prisms, face_tag, p, overlap):
+    """sem_host_schwarz: (list of subdomain node arrays, W)."""
+    m, keep = _mesh_struct(vertices, prisms, face_tag)
+    tot = C.c_int64()
+    _check(_lib.sem_host_schwarz(C.byref(m), p, overlap, C.byref(tot), None, None, None), "sem_host_schwarz")
+    E = keep[1].shape[0]
+    conn, dirm, _ = host_numbering(vertices, prisms, face_tag, p)
+    off = np.zeros(E + 1, dtype=np.int64)
+    idx = np.zeros(tot.value, dtype=np.int32)
+    W = np.zeros(dirm.size)
+    _check(_lib.sem_host_schwarz(C.byref(m), p, overlap, None, C.c_void_p(off.ctypes.data),
+                                 C.c_void_p(idx.ctypes.data), C.c_void_p(W.ctypes.data)), "sem_host_schwarz")
+    return [idx[off[k]:off[k + 1]] for k in range(E)], W
+
+
+def host_reference(p):
+    """sem_host_reference: dict of B0, Br, Bs [(p+1)^2][Nt], Bt, Dt [p+1][p+1], w [(p+1)^3]."""
+    nt, qt, n1 = (p + 1) * (p + 2) // 2, (p + 1) ** 2, p + 1
+    out = dict(B0=np.zeros((qt, nt)), Br=np.zeros((qt, nt)), Bs=np.zeros((qt, nt)), Bt=np.zeros((n1, n1)),
+               Dt=np.zeros((n1, n1)), w=np.zeros(qt * n1))
+    _check(_lib.sem_host_reference(p, *[C.c_void_p(out[k].ctypes.data) for k in ("B0", "Br", "Bs", "Bt", "Dt", "w")]),
+           "sem_host_reference")
+    return out
+
+
+def _ptr(t):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError("expected a contiguous CUDA float64 tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+class Solver:
+    """sem_setup(mesh, p) + the compute calls of include/sem_pmg.h."""
+
+    def __init__(self, vertices, prisms, face_tag, p: int, node_xyz=None, *, levels=None, stream=None,
+                 **opts):
+        import torch
+        self._torch = torch
+        o = SemOpts()
+        _lib.sem_default_opts(C.byref(o))
+        for k, v in opts.items():
+            if not hasattr(o, k):
+                raise TypeError(f"unknown option {k}")
+            setattr(o, k, v)
+        self._levels = None
+        if levels is not None:
+            self._levels = (C.c_int * len(levels))(*levels)
+            o.levels = self._levels
+            o.n_levels = len(levels)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        self.stream = stream
+        o.stream = C.c_void_p(stream.cuda_stream)
+        o.device = torch.cuda.current_device() if o.device < 0 else o.device
+        self._keep = [np.ascontiguousarray(vertices, dtype=np.float64),
+                      np.ascontiguousarray(prisms, dtype=np.int32),
+                      np.ascontiguousarray(face_tag, dtype=np.uint8)]
+        m = SemMesh()
+        m.n_vert = self._keep[0].shape[0]
+        m.xyz = self._keep[0].ctypes.data_as(_dp)
+        m.n_prism = self._keep[1].shape[0]
+        m.prism = self._keep[1].ctypes.data_as(C.POINTER(C.c_int32))
+        m.face_tag = self._keep[2].ctypes.data_as(C.POINTER(C.c_uint8))
+        if node_xyz is not None:
+            nx = np.ascontiguousarray(node_xyz, dtype=np.float64)
+            self._keep.append(nx)
+            m.node_xyz = nx.ctypes.data_as(_dp)
+        self._ctx = C.c_void_p()
+        _check(_lib.sem_setup(C.byref(m), p, C.byref(o), C.byref(self._ctx)), "sem_setup")
+        self._keep = None
+        self.p = p
+        inf = SemInfo()
+        _check(_lib.sem_get_info(self._ctx, C.byref(inf)), "sem_get_info")
+        self.info = dict(n_dof=inf.n_dof, n_free=inf.n_free, n_elem=inf.n_elem, n_levels=inf.n_levels,
+                         level_p=list(inf.level_p[: inf.n_levels]),
+                         level_n_dof=list(inf.level_n_dof[: inf.n_levels]),
+                         level_n_free=list(inf.level_n_free[: inf.n_levels]),
+                         schwarz_bytes=list(inf.schwarz_bytes[: inf.n_levels]),
+                         schwarz_nk_sum=list(inf.schwarz_nk_sum[: inf.n_levels]),
+                         schwarz_packed=list(inf.schwarz_packed[: inf.n_levels]),
+                         coarse_n=inf.coarse_n, device_bytes=inf.device_bytes, setup_ms=inf.setup_ms)
+
+    # ---------------------------------------------------------------- helpers
+    def n_dof(self, level=0):
+        return self.info["level_n_dof"][level]
+
+    def empty(self, level=0):
+        return self._torch.zeros(self.n_dof(level), dtype=self._torch.float64, device="cuda")
+
+    def node_xyz(self, level=0) -> np.ndarray:
+        out = np.zeros((self.n_dof(level), 3))
+        _check(_lib.sem_node_xyz(self._ctx, level, C.c_void_p(out.ctypes.data), 0), "sem_node_xyz")
+        return out
+
+    def dirichlet_mask(self, level=0) -> np.ndarray:
+        out = np.zeros(self.n_dof(level), dtype=np.uint8)
+        _check(_lib.sem_dirichlet_mask(self._ctx, level, C.c_void_p(out.ctypes.data), 0), "sem_dirichlet_mask")
+        return out.astype(bool)
+
+    # ---------------------------------------------------------------- compute
+    def apply(self, u, level=0, masked=False, out=None):
+        y = self.empty(level) if out is None else out
+        _check(_lib.sem_apply_laplace(self._ctx, _ptr(u), _ptr(y), level, int(masked)), "sem_apply_laplace")
+        return y
+
+    def vcycle(self, r, out=None):
+        z = self.empty(0) if out is None else out
+        _check(_lib.pmg_vcycle(self._ctx, _ptr(r), _ptr(z)), "pmg_vcycle")
+        return z
+
+    def solve(self, dirichlet_phi, tol, rhs=None, out=None, check=True):
+        phi = self.empty(0) if out is None else out
+        rep = SemReport()
+        code = _lib.laplace_solve(self._ctx, None if rhs is None else _ptr(rhs), _ptr(dirichlet_phi), tol,
+                                  _ptr(phi), C.byref(rep))
+        if check and code not in (0,):
+            raise SemError(code, "laplace_solve")
+        return phi, rep.as_dict()
+
+    def solve_host(self, dirichlet_phi_host, tol, out_host, rhs_host=None):
+        """Host buffers (numpy arrays or pinned CPU tensors), copies inside the call."""
+        def hp(a):
+            if a is None:
+                return None
+            if isinstance(a, np.ndarray):
+                return C.c_void_p(a.ctypes.data)
+            return C.c_void_p(a.data_ptr())
+        rep = SemReport()
+        code = _lib.laplace_solve_host(self._ctx, hp(rhs_host), hp(dirichlet_phi_host), tol, hp(out_host),
+                                       C.byref(rep))
+        if code != 0:
+            raise SemError(code, "laplace_solve_host")
+        return rep.as_dict()
+
+    def prolong(self, level, uc, uf):
+        _check(_lib.sem_prolong(self._ctx, level, _ptr(uc), _ptr(uf)), "sem_prolong")
+        return uf
+
+    def restrict(self, level, rf, out=None):
+        rc = self.empty(level + 1) if out is None else out
+        _check(_lib.sem_restrict(self._ctx, level, _ptr(rf), _ptr(rc)), "sem_restrict")
+        return rc
+
+    def schwarz(self, level, r, u, transpose=False):
+        _check(_lib.sem_schwarz(self._ctx, level, _ptr(r), _ptr(u), int(transpose)), "sem_schwarz")
+        return u
+
+    def coarse_solve(self, r, out=None):
+        z = self.empty(self.info["n_levels"] - 1) if out is None else out
+        _check(_lib.sem_coarse_solve(self._ctx, _ptr(r), _ptr(z)), "sem_coarse_solve")
+        return z
+
+    def launches(self, reset=False) -> int:
+        return int(_lib.sem_launch_count(self._ctx, int(reset)))
+
+    def close(self):
+        if getattr(self, "_ctx", None) is not None and self._ctx.value:
+            _lib.sem_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,864 @@
+// C ABI (include/sem_pmg.h): setup ("pre-compute S^-1 and A on all grids
+// and re-use them"), V-cycle (Alg 4.1), PDC (Alg 4.2), PCG (Alg 4.3).
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace sem;
+
+static thread_local std::string g_last_error;
+
+namespace {
+
+#define CUBLAS_CHECK(x)                                                                  \
+  do {                                                                                   \
+    cublasStatus_t _s = (x);                                                             \
+    if (_s != CUBLAS_STATUS_SUCCESS) throw SemError(SEM_ECUDA, std::string(#x) + " failed"); \
+  } while (0)
+#define CUSOLVER_CHECK(x)                                                                \
+  do {                                                                                   \
+    cusolverStatus_t _s = (x);                                                           \
+    if (_s != CUSOLVER_STATUS_SUCCESS) throw SemError(SEM_ECUDA, std::string(#x) + " failed"); \
+  } while (0)
+
+template <class T>
+T* dalloc(sem_ctx* c, size_t count) {
+  if (count == 0) count = 1;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw SemError(SEM_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+  }
+  c->allocs.push_back(p);
+  c->device_bytes += (int64_t)(count * sizeof(T));
+  return (T*)p;
+}
+
+template <class T>
+T* upload(sem_ctx* c, const std::vector<T>& v) {
+  T* d = dalloc<T>(c, v.size());
+  if (!v.empty()) CUDA_CHECK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+// scratch allocation freed at the end of setup
+struct Scratch {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw SemError(SEM_ENOMEM, "setup scratch cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+    }
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* put(const std::vector<T>& v) {
+    T* d = get<T>(v.size());
+    if (!v.empty()) CUDA_CHECK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  void release(void* p) {
+    auto it = std::find(ptrs.begin(), ptrs.end(), p);
+    if (it != ptrs.end()) { cudaFree(p); ptrs.erase(it); }
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+std::vector<int> schedule_for(int p, const sem_opts& o) {
+  std::vector<int> s;
+  if (o.levels && o.n_levels > 0) {
+    for (int i = 0; i < o.n_levels; ++i) s.push_back(o.levels[i]);
+    if (s[0] != p) throw SemError(SEM_EINVAL, "levels[0] must equal p");
+    for (size_t i = 1; i < s.size(); ++i)
+      if (s[i] >= s[i - 1] || s[i] < 1) throw SemError(SEM_EINVAL, "levels must strictly decrease to >= 1");
+    if (s.back() != 1) throw SemError(SEM_EINVAL, "the coarsest level must be P=1 (P:222-223)");
+    return s;
+  }
+  s.push_back(p);  // P -> ceil((P+1)/2), strict-decrease guard (O18)
+  while (s.back() > 1) {
+    int c = (s.back() + 2) / 2;
+    if (c >= s.back()) c = s.back() - 1;
+    s.push_back(c);
+  }
+  return s;
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------------ Schwarz setup
+void setup_schwarz(sem_ctx* c, int li, const LevelTopo& topo, int overlap, cublasHandle_t blas,
+                   cusolverDnHandle_t sol, const double* d_D, int verbose) {
+  DeviceLevel& L = c->L[li];
+  const int E = c->E;
+  double t0 = now_ms();
+  int nth = std::min(32, std::max(1, omp_get_max_threads()));
+  SchwarzTopo S = schwarz_topology(topo, E, overlap, nth);
+  double t1 = now_ms();
+  // padded index lists and tile offsets
+  std::vector<int64_t> poff(E + 1, 0), toff(E + 1, 0);
+  int maxT = 0;
+  for (int k = 0; k < E; ++k) {
+    int nk = (int)(S.off[k + 1] - S.off[k]);
+    int T = (nk + 15) / 16;
+    maxT = std::max(maxT, T);
+    L.nk_sum += nk;
+    L.packed += (int64_t)nk * (nk + 1) / 2;
+    poff[k + 1] = poff[k] + 16 * (int64_t)T;
+    toff[k + 1] = toff[k] + 256 * (int64_t)T * (T + 1) / 2;
+  }
+  std::vector<int32_t> pidx(poff[E], -1);
+  for (int k = 0; k < E; ++k)
+    std::copy(S.idx.begin() + S.off[k], S.idx.begin() + S.off[k + 1], pidx.begin() + poff[k]);
+  L.max_tiles_1d = maxT;
+  L.schwarz_bytes = toff[E] * 8;
+  size_t freeb = 0, totb = 0;
+  CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
+  const size_t ae_bytes = (size_t)E * L.N * L.N * 8;
+  if ((size_t)L.schwarz_bytes + ae_bytes > freeb * 0.9)
+    throw SemError(SEM_ENOMEM, "dense Schwarz inverses of level p=" + std::to_string(L.p) + " need " +
+                                   std::to_string(L.schwarz_bytes >> 20) + " MiB (+ " + std::to_string(ae_bytes >> 20) +
+                                   " MiB element matrices during setup); reduce overlap");
+  L.sidx = upload(c, pidx);
+  L.sidx_off = upload(c, poff);
+  L.tile_off = upload(c, toff);
+  L.tiles = dalloc<double>(c, (size_t)toff[E]);
+  L.W = upload(c, S.W);
+
+  Scratch sc;
+  const int32_t* d_idx = sc.put(S.idx);
+  const int64_t* d_off = sc.put(S.off);
+  const int32_t* d_el = sc.put(S.elist);
+  const int64_t* d_eoff = sc.put(S.eoff);
+  double* Ae = sc.get<double>((size_t)E * L.N * L.N);
+  launch_elem_matrices(c, li, d_D, Ae, 0, E);
+  const int npad = 16 * maxT;
+  CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
+  size_t per = (size_t)npad * npad * 8 * 2 + 64;
+  size_t nb_max = std::max<size_t>(1, std::min<size_t>((size_t)(freeb * 0.6) / per, 8192));
+  int nb = (int)std::min<size_t>(nb_max, (size_t)E);
+  double* B = sc.get<double>((size_t)nb * npad * npad);
+  double* X = sc.get<double>((size_t)nb * npad * npad);
+  double** dA = sc.get<double*>(nb);
+  double** dX = sc.get<double*>(nb);
+  int* dinfo = sc.get<int>(nb);
+  {
+    std::vector<double*> hA(nb), hX(nb);
+    for (int i = 0; i < nb; ++i) {
+      hA[i] = B + (size_t)i * npad * npad;
+      hX[i] = X + (size_t)i * npad * npad;
+    }
+    CUDA_CHECK(cudaMemcpy(dA, hA.data(), nb * sizeof(double*), cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(dX, hX.data(), nb * sizeof(double*), cudaMemcpyHostToDevice));
+  }
+  const double one = 1.0, zero = 0.0;
+  std::vector<int> hinfo(nb);
+  for (int k0 = 0; k0 < E; k0 += nb) {
+    const int cnt = std::min(nb, E - k0);
+    CUDA_CHECK(cudaMemsetAsync(B, 0, (size_t)cnt * npad * npad * 8, c->stream));
+    launch_assemble_blocks(c, li, d_idx, d_off, d_el, d_eoff, Ae, k0, cnt, npad, B);
+    launch_set_identity(c, X, cnt, npad);  // X <- I for every block
+    CUSOLVER_CHECK(cusolverDnDpotrfBatched(sol, CUBLAS_FILL_MODE_LOWER, npad, dA, npad, dinfo, cnt));
+    CUDA_CHECK(cudaMemcpyAsync(hinfo.data(), dinfo, cnt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < cnt; ++i)
+      if (hinfo[i] != 0)
+        throw SemError(SEM_ESINGULAR, "Schwarz block of element " + std::to_string(k0 + i) + " on level p=" +
+                                          std::to_string(L.p) + " is not SPD (potrf info " + std::to_string(hinfo[i]) +
+                                          ")");
+    // X = L^-1 ; B = X^T X = (L L^T)^-1
+    CUBLAS_CHECK(cublasDtrsmBatched(blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                                    npad, npad, &one, (const double* const*)dA, npad, dX, npad, cnt));
+    CUBLAS_CHECK(cublasDgemmStridedBatched(blas, CUBLAS_OP_T, CUBLAS_OP_N, npad, npad, npad, &one, X, npad,
+                                           (long long)npad * npad, X, npad, (long long)npad * npad, &zero, B, npad,
+                                           (long long)npad * npad, cnt));
+    launch_pack_tiles(c, li, B, k0, cnt, npad, d_off);
+  }
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (verbose)
+    fprintf(stderr, "[sem] level p=%d schwarz: topo %.0f ms, blocks+inverse %.0f ms, max n_k %d, %.1f MiB\n", L.p,
+            t1 - t0, now_ms() - t1, S.max_nk, L.schwarz_bytes / 1048576.0);
+}
+
+// ------------------------------------------------------------------ coarse setup
+void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, const double* d_D) {
+  DeviceLevel& L = c->L.back();
+  const int E = c->E;
+  std::vector<int32_t> cmap(topo.n, -1), fidx;
+  for (int64_t i = 0; i < topo.n; ++i)
+    if (!topo.dir[i]) {
+      cmap[i] = (int32_t)fidx.size();
+      fidx.push_back((int32_t)i);
+    }
+  const int64_t nc = (int64_t)fidx.size();
+  if (nc > 46000)
+    throw SemError(SEM_EUNSUPPORTED, "coarse P=1 problem has " + std::to_string(nc) +
+                                         " free nodes; the dense coarse inverse supports <= 46000 (inner-CG coarse "
+                                         "solve is not built yet)");
+  c->C.nc = nc;
+  c->C.fidx = upload(c, fidx);
+  c->C.x = dalloc<double>(c, nc);
+  c->C.Ainv = dalloc<double>(c, (size_t)nc * nc);
+  if (nc == 0) return;
+  Scratch sc;
+  double* Ae = sc.get<double>((size_t)E * L.N * L.N);
+  launch_elem_matrices(c, (int)c->L.size() - 1, d_D, Ae, 0, E);
+  int32_t* d_cmap = sc.put(cmap);
+  CUDA_CHECK(cudaMemsetAsync(c->C.Ainv, 0, (size_t)nc * nc * 8, c->stream));
+  launch_assemble_coarse(c, Ae, d_cmap, c->C.Ainv, nc);
+  int lwork = 0;
+  CUSOLVER_CHECK(cusolverDnDpotrf_bufferSize(sol, CUBLAS_FILL_MODE_LOWER, (int)nc, c->C.Ainv, (int)nc, &lwork));
+  int lwork2 = 0;
+  CUSOLVER_CHECK(cusolverDnDpotri_bufferSize(sol, CUBLAS_FILL_MODE_LOWER, (int)nc, c->C.Ainv, (int)nc, &lwork2));
+  double* work = sc.get<double>(std::max(lwork, lwork2));
+  int* dinfo = sc.get<int>(1);
+  int hinfo = 0;
+  CUSOLVER_CHECK(cusolverDnDpotrf(sol, CUBLAS_FILL_MODE_LOWER, (int)nc, c->C.Ainv, (int)nc, work, lwork, dinfo));
+  CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (hinfo != 0) throw SemError(SEM_ESINGULAR, "coarse Cholesky failed (info " + std::to_string(hinfo) + ")");
+  CUSOLVER_CHECK(cusolverDnDpotri(sol, CUBLAS_FILL_MODE_LOWER, (int)nc, c->C.Ainv, (int)nc, work, lwork2, dinfo));
+  CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (hinfo != 0) throw SemError(SEM_ESINGULAR, "coarse inverse failed (info " + std::to_string(hinfo) + ")");
+  launch_symmetrize(c, c->C.Ainv, nc);
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+}
+
+void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
+  const double t_start = now_ms();
+  if (!mesh || !mesh->prism || !mesh->face_tag || mesh->n_prism <= 0 || (!mesh->xyz && !mesh->node_xyz))
+    throw SemError(SEM_EINVAL, "mesh arrays missing");
+  if (p < 1 || p > 8) throw SemError(SEM_EINVAL, "order p must be in 1..8");
+  if (opts) c->opts = *opts;
+  else sem_default_opts(&c->opts);
+  const sem_opts& o = c->opts;
+  if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2) throw SemError(SEM_EINVAL, "bad options");
+  if (o.device >= 0) CUDA_CHECK(cudaSetDevice(o.device));
+  CUDA_CHECK(cudaGetDevice(&c->device));
+  c->stream = (cudaStream_t)o.stream;
+  c->E = mesh->n_prism;
+  c->P = p;
+  const int E = c->E;
+  HostMesh hm;
+  hm.nv = mesh->n_vert;
+  hm.E = E;
+  hm.prism.assign(mesh->prism, mesh->prism + (size_t)E * 6);
+  hm.tag.assign(mesh->face_tag, mesh->face_tag + (size_t)E * 5);
+  for (auto v : hm.prism)
+    if (v < 0 || v >= hm.nv) throw SemError(SEM_EINVAL, "prism vertex index out of range");
+  if (mesh->xyz) hm.xyz.assign(mesh->xyz, mesh->xyz + (size_t)hm.nv * 3);
+  const std::vector<int> sched = schedule_for(p, o);
+  const int nl = (int)sched.size();
+  if (nl > 16) throw SemError(SEM_EINVAL, "too many levels");
+  // fine nodal map X [E][N_P][3]
+  const int Nf = n_prism(p);
+  std::vector<double> X((size_t)E * Nf * 3);
+  if (mesh->node_xyz) {
+    std::copy(mesh->node_xyz, mesh->node_xyz + X.size(), X.begin());
+  } else {  // straight-sided: linear wedge map from the 6 vertices
+    std::vector<double> rst = reference_nodes(p);
+#pragma omp parallel for
+    for (int e = 0; e < E; ++e)
+      for (int n = 0; n < Nf; ++n) {
+        const double r = rst[3 * n], s = rst[3 * n + 1], t = rst[3 * n + 2];
+        const double lam[3] = {-(r + s) / 2, (1 + r) / 2, (1 + s) / 2};
+        for (int i = 0; i < 3; ++i) {
+          double x = 0;
+          for (int a = 0; a < 3; ++a) {
+            x += lam[a] * (1 - t) / 2 * hm.xyz[3 * (size_t)hm.prism[(size_t)e * 6 + a] + i];
+            x += lam[a] * (1 + t) / 2 * hm.xyz[3 * (size_t)hm.prism[(size_t)e * 6 + 3 + a] + i];
+          }
+          X[((size_t)e * Nf + n) * 3 + i] = x;
+        }
+      }
+  }
+  double tm = now_ms();
+  Entities ent;
+  if (sched[0] >= 2) ent = build_entities(hm);
+  std::vector<LevelTopo> topo(nl);
+  for (int li = 0; li < nl; ++li) topo[li] = number_level(hm, ent, sched[li]);
+  if (o.verbose) fprintf(stderr, "[sem] numbering %.0f ms\n", now_ms() - tm);
+
+  c->L.resize(nl);
+  cublasHandle_t blas;
+  cusolverDnHandle_t sol;
+  CUBLAS_CHECK(cublasCreate(&blas));
+  CUSOLVER_CHECK(cusolverDnCreate(&sol));
+  struct HG {
+    cublasHandle_t b;
+    cusolverDnHandle_t s;
+    ~HG() {
+      cublasDestroy(b);
+      cusolverDnDestroy(s);
+    }
+  } hg{blas, sol};
+  CUBLAS_CHECK(cublasSetStream(blas, c->stream));
+  CUSOLVER_CHECK(cusolverDnSetStream(sol, c->stream));
+
+  Scratch sc;
+  double* d_X = sc.put(X);
+  for (int li = 0; li < nl; ++li) {
+    DeviceLevel& L = c->L[li];
+    const LevelTopo& T = topo[li];
+    L.p = sched[li];
+    L.ref = make_level_ref(L.p);
+    L.N = L.ref.N;
+    L.Q = L.ref.Q;
+    L.n = T.n;
+    L.nfree = T.nfree;
+    // signed connectivity: Dirichlet nodes as ~gid
+    std::vector<int32_t> sc_conn(T.conn.size());
+    for (size_t t = 0; t < T.conn.size(); ++t) sc_conn[t] = T.dir[T.conn[t]] ? ~T.conn[t] : T.conn[t];
+    L.conn = upload(c, sc_conn);
+    L.owner = upload(c, T.owner);
+    L.dmask = upload(c, T.dir);
+    L.dir_host = T.dir;
+    // reference matrices: B0 Br Bs [qt][ntp], Bt Dt [n1][n1]
+    const LevelRef& R = L.ref;
+    const int ntp = R.nt | 1;
+    std::vector<double> mats((size_t)3 * R.qt * ntp + 2 * R.n1 * R.n1, 0.0);
+    for (int a = 0; a < R.qt; ++a)
+      for (int m = 0; m < R.nt; ++m) {
+        mats[(size_t)0 * R.qt * ntp + a * ntp + m] = R.B0[a * R.nt + m];
+        mats[(size_t)1 * R.qt * ntp + a * ntp + m] = R.Br[a * R.nt + m];
+        mats[(size_t)2 * R.qt * ntp + a * ntp + m] = R.Bs[a * R.nt + m];
+      }
+    for (int i = 0; i < R.n1 * R.n1; ++i) {
+      mats[(size_t)3 * R.qt * ntp + i] = R.Bt[i];
+      mats[(size_t)3 * R.qt * ntp + R.n1 * R.n1 + i] = R.Dt[i];
+    }
+    L.mats = upload(c, mats);
+    // geometric factors from the finest nodal map
+    L.G = dalloc<double>(c, (size_t)E * 6 * L.Q);
+    {
+      Scratch s2;
+      double* d_gm = s2.put(geometry_matrix(p, L.p));
+      double* d_w = s2.put(R.wq);
+      if (launch_geometry(c, li, d_X, d_gm, Nf, d_w)) throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
+    }
+    // node coordinates of this level (fine map evaluated at the level's nodes)
+    L.xyz.assign((size_t)L.n * 3, 0.0);
+    {
+      std::vector<double> It, I1;
+      transfer_matrices(L.p, p, It, I1);  // order-p basis at this level's nodes
+      const int ntl = R.nt, n1l = R.n1, ntf = n_tri(p), n1f = p + 1;
+#pragma omp parallel for
+      for (int e = 0; e < E; ++e)
+        for (int l = 0; l < n1l; ++l)
+          for (int m = 0; m < ntl; ++m) {
+            const int n = m + ntl * l;
+            if (!T.owner[(size_t)e * L.N + n]) continue;
+            double x[3] = {0, 0, 0};
+            for (int lf = 0; lf < n1f; ++lf)
+              for (int mf = 0; mf < ntf; ++mf) {
+                const double w = It[(size_t)m * ntf + mf] * I1[(size_t)l * n1f + lf];
+                if (w == 0.0) continue;
+                const double* Xn = &X[((size_t)e * Nf + mf + ntf * lf) * 3];
+                x[0] += w * Xn[0];
+                x[1] += w * Xn[1];
+                x[2] += w * Xn[2];
+              }
+            const int32_t g = T.conn[(size_t)e * L.N + n];
+            L.xyz[3 * (size_t)g] = x[0];
+            L.xyz[3 * (size_t)g + 1] = x[1];
+            L.xyz[3 * (size_t)g + 2] = x[2];
+          }
+    }
+    if (li + 1 < nl) {
+      std::vector<double> It, I1;
+      transfer_matrices(L.p, sched[li + 1], It, I1);
+      L.Itri = upload(c, It);
+      L.I1 = upload(c, I1);
+    }
+    L.u = dalloc<double>(c, L.n);
+    L.f = dalloc<double>(c, L.n);
+    L.r = dalloc<double>(c, L.n);
+  }
+  sc.release(d_X);
+  // smoothers (all but the coarsest) and the coarse inverse
+  for (int li = 0; li < nl; ++li) {
+    Scratch s2;
+    double* d_D = s2.put(c->L[li].ref.Dfull);
+    if (li + 1 < nl) {
+      int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
+      setup_schwarz(c, li, topo[li], ov, blas, sol, d_D, o.verbose);
+    } else {
+      setup_coarse(c, topo[li], sol, d_D);
+    }
+  }
+  // solver work
+  const int64_t n0 = c->L[0].n;
+  c->pw = dalloc<double>(c, n0);
+  c->qw = dalloc<double>(c, n0);
+  c->zw = dalloc<double>(c, n0);
+  c->bw = dalloc<double>(c, n0);
+  c->xw = dalloc<double>(c, n0);
+  c->host_in = dalloc<double>(c, n0);
+  c->host_in2 = dalloc<double>(c, n0);
+  c->host_out = dalloc<double>(c, n0);
+  c->scal = dalloc<double>(c, 16);
+  CUDA_CHECK(cudaMallocHost(&c->hscal, 16 * sizeof(double)));
+  CUDA_CHECK(cudaEventCreate(&c->ev0));
+  CUDA_CHECK(cudaEventCreate(&c->ev1));
+  CUDA_CHECK(cudaDeviceSynchronize());
+  c->launches = 0;
+  c->setup_ms = now_ms() - t_start;
+  if (o.verbose) fprintf(stderr, "[sem] setup %.0f ms, device %.1f MiB\n", c->setup_ms, c->device_bytes / 1048576.0);
+}
+
+// ------------------------------------------------------------------ V-cycle (Alg 4.1)
+void vcycle(sem_ctx* c, int li, const double* f, double* u) {
+  const int nl = (int)c->L.size();
+  if (li == nl - 1) {  // coarsest: exact solve (O10, O26)
+    launch_coarse(c, f, u);
+    return;
+  }
+  DeviceLevel& L = c->L[li];
+  const sem_opts& o = c->opts;
+  const int post_t = o.literal_smoother ? 0 : 1;
+  CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * L.n, c->stream));
+  // line 1: nu1 pre-smoothing steps u <- u + S^-1 (f - A u)
+  for (int m = 0; m < o.nu1; ++m) {
+    if (m == 0) {
+      launch_schwarz(c, li, f, u, 0);  // u = 0: the residual is f
+    } else {
+      launch_init_masked(c, li, f, L.r, 1);
+      launch_apply(c, li, u, L.r, AP_NEGATE);
+      launch_schwarz(c, li, L.r, u, 0);
+    }
+  }
+  // line 2: r = f - A u
+  launch_init_masked(c, li, f, L.r, 1);
+  if (o.nu1 > 0) launch_apply(c, li, u, L.r, AP_NEGATE);
+  // line 3: restrict; lines 4-6: coarse solve or recursion
+  DeviceLevel& C = c->L[li + 1];
+  launch_restrict(c, li, L.r, C.f);
+  vcycle(c, li + 1, C.f, C.u);
+  // lines 7-8: prolong and correct
+  launch_prolong(c, li, C.u, u);
+  // line 9: nu2 post-smoothing steps with S^-T (reading O14) or S^-1 (literal)
+  for (int m = 0; m < o.nu2; ++m) {
+    launch_init_masked(c, li, f, L.r, 1);
+    launch_apply(c, li, u, L.r, AP_NEGATE);
+    launch_schwarz(c, li, L.r, u, post_t);
+  }
+}
+
+void read_scalars(sem_ctx* c, int n) {
+  CUDA_CHECK(cudaMemcpyAsync(c->hscal, c->scal, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+}
+
+// ------------------------------------------------------------------ solve
+int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
+  if (!phiD || !phi) throw SemError(SEM_EINVAL, "dirichlet_phi and phi are required");
+  if (!(tol >= 0.0)) throw SemError(SEM_EINVAL, "tol must be >= 0");
+  DeviceLevel& L = c->L[0];
+  const sem_opts& o = c->opts;
+  const int64_t n = L.n;
+  sem_report R;
+  memset(&R, 0, sizeof(R));
+  CUDA_CHECK(cudaEventRecord(c->ev0, c->stream));
+  double* u = c->xw;   // free-node iterate
+  double* r = c->bw;   // residual
+  double* p = c->pw;
+  double* q = c->qw;
+  double* z = c->zw;
+  double* sc = c->scal;
+  // lift: v = phi_D on Dirichlet nodes (0 elsewhere), b_F = rhs_F - A_FD phi_D
+  launch_init_masked(c, 0, phiD, q, 0);
+  launch_init_masked(c, 0, rhs, r, 1);
+  launch_apply(c, 0, q, r, AP_GATHER_ALL | AP_NEGATE);
+  CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * n, c->stream));
+  launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 4);
+  read_scalars(c, 5);
+  const double nf = std::sqrt(c->hscal[4]);
+  R.norm_f = nf;
+  const double thresh = tol * nf + o.atol;
+  double rn = nf;
+  R.res_hist[R.n_hist++] = rn;
+  int status = SEM_OK;
+  if (rn <= thresh) {
+    R.converged = 1;
+  } else if (o.outer == 0) {
+    // Alg 4.3: p = V(r); delta = p^T r
+    vcycle(c, 0, r, p);
+    R.vcycles++;
+    int dcur = 0, dnew = 2;
+    launch_dot2(c, n, p, r, nullptr, nullptr, nullptr, sc + dcur);
+    while (R.iters < o.imax) {
+      // q = A p (masked: p is 0 on Dirichlet nodes)
+      CUDA_CHECK(cudaMemsetAsync(q, 0, sizeof(double) * n, c->stream));
+      launch_apply(c, 0, p, q, 0);
+      launch_dot2(c, n, p, q, nullptr, nullptr, nullptr, sc + 1);
+      // alpha = delta / p^T q; u += alpha p; r -= alpha q; ||r||^2
+      launch_axpy_pcg(c, n, u, r, p, q, sc + dcur, sc + 1, sc + 3);
+      R.iters++;
+      read_scalars(c, 4);
+      if (!(c->hscal[1] > 0.0)) {
+        status = SEM_EBREAKDOWN;
+        break;
+      }
+      rn = std::sqrt(c->hscal[3]);
+      if (R.n_hist < 256) R.res_hist[R.n_hist++] = rn;
+      if (rn <= thresh) {
+        R.converged = 1;
+        break;
+      }
+      // z = V(r); beta = z^T r / delta; p = z + beta p; delta = z^T r
+      vcycle(c, 0, r, z);
+      R.vcycles++;
+      launch_dot2(c, n, z, r, nullptr, nullptr, nullptr, sc + dnew);
+      // beta = z^T r / delta
+      launch_xpby(c, n, p, z, sc + dnew, sc + dcur, 0);
+      std::swap(dcur, dnew);
+    }
+  } else {
+    // Alg 4.2 (PDC; reading O13) and stand-alone MG: u <- u - MG(-r) = u + V(r)
+    while (R.iters < o.imax) {
+      vcycle(c, 0, r, z);
+      R.vcycles++;
+      launch_axpy(c, n, 1.0, z, u);
+      // r = b - A u
+      launch_init_masked(c, 0, rhs, r, 1);
+      launch_apply(c, 0, q, r, AP_GATHER_ALL | AP_NEGATE);  // q still holds the lift v
+      launch_apply(c, 0, u, r, AP_NEGATE);
+      R.iters++;
+      launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 3);
+      read_scalars(c, 4);
+      rn = std::sqrt(c->hscal[3]);
+      if (R.n_hist < 256) R.res_hist[R.n_hist++] = rn;
+      if (rn <= thresh) {
+        R.converged = 1;
+        break;
+      }
+    }
+  }
+  launch_combine_phi(c, 0, u, phiD, phi);
+  CUDA_CHECK(cudaEventRecord(c->ev1, c->stream));
+  CUDA_CHECK(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  R.t_ms = ms;
+  R.rel_res = nf > 0 ? rn / nf : 0.0;
+  if (R.n_hist > 1) {
+    const int m = R.n_hist - 1;
+    R.q_mean = std::pow(R.res_hist[m] / R.res_hist[0], 1.0 / m);
+  }
+  if (status == SEM_OK && !R.converged) status = SEM_ENOTCONV;
+  if (rep) *rep = R;
+  return status;
+}
+
+int fail(const SemError& e) {
+  g_last_error = e.what();
+  return e.code;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void sem_default_opts(sem_opts* o) {
+  memset(o, 0, sizeof(*o));
+  o->nu1 = 3;
+  o->nu2 = 3;
+  o->overlap = 1;
+  o->literal_smoother = 0;
+  o->outer = 0;
+  o->levels = nullptr;
+  o->n_levels = 0;
+  o->atol = 0.0;
+  o->imax = 200;
+  o->stream = nullptr;
+  o->device = -1;
+  o->verbose = 0;
+}
+
+int sem_reference_nodes(int p, double* rst) {
+  if (p < 1 || p > 8 || !rst) return SEM_EINVAL;
+  std::vector<double> v = reference_nodes(p);
+  std::copy(v.begin(), v.end(), rst);
+  return SEM_OK;
+}
+
+int sem_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx** out) {
+  if (!out) return SEM_EINVAL;
+  *out = nullptr;
+  sem_ctx* c = new sem_ctx();
+  try {
+    do_setup(mesh, p, opts, c);
+  } catch (const SemError& e) {
+    sem_destroy(c);
+    return fail(e);
+  } catch (const std::exception& e) {
+    sem_destroy(c);
+    g_last_error = e.what();
+    return SEM_EINVAL;
+  }
+  *out = c;
+  return SEM_OK;
+}
+
+int sem_get_info(const sem_ctx* c, sem_info* info) {
+  if (!c || !info) return SEM_EINVAL;
+  memset(info, 0, sizeof(*info));
+  info->n_dof = c->L[0].n;
+  info->n_free = c->L[0].nfree;
+  info->n_elem = c->E;
+  info->n_levels = (int)c->L.size();
+  for (size_t i = 0; i < c->L.size(); ++i) {
+    info->level_p[i] = c->L[i].p;
+    info->level_n_dof[i] = c->L[i].n;
+    info->level_n_free[i] = c->L[i].nfree;
+    info->schwarz_bytes[i] = c->L[i].schwarz_bytes;
+    info->schwarz_nk_sum[i] = c->L[i].nk_sum;
+    info->schwarz_packed[i] = c->L[i].packed;
+  }
+  info->coarse_n = c->C.nc;
+  info->device_bytes = c->device_bytes;
+  info->setup_ms = c->setup_ms;
+  return SEM_OK;
+}
+
+int sem_node_xyz(const sem_ctx* c, int level, double* xyz, int on_device) {
+  if (!c || !xyz || level < 0 || level >= (int)c->L.size()) return SEM_EINVAL;
+  const auto& v = c->L[level].xyz;
+  if (on_device) {
+    if (cudaMemcpy(xyz, v.data(), v.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return SEM_ECUDA;
+  } else {
+    std::copy(v.begin(), v.end(), xyz);
+  }
+  return SEM_OK;
+}
+
+int sem_dirichlet_mask(const sem_ctx* c, int level, uint8_t* mask, int on_device) {
+  if (!c || !mask || level < 0 || level >= (int)c->L.size()) return SEM_EINVAL;
+  const auto& v = c->L[level].dir_host;
+  if (on_device) {
+    if (cudaMemcpy(mask, v.data(), v.size(), cudaMemcpyHostToDevice) != cudaSuccess) return SEM_ECUDA;
+  } else {
+    std::copy(v.begin(), v.end(), mask);
+  }
+  return SEM_OK;
+}
+
+int sem_apply_laplace(sem_ctx* c, const double* u, double* y, int level, int masked) {
+  if (!c || !u || !y || u == y || level < 0 || level >= (int)c->L.size()) return SEM_EINVAL;
+  try {
+    if (masked) {
+      launch_init_masked(c, level, u, y, 0);
+      launch_apply(c, level, u, y, 0);
+    } else {
+      CUDA_CHECK(cudaMemsetAsync(y, 0, sizeof(double) * c->L[level].n, c->stream));
+      launch_apply(c, level, u, y, AP_GATHER_ALL | AP_SCATTER_ALL);
+    }
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int pmg_vcycle(sem_ctx* c, const double* r, double* z) {
+  if (!c || !r || !z || r == z) return SEM_EINVAL;
+  try {
+    vcycle(c, 0, r, z);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int laplace_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
+  if (!c) return SEM_EINVAL;
+  try {
+    return do_solve(c, rhs, phiD, tol, phi, rep);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+}
+
+int laplace_solve_host(sem_ctx* c, const double* rhs_host, const double* phiD_host, double tol, double* phi_host,
+                       sem_report* rep) {
+  if (!c || !phiD_host || !phi_host) return SEM_EINVAL;
+  try {
+    const int64_t n = c->L[0].n;
+    if (rhs_host)
+      CUDA_CHECK(cudaMemcpyAsync(c->host_in2, rhs_host, n * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(c->host_in, phiD_host, n * 8, cudaMemcpyHostToDevice, c->stream));
+    int st = do_solve(c, rhs_host ? c->host_in2 : nullptr, c->host_in, tol, c->host_out, rep);
+    CUDA_CHECK(cudaMemcpyAsync(phi_host, c->host_out, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    return st;
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+}
+
+int sem_prolong(sem_ctx* c, int level, const double* uc, double* uf) {
+  if (!c || !uc || !uf || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
+  try {
+    launch_prolong(c, level, uc, uf);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int sem_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
+  if (!c || !rf || !rc || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
+  try {
+    launch_restrict(c, level, rf, rc);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int sem_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose) {
+  if (!c || !r || !u || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
+  try {
+    launch_schwarz(c, level, r, u, transpose);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
+  if (!c || !r || !z) return SEM_EINVAL;
+  try {
+    launch_coarse(c, r, z);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int64_t sem_launch_count(const sem_ctx* c, int reset) {
+  if (!c) return -1;
+  int64_t v = c->launches;
+  if (reset) const_cast<sem_ctx*>(c)->launches = 0;
+  return v;
+}
+
+void sem_destroy(sem_ctx* c) {
+  if (!c) return;
+  cudaDeviceSynchronize();
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->hscal) cudaFreeHost(c->hscal);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  delete c;
+}
+
+// ---------------------------------------------------------------- host diagnostics
+static HostMesh host_mesh_of(const sem_mesh* mesh) {
+  if (!mesh || !mesh->prism || !mesh->face_tag || mesh->n_prism <= 0) throw SemError(SEM_EINVAL, "mesh arrays missing");
+  HostMesh hm;
+  hm.nv = mesh->n_vert;
+  hm.E = mesh->n_prism;
+  hm.prism.assign(mesh->prism, mesh->prism + (size_t)hm.E * 6);
+  hm.tag.assign(mesh->face_tag, mesh->face_tag + (size_t)hm.E * 5);
+  for (auto v : hm.prism)
+    if (v < 0 || v >= hm.nv) throw SemError(SEM_EINVAL, "prism vertex index out of range");
+  return hm;
+}
+
+int sem_host_numbering(const sem_mesh* mesh, int p, int64_t* n_dof, int64_t* n_free, int32_t* conn,
+                       uint8_t* dirichlet, uint8_t* owner) {
+  if (p < 1 || p > 8) return SEM_EINVAL;
+  try {
+    HostMesh hm = host_mesh_of(mesh);
+    Entities ent;
+    if (p >= 2) ent = build_entities(hm);
+    LevelTopo T = number_level(hm, ent, p);
+    if (n_dof) *n_dof = T.n;
+    if (n_free) *n_free = T.nfree;
+    if (conn) std::copy(T.conn.begin(), T.conn.end(), conn);
+    if (dirichlet) std::copy(T.dir.begin(), T.dir.end(), dirichlet);
+    if (owner) std::copy(T.owner.begin(), T.owner.end(), owner);
+  } catch (const SemError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SEM_EINVAL;
+  }
+  return SEM_OK;
+}
+
+int sem_host_schwarz(const sem_mesh* mesh, int p, int overlap, int64_t* total, int64_t* off, int32_t* idx,
+                     double* W) {
+  if (p < 1 || p > 8 || overlap < 0) return SEM_EINVAL;
+  try {
+    HostMesh hm = host_mesh_of(mesh);
+    Entities ent;
+    if (p >= 2) ent = build_entities(hm);
+    LevelTopo T = number_level(hm, ent, p);
+    SchwarzTopo S = schwarz_topology(T, hm.E, overlap, std::min(32, std::max(1, omp_get_max_threads())));
+    if (total) *total = S.off[hm.E];
+    if (off) std::copy(S.off.begin(), S.off.end(), off);
+    if (idx) std::copy(S.idx.begin(), S.idx.end(), idx);
+    if (W) std::copy(S.W.begin(), S.W.end(), W);
+  } catch (const SemError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SEM_EINVAL;
+  }
+  return SEM_OK;
+}
+
+int sem_host_reference(int p, double* B0, double* Br, double* Bs, double* Bt, double* Dt, double* w) {
+  if (p < 1 || p > 8) return SEM_EINVAL;
+  LevelRef R = make_level_ref(p);
+  if (B0) std::copy(R.B0.begin(), R.B0.end(), B0);
+  if (Br) std::copy(R.Br.begin(), R.Br.end(), Br);
+  if (Bs) std::copy(R.Bs.begin(), R.Bs.end(), Bs);
+  if (Bt) std::copy(R.Bt.begin(), R.Bt.end(), Bt);
+  if (Dt) std::copy(R.Dt.begin(), R.Dt.end(), Dt);
+  if (w) std::copy(R.wq.begin(), R.wq.end(), w);
+  return SEM_OK;
+}
+
+const char* sem_strerror(int code) {
+  switch (code) {
+    case SEM_OK: return "success";
+    case SEM_EINVAL: return "invalid argument";
+    case SEM_EBADELEM: return "invalid element (detJ <= 0)";
+    case SEM_ENOMEM: return "out of device memory";
+    case SEM_ESINGULAR: return "singular Schwarz block or coarse matrix";
+    case SEM_ENOTCONV: return "not converged within imax iterations";
+    case SEM_EBREAKDOWN: return "PCG breakdown (p^T A p <= 0)";
+    case SEM_ECUDA: return "CUDA / cuSOLVER / cuBLAS error";
+    case SEM_ENCCL: return "communication error";
+    case SEM_EUNSUPPORTED: return "unsupported option combination";
+    default: return "unknown error";
+  }
+}
+
+const char* sem_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// Internal structures of the C-ABI library (not installed).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sem_pmg.h"
+#include "refelem.h"
+#include "topology.h"
+
+namespace sem {
+
+struct SemError : std::runtime_error {
+  int code;
+  SemError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_CHECK(x)                                                                          \
+  do {                                                                                         \
+    cudaError_t _e = (x);                                                                      \
+    if (_e != cudaSuccess)                                                                     \
+      throw ::sem::SemError(_e == cudaErrorMemoryAllocation ? SEM_ENOMEM : SEM_ECUDA,          \
+                            std::string(#x) + ": " + cudaGetErrorString(_e));                  \
+  } while (0)
+
+// apply-kernel flags
+enum : int {
+  AP_GATHER_ALL = 1,   // read u on Dirichlet nodes too (else treated as 0)
+  AP_SCATTER_ALL = 2,  // write y on Dirichlet nodes too (else skipped)
+  AP_NEGATE = 4,       // y -= A u instead of y += A u
+};
+
+struct DeviceLevel {
+  int p = 0, N = 0, Q = 0;
+  int64_t n = 0, nfree = 0;
+  LevelRef ref;                 // host copy
+  int32_t* conn = nullptr;      // [E][N], Dirichlet nodes stored as ~gid
+  uint8_t* owner = nullptr;     // [E][N]
+  uint8_t* dmask = nullptr;     // [n]
+  double* G = nullptr;          // [E][6][Q]
+  double* mats = nullptr;       // B0 Br Bs [qt][nt|1], Bt Dt [qv][n1]
+  // Schwarz (not on the coarsest level)
+  int32_t* sidx = nullptr;      // padded to 16 per subdomain, -1 = padding
+  int64_t* sidx_off = nullptr;  // [E+1] (padded offsets)
+  int64_t* tile_off = nullptr;  // [E+1] offsets in doubles into tiles
+  double* tiles = nullptr;
+  double* W = nullptr;          // [n]
+  int64_t schwarz_bytes = 0;
+  int64_t nk_sum = 0, packed = 0;
+  int max_tiles_1d = 0;
+  // transfer from the next coarser level (level+1 -> this)
+  double* Itri = nullptr;       // [ntf][ntc]
+  double* I1 = nullptr;         // [n1f][n1c]
+  // work vectors
+  double *u = nullptr, *f = nullptr, *r = nullptr;
+  std::vector<double> xyz;      // host [n][3]
+  std::vector<uint8_t> dir_host;
+};
+
+struct Coarse {
+  int64_t nc = 0;               // free coarse nodes
+  int32_t* fidx = nullptr;      // [nc] compact -> level gid
+  double* Ainv = nullptr;       // [nc][nc] row-major, symmetric
+  double* x = nullptr;          // [nc] work
+};
+
+}  // namespace sem
+
+struct sem_ctx {
+  sem_opts opts;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int E = 0;
+  int P = 0;
+  std::vector<sem::DeviceLevel> L;
+  sem::Coarse C;
+  double* scal = nullptr;       // device scalars [16]
+  double* hscal = nullptr;      // pinned host scalars [16]
+  double *pw = nullptr, *qw = nullptr, *zw = nullptr, *bw = nullptr, *xw = nullptr;  // solver work
+  double *host_in = nullptr, *host_in2 = nullptr, *host_out = nullptr;               // device staging for *_host
+  int64_t launches = 0;
+  int64_t device_bytes = 0;
+  double setup_ms = 0.0;
+  std::vector<void*> allocs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace sem {
+// kernels.cu launchers (all enqueue on ctx->stream and count launches)
+void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags);
+void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);
+void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose);
+void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc);
+void launch_prolong(sem_ctx* c, int level, const double* uc, double* uf);
+void launch_coarse(sem_ctx* c, const double* r, double* z);
+void launch_dot2(sem_ctx* c, int64_t n, const double* a, const double* b, const double* d, const double* e,
+                 const uint8_t* mask, double* out2);
+void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* p, const double* q,
+                     const double* num, const double* den, double* rr);
+void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den, int mode);
+void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi);
+void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);
+// setup kernels
+int launch_geometry(sem_ctx* c, int level, const double* d_xfine, const double* d_gmat, int Nf, const double* d_w);
+void launch_elem_matrices(sem_ctx* c, int level, const double* d_D, double* Ae, int e0, int ne);
+void launch_assemble_blocks(sem_ctx* c, int level, const int32_t* d_idx, const int64_t* d_off, const int32_t* d_elist,
+                            const int64_t* d_eoff, const double* Ae, int k0, int nb, int npad, double* B);
+void launch_pack_tiles(sem_ctx* c, int level, const double* Binv, int k0, int nb, int npad, const int64_t* d_off);
+void launch_assemble_coarse(sem_ctx* c, const double* Ae, const int32_t* d_cmap, double* A, int64_t nc);
+void launch_symmetrize(sem_ctx* c, double* A, int64_t n);
+void launch_set_identity(sem_ctx* c, double* X, int nb, int npad);
+}  // namespace sem

@@ -1,0 +1,806 @@
+// Device kernels of the hot path (sm_100a, FP64).
+//
+//  k_apply<P>      a2/a3/a4: y (+/-)= sum_e Q_e^T D^T (G (.) D Q_e u), matrix-free
+//                  sum-factorised prism operator (eq 3.8) with
+//                  gather-scatter of shared nodes and Dirichlet mask.
+//  k_schwarz       a5/a6: u += W sum_k R_k^T B_k^-1 R_k r (eq 4.4-4.6),
+//                  packed-symmetric 16x16-tile GEMV per subdomain, HBM streaming.
+//  k_restrict      a7: r_c = P^T r_f (eq 4.3), sum-factorised.
+//  k_prolong       a9: u_f += P u_c, sum-factorised.
+//  k_coarse_gemv   a8: z = A_1^-1 r, dense symmetric inverse.
+//  vector kernels  a11: fused PCG updates and dot products (Alg 4.3).
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace sem {
+
+// ============================================================== operator apply
+template <int P>
+struct AD {
+  static constexpr int N1 = P + 1;
+  static constexpr int NT = N1 * (N1 + 1) / 2;
+  static constexpr int N = NT * N1;
+  static constexpr int QT = N1 * N1;
+  static constexpr int Q = QT * N1;
+  static constexpr int NTP = NT | 1;  // odd row stride: conflict-free strided smem reads
+  static constexpr int N1P = N1 | 1;
+  static constexpr int T = 256;
+  static constexpr int NE = (3 * QT >= T) ? 1 : T / (3 * QT);
+  static constexpr int SM_MATS = 3 * QT * NTP + 2 * N1 * N1;
+  static constexpr int SM_U = NE * N;
+  static constexpr int SM_UU = NE * 3 * QT * N1P;
+  static constexpr int SM_G = NE * 3 * Q;
+  static constexpr int SMEM = (SM_MATS + SM_U + SM_UU + SM_G) * (int)sizeof(double);
+  static constexpr int IT3 = (NE * Q + T - 1) / T;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256) k_apply(int E, const int32_t* __restrict__ conn,
+                                               const double* __restrict__ G, const double* __restrict__ mats,
+                                               const double* __restrict__ u, double* __restrict__ y, int flags) {
+  using D = AD<P>;
+  extern __shared__ double sm[];
+  double* sB0 = sm;
+  double* sBr = sB0 + D::QT * D::NTP;
+  double* sBs = sBr + D::QT * D::NTP;
+  double* sBt = sBs + D::QT * D::NTP;
+  double* sDt = sBt + D::N1 * D::N1;
+  double* su = sm + D::SM_MATS;
+  double* sU = su + D::SM_U;
+  double* sg = sU + D::SM_UU;
+  const int tid = threadIdx.x;
+  const int e0 = blockIdx.x * D::NE;
+
+  for (int i = tid; i < D::SM_MATS; i += D::T) sm[i] = __ldg(mats + i);
+  // gather u_e = Q_e u (Dirichlet entries as 0 unless AP_GATHER_ALL)
+  for (int i = tid; i < D::NE * D::N; i += D::T) {
+    const int e = e0 + i / D::N;
+    double v = 0.0;
+    if (e < E) {
+      const int c = __ldg(conn + (size_t)e * D::N + (i % D::N));
+      if (c >= 0) v = u[c];
+      else if (flags & AP_GATHER_ALL) v = u[~c];
+    }
+    su[i] = v;
+  }
+  // prefetch this thread's geometric factors (consumed in stage 3)
+  double gv[D::IT3][6];
+#pragma unroll
+  for (int k = 0; k < D::IT3; ++k) {
+    const int it = tid + k * D::T;
+    const int e = it / D::Q, q = it % D::Q;
+    if (it < D::NE * D::Q && e0 + e < E) {
+      const double* g = G + (size_t)(e0 + e) * 6 * D::Q + q;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) gv[k][c] = __ldg(g + c * D::Q);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 6; ++c) gv[k][c] = 0.0;
+    }
+  }
+  __syncthreads();
+  // stage 1: triangle contraction  U_c[a][l] = sum_m B_c[a][m] u[m][l]
+  for (int it = tid; it < D::NE * 3 * D::QT; it += D::T) {
+    const int e = it / (3 * D::QT), rem = it % (3 * D::QT), c = rem / D::QT, a = rem % D::QT;
+    const double* B = (c == 0 ? sBr : (c == 1 ? sBs : sB0)) + a * D::NTP;
+    const double* ue = su + e * D::N;
+    double acc[D::N1];
+#pragma unroll
+    for (int l = 0; l < D::N1; ++l) acc[l] = 0.0;
+#pragma unroll 4
+    for (int m = 0; m < D::NT; ++m) {
+      const double b = B[m];
+#pragma unroll
+      for (int l = 0; l < D::N1; ++l) acc[l] = fma(b, ue[m + D::NT * l], acc[l]);
+    }
+    double* o = sU + ((e * 3 + c) * D::QT + a) * D::N1P;
+#pragma unroll
+    for (int l = 0; l < D::N1; ++l) o[l] = acc[l];
+  }
+  __syncthreads();
+  // stage 2: vertical  g_c[a][q] = sum_l M_c[q][l] U_c[a][l]   (M = Bt for r,s; Dt for t)
+  for (int it = tid; it < D::NE * 3 * D::QT; it += D::T) {
+    const int e = it / (3 * D::QT), rem = it % (3 * D::QT), c = rem / D::QT, a = rem % D::QT;
+    const double* row = sU + ((e * 3 + c) * D::QT + a) * D::N1P;
+    double v[D::N1];
+#pragma unroll
+    for (int l = 0; l < D::N1; ++l) v[l] = row[l];
+    const double* M = (c < 2) ? sBt : sDt;
+    double* o = sg + (e * 3 + c) * D::Q + a;
+#pragma unroll
+    for (int q = 0; q < D::N1; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < D::N1; ++l) s = fma(M[q * D::N1 + l], v[l], s);
+      o[q * D::QT] = s;
+    }
+  }
+  __syncthreads();
+  // stage 3: w = G g at every cubature point
+#pragma unroll
+  for (int k = 0; k < D::IT3; ++k) {
+    const int it = tid + k * D::T;
+    if (it < D::NE * D::Q) {
+      const int e = it / D::Q, q = it % D::Q;
+      double* g = sg + e * 3 * D::Q + q;
+      const double gr = g[0], gs = g[D::Q], gt = g[2 * D::Q];
+      g[0] = gv[k][0] * gr + gv[k][1] * gs + gv[k][2] * gt;
+      g[D::Q] = gv[k][1] * gr + gv[k][3] * gs + gv[k][4] * gt;
+      g[2 * D::Q] = gv[k][2] * gr + gv[k][4] * gs + gv[k][5] * gt;
+    }
+  }
+  __syncthreads();
+  // stage 4: vertical transpose  V_c[a][l] = sum_q M_c[q][l] w_c[a][q]
+  for (int it = tid; it < D::NE * 3 * D::QT; it += D::T) {
+    const int e = it / (3 * D::QT), rem = it % (3 * D::QT), c = rem / D::QT, a = rem % D::QT;
+    const double* src = sg + (e * 3 + c) * D::Q + a;
+    double w[D::N1];
+#pragma unroll
+    for (int q = 0; q < D::N1; ++q) w[q] = src[q * D::QT];
+    const double* M = (c < 2) ? sBt : sDt;
+    double* o = sU + ((e * 3 + c) * D::QT + a) * D::N1P;
+#pragma unroll
+    for (int l = 0; l < D::N1; ++l) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < D::N1; ++q) s = fma(M[q * D::N1 + l], w[q], s);
+      o[l] = s;
+    }
+  }
+  __syncthreads();
+  // stage 5: triangle transpose, one partial per gradient component c
+  double* part = sg;  // [3][NE][N]
+  for (int it = tid; it < D::NE * 3 * D::NT; it += D::T) {
+    const int e = it / (3 * D::NT), rem = it % (3 * D::NT), c = rem / D::NT, m = rem % D::NT;
+    const double* B = (c == 0 ? sBr : (c == 1 ? sBs : sB0)) + m;
+    const double* V = sU + (e * 3 + c) * D::QT * D::N1P;
+    double acc[D::N1];
+#pragma unroll
+    for (int l = 0; l < D::N1; ++l) acc[l] = 0.0;
+#pragma unroll 4
+    for (int a = 0; a < D::QT; ++a) {
+      const double b = B[a * D::NTP];
+#pragma unroll
+      for (int l = 0; l < D::N1; ++l) acc[l] = fma(b, V[a * D::N1P + l], acc[l]);
+    }
+    double* o = part + (c * D::NE + e) * D::N + m;
+#pragma unroll
+    for (int l = 0; l < D::N1; ++l) o[D::NT * l] = acc[l];
+  }
+  __syncthreads();
+  // stage 6: scatter-add y = Q_e^T y_e (gather-scatter of shared nodes)
+  const double sgn = (flags & AP_NEGATE) ? -1.0 : 1.0;
+  for (int it = tid; it < D::NE * D::N; it += D::T) {
+    const int e = it / D::N, n = it % D::N;
+    if (e0 + e >= E) continue;
+    const double v = part[(0 * D::NE + e) * D::N + n] + part[(1 * D::NE + e) * D::N + n] +
+                     part[(2 * D::NE + e) * D::N + n];
+    const int c = __ldg(conn + (size_t)(e0 + e) * D::N + n);
+    if (c >= 0) atomicAdd(y + c, sgn * v);
+    else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~c, sgn * v);
+  }
+}
+
+template <int P>
+static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags) {
+  using D = AD<P>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_apply<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
+    attr = true;
+  }
+  const int grid = (c->E + D::NE - 1) / D::NE;
+  k_apply<P><<<grid, D::T, D::SMEM, c->stream>>>(c->E, L.conn, L.G, L.mats, u, y, flags);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
+  const DeviceLevel& L = c->L[level];
+  switch (L.p) {
+    case 1: apply_P<1>(c, L, u, y, flags); break;
+    case 2: apply_P<2>(c, L, u, y, flags); break;
+    case 3: apply_P<3>(c, L, u, y, flags); break;
+    case 4: apply_P<4>(c, L, u, y, flags); break;
+    case 5: apply_P<5>(c, L, u, y, flags); break;
+    case 6: apply_P<6>(c, L, u, y, flags); break;
+    case 7: apply_P<7>(c, L, u, y, flags); break;
+    case 8: apply_P<8>(c, L, u, y, flags); break;
+    default: throw SemError(SEM_EINVAL, "order out of range");
+  }
+  c->launches++;
+}
+
+// ============================================================== masked vector init
+// mode 0: dst = free ? 0 : src     (masked apply: identity rows on Dirichlet nodes)
+// mode 1: dst = free ? src : 0     (residual / RHS restricted to free nodes)
+__global__ void k_init_masked(int64_t n, const uint8_t* __restrict__ dmask, const double* __restrict__ src,
+                              double* __restrict__ dst, int mode) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool dir = dmask[i];
+    double v;
+    if (mode == 0) v = dir ? (src ? src[i] : 0.0) : 0.0;
+    else v = dir ? 0.0 : (src ? src[i] : 0.0);
+    dst[i] = v;
+  }
+}
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode) {
+  const DeviceLevel& L = c->L[level];
+  k_init_masked<<<grid_for(L.n, 256), 256, 0, c->stream>>>(L.n, L.dmask, src, dst, mode);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// ============================================================== Schwarz smoother
+// One CTA (8 warps) per subdomain k.  B_k^-1 is stored as the lower triangle of
+// 16x16 tiles (diagonal tiles full), row-major inside a tile, tiles in order
+// (0,0),(1,0),(1,1),(2,0),...  Each warp streams whole tiles with coalesced
+// 256-byte loads; row sums are reduced with a value-halving shuffle butterfly,
+// column sums (the symmetric half) accumulated per lane; per-warp private
+// accumulators in shared memory avoid atomics.
+__global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sidx, const int64_t* __restrict__ sidx_off,
+                                                 const int64_t* __restrict__ tile_off,
+                                                 const double* __restrict__ tiles, const double* __restrict__ W,
+                                                 const double* __restrict__ r, double* __restrict__ u, int transpose,
+                                                 int npad_max) {
+  extern __shared__ double sm[];
+  double* x = sm;                 // [npad_max]
+  double* yw = sm + npad_max;     // [8][npad_max]
+  const int k = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = sidx_off[k];
+  const int np = (int)(sidx_off[k + 1] - base);
+  const int T = np >> 4;
+  for (int i = tid; i < np; i += 256) {
+    const int g = sidx[base + i];
+    double v = 0.0;
+    if (g >= 0) {
+      v = r[g];
+      if (transpose) v *= W[g];
+    }
+    x[i] = v;
+  }
+  for (int i = tid; i < 8 * np; i += 256) yw[(i / np) * npad_max + (i % np)] = 0.0;
+  __syncthreads();
+  double* y = yw + warp * npad_max;
+  const double* tk = tiles + tile_off[k];
+  const int ntiles = T * (T + 1) / 2;
+  const int r0 = lane >> 4, cc = lane & 15;
+  for (int t = warp; t < ntiles; t += 8) {
+    int I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    while (I * (I + 1) / 2 > t) --I;
+    const int J = t - I * (I + 1) / 2;
+    const double* A = tk + (size_t)t * 256;
+    double a[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) a[m] = __ldg(A + 32 * m + lane);
+    const double xc = x[16 * J + cc];
+    double v[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) v[m] = a[m] * xc;
+    if (I != J) {
+      double col = 0.0;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) col = fma(a[m], x[16 * I + 2 * m + r0], col);
+      col += __shfl_xor_sync(0xffffffffu, col, 16);
+      if (r0 == 0) y[16 * J + cc] += col;
+    }
+    // value-halving butterfly: 8 row partials over the 16 lanes of a half-warp
+    const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+    double k4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double send = b3 ? v[j] : v[j + 4];
+      const double keep = b3 ? v[j + 4] : v[j];
+      k4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    double k2[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double send = b2 ? k4[j] : k4[j + 2];
+      const double keep = b2 ? k4[j + 2] : k4[j];
+      k2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    double k1;
+    {
+      const double send = b1 ? k2[0] : k2[1];
+      const double keep = b1 ? k2[1] : k2[0];
+      k1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    k1 += __shfl_xor_sync(0xffffffffu, k1, 1);
+    if ((lane & 1) == 0) {
+      const int m = (b1 ? 1 : 0) + (b2 ? 2 : 0) + (b3 ? 4 : 0);
+      y[16 * I + 2 * m + r0] += k1;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < np; i += 256) {
+    const int g = sidx[base + i];
+    if (g < 0) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += yw[w * npad_max + i];
+    if (!transpose) s *= W[g];
+    atomicAdd(u + g, s);
+  }
+}
+
+void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose) {
+  const DeviceLevel& L = c->L[level];
+  const int npad = 16 * L.max_tiles_1d;
+  const int smem = 9 * npad * (int)sizeof(double);
+  static int attr_set = 0;
+  if (smem > 48 * 1024 && smem > attr_set) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_schwarz, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = smem;
+  }
+  k_schwarz<<<c->E, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u, transpose, npad);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// ============================================================== transfers
+// Prolongation u_f += P u_c with P evaluated element by element, each fine node
+// written only by its owner element (first element containing it): P[j][i] =
+// N_i^c(x_j^f) exactly as in P:285-291; restriction is its exact transpose.
+__global__ void k_prolong(int E, int ntf, int n1f, int ntc, int n1c, const int32_t* __restrict__ connf,
+                          const uint8_t* __restrict__ owner, const int32_t* __restrict__ connc,
+                          const double* __restrict__ Itri, const double* __restrict__ I1,
+                          const double* __restrict__ uc, double* __restrict__ uf) {
+  extern __shared__ double sm[];
+  const int Nf = ntf * n1f, Nc = ntc * n1c;
+  double* ec = sm;               // [Nc]
+  double* Tm = sm + Nc;          // [ntf][n1c]
+  const int e = blockIdx.x;
+  for (int i = threadIdx.x; i < Nc; i += blockDim.x) {
+    const int g = connc[(size_t)e * Nc + i];
+    ec[i] = (g >= 0) ? uc[g] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ntf * n1c; i += blockDim.x) {
+    const int mf = i / n1c, lc = i % n1c;
+    double s = 0.0;
+    for (int mc = 0; mc < ntc; ++mc) s = fma(Itri[mf * ntc + mc], ec[mc + ntc * lc], s);
+    Tm[i] = s;
+  }
+  __syncthreads();
+  for (int n = threadIdx.x; n < Nf; n += blockDim.x) {
+    if (!owner[(size_t)e * Nf + n]) continue;
+    const int g = connf[(size_t)e * Nf + n];
+    if (g < 0) continue;
+    const int mf = n % ntf, lf = n / ntf;
+    double s = 0.0;
+    for (int lc = 0; lc < n1c; ++lc) s = fma(I1[lf * n1c + lc], Tm[mf * n1c + lc], s);
+    uf[g] += s;
+  }
+}
+
+__global__ void k_restrict(int E, int ntf, int n1f, int ntc, int n1c, const int32_t* __restrict__ connf,
+                           const uint8_t* __restrict__ owner, const int32_t* __restrict__ connc,
+                           const double* __restrict__ Itri, const double* __restrict__ I1,
+                           const double* __restrict__ rf, double* __restrict__ rc) {
+  extern __shared__ double sm[];
+  const int Nf = ntf * n1f, Nc = ntc * n1c;
+  double* xf = sm;               // [Nf]
+  double* S = sm + Nf;           // [ntf][n1c]
+  const int e = blockIdx.x;
+  for (int n = threadIdx.x; n < Nf; n += blockDim.x) {
+    const int g = connf[(size_t)e * Nf + n];
+    xf[n] = (owner[(size_t)e * Nf + n] && g >= 0) ? rf[g] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ntf * n1c; i += blockDim.x) {
+    const int mf = i / n1c, lc = i % n1c;
+    double s = 0.0;
+    for (int lf = 0; lf < n1f; ++lf) s = fma(I1[lf * n1c + lc], xf[mf + ntf * lf], s);
+    S[i] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < Nc; i += blockDim.x) {
+    const int g = connc[(size_t)e * Nc + i];
+    if (g < 0) continue;
+    const int mc = i % ntc, lc = i / ntc;
+    double s = 0.0;
+    for (int mf = 0; mf < ntf; ++mf) s = fma(Itri[mf * ntc + mc], S[mf * n1c + lc], s);
+    atomicAdd(rc + g, s);
+  }
+}
+
+void launch_prolong(sem_ctx* c, int level, const double* uc, double* uf) {
+  const DeviceLevel& F = c->L[level];
+  const DeviceLevel& C = c->L[level + 1];
+  const int smem = (C.N + F.ref.nt * C.ref.n1) * (int)sizeof(double);
+  k_prolong<<<c->E, 128, smem, c->stream>>>(c->E, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
+                                            F.Itri, F.I1, uc, uf);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
+  const DeviceLevel& F = c->L[level];
+  const DeviceLevel& C = c->L[level + 1];
+  CUDA_CHECK(cudaMemsetAsync(rc, 0, sizeof(double) * C.n, c->stream));
+  const int smem = (F.N + F.ref.nt * C.ref.n1) * (int)sizeof(double);
+  k_restrict<<<c->E, 128, smem, c->stream>>>(c->E, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
+                                             F.Itri, F.I1, rf, rc);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// ============================================================== coarse solve
+__global__ void k_gather(int64_t n, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                         double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+// one warp per row of the dense symmetric inverse; z[fidx[i]] = sum_j Ainv[i][j] x[j]
+__global__ void __launch_bounds__(256) k_coarse_gemv(int64_t n, const double* __restrict__ A,
+                                                     const double* __restrict__ x, const int32_t* __restrict__ fidx,
+                                                     double* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const double* a = A + row * n;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t j = lane;
+  for (; j + 96 < n; j += 128) {
+    s0 = fma(__ldg(a + j), __ldg(x + j), s0);
+    s1 = fma(__ldg(a + j + 32), __ldg(x + j + 32), s1);
+    s2 = fma(__ldg(a + j + 64), __ldg(x + j + 64), s2);
+    s3 = fma(__ldg(a + j + 96), __ldg(x + j + 96), s3);
+  }
+  for (; j < n; j += 32) s0 = fma(__ldg(a + j), __ldg(x + j), s0);
+  double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) z[fidx[row]] = s;
+}
+
+void launch_coarse(sem_ctx* c, const double* r, double* z) {
+  const DeviceLevel& L = c->L.back();
+  CUDA_CHECK(cudaMemsetAsync(z, 0, sizeof(double) * L.n, c->stream));
+  k_gather<<<grid_for(c->C.nc, 256), 256, 0, c->stream>>>(c->C.nc, c->C.fidx, r, c->C.x);
+  CUDA_CHECK(cudaGetLastError());
+  k_coarse_gemv<<<(int)((c->C.nc + 7) / 8), 256, 0, c->stream>>>(c->C.nc, c->C.Ainv, c->C.x, c->C.fidx, z);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches += 2;
+}
+
+// ============================================================== vector kernels
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void block_sum2_atomic(double a, double b, double* out0, double* out1) {
+  __shared__ double s0[32], s1[32];
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { s0[w] = a; s1[w] = b; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    a = lane < nw ? s0[lane] : 0.0;
+    b = lane < nw ? s1[lane] : 0.0;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      atomicAdd(out0, a);
+      if (out1) atomicAdd(out1, b);
+    }
+  }
+}
+
+// out2[0] += a.b ; out2[1] += d.e (if d)
+__global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                       const double* __restrict__ d, const double* __restrict__ e, double* out2) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    s0 = fma(a[i], b[i], s0);
+    if (d) s1 = fma(d[i], e[i], s1);
+  }
+  block_sum2_atomic(s0, s1, out2, d ? out2 + 1 : nullptr);
+}
+
+void launch_dot2(sem_ctx* c, int64_t n, const double* a, const double* b, const double* d, const double* e,
+                 const uint8_t*, double* out2) {
+  CUDA_CHECK(cudaMemsetAsync(out2, 0, sizeof(double) * (d ? 2 : 1), c->stream));
+  k_dot2<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, b, d, e, out2);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// alpha = num / den; u += alpha p; r -= alpha q; rr += r.r
+__global__ void k_axpy_pcg(int64_t n, double* __restrict__ u, double* __restrict__ r, const double* __restrict__ p,
+                           const double* __restrict__ q, const double* num, const double* den, double* rr) {
+  const double alpha = *num / *den;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    u[i] = fma(alpha, p[i], u[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  block_sum2_atomic(s, 0.0, rr, nullptr);
+}
+
+void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* p, const double* q,
+                     const double* num, const double* den, double* rr) {
+  CUDA_CHECK(cudaMemsetAsync(rr, 0, sizeof(double), c->stream));
+  k_axpy_pcg<<<grid_for(n, 256), 256, 0, c->stream>>>(n, u, r, p, q, num, den, rr);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// p = z + beta p, beta = num / den   (mode 0); p = z (mode 1)
+__global__ void k_xpby(int64_t n, double* __restrict__ p, const double* __restrict__ z, const double* num,
+                       const double* den, int mode) {
+  const double beta = mode ? 0.0 : *num / *den;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = mode ? z[i] : fma(beta, p[i], z[i]);
+}
+
+void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den,
+                 int mode) {
+  k_xpby<<<grid_for(n, 256), 256, 0, c->stream>>>(n, p, z, num, den, mode);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+__global__ void k_axpy(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y) {
+  k_axpy<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, x, y);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// phi = free ? uF : phiD
+__global__ void k_combine(int64_t n, const uint8_t* __restrict__ dmask, const double* __restrict__ uF,
+                          const double* __restrict__ phiD, double* __restrict__ phi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    phi[i] = dmask[i] ? phiD[i] : uF[i];
+}
+
+void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi) {
+  const DeviceLevel& L = c->L[level];
+  k_combine<<<grid_for(L.n, 256), 256, 0, c->stream>>>(L.n, L.dmask, uF, phiD, phi);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// ============================================================== setup kernels
+// G = w detJ J^-1 J^-T from the finest nodal map (O-5, O7); J[i][c] = dx_i/dxi_c.
+__global__ void k_geometry(int E, int Nf, int Q, const double* __restrict__ X, const double* __restrict__ gm,
+                           const double* __restrict__ w, double* __restrict__ G, int* bad) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)E * Q) return;
+  const int64_t e = idx / Q;
+  const int q = (int)(idx % Q);
+  double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  const double* Xe = X + e * Nf * 3;
+  for (int n = 0; n < Nf; ++n) {
+    const double dr = gm[((int64_t)n * 3 + 0) * Q + q];
+    const double ds = gm[((int64_t)n * 3 + 1) * Q + q];
+    const double dt = gm[((int64_t)n * 3 + 2) * Q + q];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double xi = Xe[n * 3 + i];
+      J[i][0] = fma(xi, dr, J[i][0]);
+      J[i][1] = fma(xi, ds, J[i][1]);
+      J[i][2] = fma(xi, dt, J[i][2]);
+    }
+  }
+  const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                     J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                     J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+  if (!(det > 0.0)) atomicExch(bad, 1);
+  double Ji[3][3];
+  const double id = 1.0 / det;
+  Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
+  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+  Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
+  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+  Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
+  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+  const double s = w[q] * det;
+  double g[6];
+  int k = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = a; b < 3; ++b) {
+      g[k++] = s * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+    }
+  for (int c2 = 0; c2 < 6; ++c2) G[(e * 6 + c2) * Q + q] = g[c2];
+}
+
+int launch_geometry(sem_ctx* c, int level, const double* X, const double* gm, int Nf, const double* w) {
+  DeviceLevel& L = c->L[level];
+  int* bad;
+  CUDA_CHECK(cudaMalloc(&bad, sizeof(int)));
+  CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+  const int64_t tot = (int64_t)c->E * L.Q;
+  k_geometry<<<(int)((tot + 127) / 128), 128, 0, c->stream>>>(c->E, Nf, L.Q, X, gm, w, L.G, bad);
+  CUDA_CHECK(cudaGetLastError());
+  int hb = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  CUDA_CHECK(cudaFree(bad));
+  return hb;
+}
+
+// Ae[e][i][j] = sum_q sum_cd D_c[q][i] G_cd[e][q] D_d[q][j]   (setup only)
+__global__ void k_elem_matrices(int e0, int ne, int N, int Q, const double* __restrict__ D,
+                                const double* __restrict__ G, double* __restrict__ Ae) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t NN = (int64_t)N * N;
+  if (idx >= (int64_t)ne * NN) return;
+  const int64_t le = idx / NN;
+  const int i = (int)((idx % NN) / N), j = (int)(idx % N);
+  const double* g = G + (e0 + le) * 6 * Q;
+  double s = 0.0;
+  for (int q = 0; q < Q; ++q) {
+    const double ri = D[(0 * Q + q) * N + i], si = D[(1 * Q + q) * N + i], ti = D[(2 * Q + q) * N + i];
+    const double rj = D[(0 * Q + q) * N + j], sj = D[(1 * Q + q) * N + j], tj = D[(2 * Q + q) * N + j];
+    const double gxx = g[0 * Q + q], gxy = g[1 * Q + q], gxz = g[2 * Q + q];
+    const double gyy = g[3 * Q + q], gyz = g[4 * Q + q], gzz = g[5 * Q + q];
+    s += ri * (gxx * rj + gxy * sj + gxz * tj) + si * (gxy * rj + gyy * sj + gyz * tj) +
+         ti * (gxz * rj + gyz * sj + gzz * tj);
+  }
+  Ae[idx] = s;
+}
+
+void launch_elem_matrices(sem_ctx* c, int level, const double* D, double* Ae, int e0, int ne) {
+  const DeviceLevel& L = c->L[level];
+  const int64_t tot = (int64_t)ne * L.N * L.N;
+  k_elem_matrices<<<(int)((tot + 255) / 256), 256, 0, c->stream>>>(e0, ne, L.N, L.Q, D, L.G, Ae);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// B_k = R_k A R_k^T from element matrices (principal submatrix of the assembled,
+// Dirichlet-eliminated A on subdomain k); padded to npad with the identity.
+__global__ void k_assemble_blocks(int N, const int32_t* __restrict__ conn, const int32_t* __restrict__ idx,
+                                  const int64_t* __restrict__ off, const int32_t* __restrict__ elist,
+                                  const int64_t* __restrict__ eoff, const double* __restrict__ Ae, int k0,
+                                  int npad, double* __restrict__ B) {
+  extern __shared__ int ism[];
+  int* sidx = ism;              // [npad]
+  int* pos = ism + npad;        // [N]
+  int* loc = pos + N;           // [N]
+  __shared__ int nloc;
+  const int k = k0 + blockIdx.x;
+  const int64_t o = off[k];
+  const int nk = (int)(off[k + 1] - o);
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) sidx[i] = idx[o + i];
+  double* Bk = B + (size_t)blockIdx.x * npad * npad;
+  for (int i = nk + threadIdx.x; i < npad; i += blockDim.x) Bk[(size_t)i * npad + i] = 1.0;
+  __syncthreads();
+  for (int64_t t = eoff[k]; t < eoff[k + 1]; ++t) {
+    const int e = elist[t];
+    if (threadIdx.x == 0) nloc = 0;
+    __syncthreads();
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const int c = conn[(size_t)e * N + n];
+      int p = -1;
+      if (c >= 0) {
+        int lo = 0, hi = nk - 1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          const int v = sidx[mid];
+          if (v == c) { p = mid; break; }
+          if (v < c) lo = mid + 1; else hi = mid - 1;
+        }
+      }
+      pos[n] = p;
+      if (p >= 0) loc[atomicAdd(&nloc, 1)] = n;
+    }
+    __syncthreads();
+    const int nl = nloc;
+    const double* A = Ae + (size_t)e * N * N;
+    for (int pr = threadIdx.x; pr < nl * nl; pr += blockDim.x) {
+      const int i = loc[pr / nl], j = loc[pr % nl];
+      Bk[(size_t)pos[i] * npad + pos[j]] += A[(size_t)i * N + j];
+    }
+    __syncthreads();
+  }
+}
+
+void launch_assemble_blocks(sem_ctx* c, int level, const int32_t* idx, const int64_t* off, const int32_t* elist,
+                            const int64_t* eoff, const double* Ae, int k0, int nb, int npad, double* B) {
+  const DeviceLevel& L = c->L[level];
+  const int smem = (npad + 2 * L.N) * (int)sizeof(int);
+  k_assemble_blocks<<<nb, 256, smem, c->stream>>>(L.N, L.conn, idx, off, elist, eoff, Ae, k0, npad, B);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// copy the lower 16x16 tiles of each inverse (full npad x npad, symmetric) into
+// the streaming layout; entries beyond n_k are zeroed.
+__global__ void k_pack_tiles(const double* __restrict__ Binv, int k0, int npad, const int64_t* __restrict__ off,
+                             const int64_t* __restrict__ tile_off, double* __restrict__ tiles) {
+  const int k = k0 + blockIdx.x;
+  const int nk = (int)(off[k + 1] - off[k]);
+  const int T = (nk + 15) / 16;
+  const double* B = Binv + (size_t)blockIdx.x * npad * npad;
+  double* out = tiles + tile_off[k];
+  const int ntiles = T * (T + 1) / 2;
+  for (int64_t x = threadIdx.x; x < (int64_t)ntiles * 256; x += blockDim.x) {
+    const int t = (int)(x / 256), rc = (int)(x % 256), r = rc / 16, cc = rc % 16;
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    const int J = t - I * (I + 1) / 2;
+    const int gi = 16 * I + r, gj = 16 * J + cc;
+    out[x] = (gi < nk && gj < nk) ? B[(size_t)gi * npad + gj] : 0.0;
+  }
+}
+
+void launch_pack_tiles(sem_ctx* c, int level, const double* Binv, int k0, int nb, int npad, const int64_t* off) {
+  const DeviceLevel& L = c->L[level];
+  k_pack_tiles<<<nb, 256, 0, c->stream>>>(Binv, k0, npad, off, L.tile_off, L.tiles);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void k_set_identity(double* X, int nb, int npad) {
+  const int64_t tot = (int64_t)nb * npad * npad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i % ((int64_t)npad * npad);
+    X[i] = (w / npad == w % npad) ? 1.0 : 0.0;
+  }
+}
+
+void launch_set_identity(sem_ctx* c, double* X, int nb, int npad) {
+  k_set_identity<<<148 * 16, 256, 0, c->stream>>>(X, nb, npad);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// dense free-free coarse matrix from P=1 element matrices
+__global__ void k_assemble_coarse(int E, int N, const int32_t* __restrict__ conn, const int32_t* __restrict__ cmap,
+                                  const double* __restrict__ Ae, double* __restrict__ A, int64_t nc) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t NN = (int64_t)N * N;
+  if (idx >= (int64_t)E * NN) return;
+  const int64_t e = idx / NN;
+  const int i = (int)((idx % NN) / N), j = (int)(idx % N);
+  const int ci = conn[e * N + i], cj = conn[e * N + j];
+  if (ci < 0 || cj < 0) return;
+  atomicAdd(A + (int64_t)cmap[ci] * nc + cmap[cj], Ae[idx]);
+}
+
+void launch_assemble_coarse(sem_ctx* c, const double* Ae, const int32_t* cmap, double* A, int64_t nc) {
+  const DeviceLevel& L = c->L.back();
+  const int64_t tot = (int64_t)c->E * L.N * L.N;
+  k_assemble_coarse<<<(int)((tot + 255) / 256), 256, 0, c->stream>>>(c->E, L.N, L.conn, cmap, Ae, A, nc);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// copy the lower triangle (column-major potri output) to the upper one
+__global__ void k_symmetrize(double* A, int64_t n) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * n) return;
+  const int64_t i = idx / n, j = idx % n;  // row-major (i, j) = column-major (j, i)
+  // potri (column-major, lower) wrote the row-major upper triangle; mirror it
+  if (i > j) A[idx] = A[j * n + i];
+}
+
+void launch_symmetrize(sem_ctx* c, double* A, int64_t n) {
+  k_symmetrize<<<(int)((n * n + 255) / 256), 256, 0, c->stream>>>(A, n);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace sem
