@@ -86,6 +86,8 @@ typedef struct {
   void *stream;               /* cudaStream_t for every kernel; NULL = default stream               */
   int device;                 /* CUDA device ordinal used by sem_setup (default: current device)    */
   int verbose;                /* 1: setup timings to stderr                                         */
+  int apply_kernel;           /* operator kernel: 0 (default) FP64 tensor-core (DMMA) sum factorisation,
+                                 1 CUDA-core FMA sum factorisation (same arithmetic, reference variant) */
 } sem_opts;
 
 typedef struct {

@@ -25,7 +25,7 @@ class SemOpts(C.Structure):
     _fields_ = [("nu1", C.c_int), ("nu2", C.c_int), ("overlap", C.c_int), ("literal_smoother", C.c_int),
                 ("outer", C.c_int), ("levels", C.POINTER(C.c_int)), ("n_levels", C.c_int),
                 ("atol", C.c_double), ("imax", C.c_int), ("stream", C.c_void_p), ("device", C.c_int),
-                ("verbose", C.c_int)]
+                ("verbose", C.c_int), ("apply_kernel", C.c_int)]
 
 
 class SemReport(C.Structure):

@@ -5,7 +5,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = ["csrc/refelem.cpp", "csrc/topology.cpp", "csrc/kernels.cu", "csrc/capi.cu"]
+SRC = ["csrc/refelem.cpp", "csrc/topology.cpp", "csrc/kernels.cu", "csrc/apply_dmma.cu", "csrc/capi.cu"]
 LIB = os.path.join(HERE, "libsem_pmg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

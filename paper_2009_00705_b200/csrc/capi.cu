@@ -253,7 +253,9 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   if (opts) c->opts = *opts;
   else sem_default_opts(&c->opts);
   const sem_opts& o = c->opts;
-  if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2) throw SemError(SEM_EINVAL, "bad options");
+  if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
+      o.apply_kernel > 1)
+    throw SemError(SEM_EINVAL, "bad options");
   if (o.device >= 0) CUDA_CHECK(cudaSetDevice(o.device));
   CUDA_CHECK(cudaGetDevice(&c->device));
   c->stream = (cudaStream_t)o.stream;
@@ -349,6 +351,7 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
       mats[(size_t)3 * R.qt * ntp + R.n1 * R.n1 + i] = R.Dt[i];
     }
     L.mats = upload(c, mats);
+    L.frag = upload(c, dmma_fragments(R));
     // geometric factors from the finest nodal map
     L.G = dalloc<double>(c, (size_t)E * 6 * L.Q);
     {
@@ -595,6 +598,7 @@ void sem_default_opts(sem_opts* o) {
   o->stream = nullptr;
   o->device = -1;
   o->verbose = 0;
+  o->apply_kernel = 0;
 }
 
 int sem_reference_nodes(int p, double* rst) {

@@ -42,6 +42,7 @@ struct DeviceLevel {
   uint8_t* dmask = nullptr;     // [n]
   double* G = nullptr;          // [E][6][Q]
   double* mats = nullptr;       // B0 Br Bs [qt][nt|1], Bt Dt [qv][n1]
+  double* frag = nullptr;       // DMMA fragment-ordered reference operands (apply_dmma.cu)
   // Schwarz (not on the coarsest level)
   int32_t* sidx = nullptr;      // padded to 16 per subdomain, -1 = padding
   int64_t* sidx_off = nullptr;  // [E+1] (padded offsets)
@@ -91,6 +92,8 @@ struct sem_ctx {
 namespace sem {
 // kernels.cu launchers (all enqueue on ctx->stream and count launches)
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags);
+void launch_apply_dmma(sem_ctx* c, int level, const double* u, double* y, int flags);
+std::vector<double> dmma_fragments(const LevelRef& R);
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);
 void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose);
 void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc);

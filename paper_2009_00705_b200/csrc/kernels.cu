@@ -196,6 +196,10 @@ static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y
 }
 
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
+  if (c->opts.apply_kernel == 0) {
+    launch_apply_dmma(c, level, u, y, flags);
+    return;
+  }
   const DeviceLevel& L = c->L[level];
   switch (L.p) {
     case 1: apply_P<1>(c, L, u, y, flags); break;
