@@ -88,6 +88,11 @@ typedef struct {
   int verbose;                /* 1: setup timings to stderr                                         */
   int apply_kernel;           /* operator kernel: 0 (default) FP64 tensor-core (DMMA) sum factorisation,
                                  1 CUDA-core FMA sum factorisation (same arithmetic, reference variant) */
+  int coarse_solver;          /* P=1 solve (reading O9): 0 auto (dense inverse if <= 46,000 free
+                                 nodes, else iterative), 1 iterative (Jacobi-PCG, the outer PCG becomes
+                                 flexible), 2 dense                                                  */
+  double coarse_rtol;         /* relative tolerance of the iterative coarse solve, default 1e-10      */
+  int coarse_maxit;           /* iteration cap of the iterative coarse solve, default 20000           */
 } sem_opts;
 
 typedef struct {
@@ -98,6 +103,7 @@ typedef struct {
   double q_mean;              /* geometric mean of q = ||r^m||/||r^m-1|| (eq 4.7; O22)        */
   double t_ms;                /* device time of the solve (CUDA events)                             */
   double norm_f;              /* ||b_F||_2                                                           */
+  int coarse_iters;           /* inner coarse-solve iterations in this solve (iterative coarse path)  */
   int n_hist;                 /* entries of res_hist used                                            */
   double res_hist[256];       /* ||r^m||_2, m = 0..iters                                            */
 } sem_report;

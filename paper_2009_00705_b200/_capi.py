@@ -25,17 +25,20 @@ class SemOpts(C.Structure):
     _fields_ = [("nu1", C.c_int), ("nu2", C.c_int), ("overlap", C.c_int), ("literal_smoother", C.c_int),
                 ("outer", C.c_int), ("levels", C.POINTER(C.c_int)), ("n_levels", C.c_int),
                 ("atol", C.c_double), ("imax", C.c_int), ("stream", C.c_void_p), ("device", C.c_int),
-                ("verbose", C.c_int), ("apply_kernel", C.c_int)]
+                ("verbose", C.c_int), ("apply_kernel", C.c_int), ("coarse_solver", C.c_int),
+                ("coarse_rtol", C.c_double), ("coarse_maxit", C.c_int)]
 
 
 class SemReport(C.Structure):
     _fields_ = [("iters", C.c_int), ("vcycles", C.c_int), ("converged", C.c_int), ("rel_res", C.c_double),
-                ("q_mean", C.c_double), ("t_ms", C.c_double), ("norm_f", C.c_double), ("n_hist", C.c_int),
+                ("q_mean", C.c_double), ("t_ms", C.c_double), ("norm_f", C.c_double), ("coarse_iters", C.c_int),
+                ("n_hist", C.c_int),
                 ("res_hist", C.c_double * 256)]
 
     def as_dict(self):
         return dict(iters=self.iters, vcycles=self.vcycles, converged=bool(self.converged),
                     rel_res=self.rel_res, q_mean=self.q_mean, t_ms=self.t_ms, norm_f=self.norm_f,
+                    coarse_iters=self.coarse_iters,
                     res_hist=list(self.res_hist[: self.n_hist]))
 
 

@@ -134,11 +134,10 @@ void setup_schwarz(sem_ctx* c, int li, const LevelTopo& topo, int overlap, cubla
   L.schwarz_bytes = toff[E] * 8;
   size_t freeb = 0, totb = 0;
   CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
-  const size_t ae_bytes = (size_t)E * L.N * L.N * 8;
-  if ((size_t)L.schwarz_bytes + ae_bytes > freeb * 0.9)
+  if ((size_t)L.schwarz_bytes > freeb * 0.92)
     throw SemError(SEM_ENOMEM, "dense Schwarz inverses of level p=" + std::to_string(L.p) + " need " +
-                                   std::to_string(L.schwarz_bytes >> 20) + " MiB (+ " + std::to_string(ae_bytes >> 20) +
-                                   " MiB element matrices during setup); reduce overlap");
+                                   std::to_string(L.schwarz_bytes >> 20) + " MiB of " + std::to_string(freeb >> 20) +
+                                   " MiB free; reduce overlap (0 = block Jacobi)");
   L.sidx = upload(c, pidx);
   L.sidx_off = upload(c, poff);
   L.tile_off = upload(c, toff);
@@ -150,9 +149,16 @@ void setup_schwarz(sem_ctx* c, int li, const LevelTopo& topo, int overlap, cubla
   const int64_t* d_off = sc.put(S.off);
   const int32_t* d_el = sc.put(S.elist);
   const int64_t* d_eoff = sc.put(S.eoff);
-  double* Ae = sc.get<double>((size_t)E * L.N * L.N);
-  launch_elem_matrices(c, li, d_D, Ae, 0, E);
   const int npad = 16 * maxT;
+  CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
+  // element matrices are formed per chunk of subdomains, only for the element
+  // range the chunk's subdomains touch (keeps setup memory bounded)
+  const size_t ae_elem = (size_t)L.N * L.N * 8;
+  int64_t max_range = 1;
+  for (int k = 0; k < E; ++k)
+    max_range = std::max<int64_t>(max_range, S.elist[S.eoff[k + 1] - 1] - S.elist[S.eoff[k]] + 1);
+  int64_t cap = std::min<int64_t>(E, std::max<int64_t>((int64_t)(freeb * 0.25 / ae_elem), max_range));
+  double* Ae = sc.get<double>((size_t)cap * L.N * L.N);
   CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
   size_t per = (size_t)npad * npad * 8 * 2 + 64;
   size_t nb_max = std::max<size_t>(1, std::min<size_t>((size_t)(freeb * 0.6) / per, 8192));
@@ -173,10 +179,21 @@ void setup_schwarz(sem_ctx* c, int li, const LevelTopo& topo, int overlap, cubla
   }
   const double one = 1.0, zero = 0.0;
   std::vector<int> hinfo(nb);
-  for (int k0 = 0; k0 < E; k0 += nb) {
-    const int cnt = std::min(nb, E - k0);
+  for (int k0 = 0; k0 < E;) {
+    int cnt = 0;
+    int64_t emin = INT64_MAX, emax = -1;
+    while (k0 + cnt < E && cnt < nb) {
+      const int k = k0 + cnt;
+      const int64_t lo = std::min<int64_t>(emin, S.elist[S.eoff[k]]);
+      const int64_t hi = std::max<int64_t>(emax, S.elist[S.eoff[k + 1] - 1]);
+      if (cnt > 0 && hi - lo + 1 > cap) break;
+      emin = lo;
+      emax = hi;
+      ++cnt;
+    }
+    launch_elem_matrices(c, li, d_D, Ae, (int)emin, (int)(emax - emin + 1));
     CUDA_CHECK(cudaMemsetAsync(B, 0, (size_t)cnt * npad * npad * 8, c->stream));
-    launch_assemble_blocks(c, li, d_idx, d_off, d_el, d_eoff, Ae, k0, cnt, npad, B);
+    launch_assemble_blocks(c, li, d_idx, d_off, d_el, d_eoff, Ae, (int)emin, k0, cnt, npad, B);
     launch_set_identity(c, X, cnt, npad);  // X <- I for every block
     CUSOLVER_CHECK(cusolverDnDpotrfBatched(sol, CUBLAS_FILL_MODE_LOWER, npad, dA, npad, dinfo, cnt));
     CUDA_CHECK(cudaMemcpyAsync(hinfo.data(), dinfo, cnt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -193,6 +210,7 @@ void setup_schwarz(sem_ctx* c, int li, const LevelTopo& topo, int overlap, cubla
                                            (long long)npad * npad, X, npad, (long long)npad * npad, &zero, B, npad,
                                            (long long)npad * npad, cnt));
     launch_pack_tiles(c, li, B, k0, cnt, npad, d_off);
+    k0 += cnt;
   }
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
   if (verbose)
@@ -211,10 +229,32 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
       fidx.push_back((int32_t)i);
     }
   const int64_t nc = (int64_t)fidx.size();
-  if (nc > 46000)
-    throw SemError(SEM_EUNSUPPORTED, "coarse P=1 problem has " + std::to_string(nc) +
-                                         " free nodes; the dense coarse inverse supports <= 46000 (inner-CG coarse "
-                                         "solve is not built yet)");
+  const int mode = c->opts.coarse_solver;
+  const bool dense = (mode == 2) || (mode == 0 && nc <= 46000);
+  if (mode == 2 && nc > 46000)
+    throw SemError(SEM_EUNSUPPORTED, "dense coarse inverse requested for " + std::to_string(nc) +
+                                         " free P=1 nodes (limit 46000); use coarse_solver = 0 or 1");
+  if (!dense) {  // Jacobi-preconditioned CG on the matrix-free P=1 operator (reading O9)
+    c->C.iterative = 1;
+    c->C.nc = nc;
+    c->C.dinv = dalloc<double>(c, L.n);
+    c->C.r = dalloc<double>(c, L.n);
+    c->C.z = dalloc<double>(c, L.n);
+    c->C.p = dalloc<double>(c, L.n);
+    c->C.q = dalloc<double>(c, L.n);
+    CUDA_CHECK(cudaMemsetAsync(c->C.dinv, 0, sizeof(double) * L.n, c->stream));
+    Scratch sc;
+    const int64_t chunk = std::min<int64_t>(E, 1 << 20);
+    double* Ae = sc.get<double>((size_t)chunk * L.N * L.N);
+    for (int64_t e0 = 0; e0 < E; e0 += chunk) {
+      const int ne = (int)std::min<int64_t>(chunk, E - e0);
+      launch_elem_matrices(c, (int)c->L.size() - 1, d_D, Ae, (int)e0, ne);
+      launch_diag_accum_range(c, L.conn + (size_t)e0 * L.N, L.N, ne, Ae, c->C.dinv);
+    }
+    launch_invert_masked(c, (int)c->L.size() - 1, c->C.dinv);
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    return;
+  }
   c->C.nc = nc;
   c->C.fidx = upload(c, fidx);
   c->C.x = dalloc<double>(c, nc);
@@ -254,7 +294,7 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   else sem_default_opts(&c->opts);
   const sem_opts& o = c->opts;
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
-      o.apply_kernel > 1)
+      o.apply_kernel > 1 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) || o.coarse_maxit < 1)
     throw SemError(SEM_EINVAL, "bad options");
   if (o.device >= 0) CUDA_CHECK(cudaSetDevice(o.device));
   CUDA_CHECK(cudaGetDevice(&c->device));
@@ -420,8 +460,9 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   c->host_in = dalloc<double>(c, n0);
   c->host_in2 = dalloc<double>(c, n0);
   c->host_out = dalloc<double>(c, n0);
-  c->scal = dalloc<double>(c, 16);
-  CUDA_CHECK(cudaMallocHost(&c->hscal, 16 * sizeof(double)));
+  c->scal = dalloc<double>(c, 32);
+  c->rw_old = dalloc<double>(c, n0);
+  CUDA_CHECK(cudaMallocHost(&c->hscal, 32 * sizeof(double)));
   CUDA_CHECK(cudaEventCreate(&c->ev0));
   CUDA_CHECK(cudaEventCreate(&c->ev1));
   CUDA_CHECK(cudaDeviceSynchronize());
@@ -430,11 +471,55 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   if (o.verbose) fprintf(stderr, "[sem] setup %.0f ms, device %.1f MiB\n", c->setup_ms, c->device_bytes / 1048576.0);
 }
 
+void read_scalars(sem_ctx* c, int n);
+
+// ------------------------------------------------------------------ iterative coarse solve
+// x = A_1^-1 b on the free nodes of the coarsest level by Jacobi-preconditioned CG
+// from x = 0 to ||r|| <= coarse_rtol ||b|| (reading O9).  Convergence is checked
+// every 8 iterations (one host sync each).
+void coarse_pcg(sem_ctx* c, const double* b, double* x) {
+  const int li = (int)c->L.size() - 1;
+  const DeviceLevel& L = c->L[li];
+  Coarse& C = c->C;
+  const int64_t n = L.n;
+  double* s = c->scal + 16;  // [0] p.q  [2] r.r  [4],[6] z.r ping-pong (+1: r.r from jacobi_dot)
+  CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+  launch_init_masked(c, li, b, C.r, 1);
+  int dcur = 4, dnew = 6;
+  launch_jacobi_dot(c, n, C.dinv, C.r, C.z, s + dcur);
+  CUDA_CHECK(cudaMemcpyAsync(c->hscal, s + dcur, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  const double nb = std::sqrt(c->hscal[1]);
+  if (nb == 0.0) return;
+  const double thr = c->opts.coarse_rtol * nb;
+  launch_xpby(c, n, C.p, C.z, nullptr, nullptr, 1);
+  for (int it = 1; it <= c->opts.coarse_maxit; ++it) {
+    CUDA_CHECK(cudaMemsetAsync(C.q, 0, sizeof(double) * n, c->stream));
+    launch_apply(c, li, C.p, C.q, 0);
+    launch_dot2(c, n, C.p, C.q, nullptr, nullptr, nullptr, s + 0);
+    launch_axpy_pcg(c, n, x, C.r, C.p, C.q, s + dcur, s + 0, s + 2);
+    C.iters++;
+    if ((it & 7) == 0 || it == c->opts.coarse_maxit) {
+      CUDA_CHECK(cudaMemcpyAsync(c->hscal, s + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      if (std::sqrt(c->hscal[0]) <= thr) return;
+    }
+    launch_jacobi_dot(c, n, C.dinv, C.r, C.z, s + dnew);
+    launch_xpby(c, n, C.p, C.z, s + dnew, s + dcur, 0);
+    std::swap(dcur, dnew);
+  }
+}
+
+void coarse_solve(sem_ctx* c, const double* f, double* u) {
+  if (c->C.iterative) coarse_pcg(c, f, u);
+  else launch_coarse(c, f, u);
+}
+
 // ------------------------------------------------------------------ V-cycle (Alg 4.1)
 void vcycle(sem_ctx* c, int li, const double* f, double* u) {
   const int nl = (int)c->L.size();
   if (li == nl - 1) {  // coarsest: exact solve (O10, O26)
-    launch_coarse(c, f, u);
+    coarse_solve(c, f, u);
     return;
   }
   DeviceLevel& L = c->L[li];
@@ -482,6 +567,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   const int64_t n = L.n;
   sem_report R;
   memset(&R, 0, sizeof(R));
+  c->C.iters = 0;
   CUDA_CHECK(cudaEventRecord(c->ev0, c->stream));
   double* u = c->xw;   // free-node iterate
   double* r = c->bw;   // residual
@@ -505,16 +591,19 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   if (rn <= thresh) {
     R.converged = 1;
   } else if (o.outer == 0) {
-    // Alg 4.3: p = V(r); delta = p^T r
+    // Alg 4.3: p = V(r); delta = p^T r.  With an iterative coarse solve the
+    // preconditioner is not exactly linear: flexible CG (Polak-Ribiere beta)
+    const bool flex = c->C.iterative != 0;
     vcycle(c, 0, r, p);
     R.vcycles++;
-    int dcur = 0, dnew = 2;
+    int dcur = 8, dnew = 10;  // [d] = z^T r, [d+1] = z^T r_old
     launch_dot2(c, n, p, r, nullptr, nullptr, nullptr, sc + dcur);
     while (R.iters < o.imax) {
       // q = A p (masked: p is 0 on Dirichlet nodes)
       CUDA_CHECK(cudaMemsetAsync(q, 0, sizeof(double) * n, c->stream));
       launch_apply(c, 0, p, q, 0);
       launch_dot2(c, n, p, q, nullptr, nullptr, nullptr, sc + 1);
+      if (flex) CUDA_CHECK(cudaMemcpyAsync(c->rw_old, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
       // alpha = delta / p^T q; u += alpha p; r -= alpha q; ||r||^2
       launch_axpy_pcg(c, n, u, r, p, q, sc + dcur, sc + 1, sc + 3);
       R.iters++;
@@ -529,12 +618,16 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
         R.converged = 1;
         break;
       }
-      // z = V(r); beta = z^T r / delta; p = z + beta p; delta = z^T r
+      // z = V(r); beta = z^T r / delta (flexible: z^T (r - r_old) / delta); p = z + beta p
       vcycle(c, 0, r, z);
       R.vcycles++;
-      launch_dot2(c, n, z, r, nullptr, nullptr, nullptr, sc + dnew);
-      // beta = z^T r / delta
-      launch_xpby(c, n, p, z, sc + dnew, sc + dcur, 0);
+      if (flex) {
+        launch_dot2(c, n, z, r, z, c->rw_old, nullptr, sc + dnew);
+        launch_xpby(c, n, p, z, sc + dnew, sc + dcur, 2);
+      } else {
+        launch_dot2(c, n, z, r, nullptr, nullptr, nullptr, sc + dnew);
+        launch_xpby(c, n, p, z, sc + dnew, sc + dcur, 0);
+      }
       std::swap(dcur, dnew);
     }
   } else {
@@ -564,6 +657,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   float ms = 0.f;
   CUDA_CHECK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   R.t_ms = ms;
+  R.coarse_iters = (int)c->C.iters;
   R.rel_res = nf > 0 ? rn / nf : 0.0;
   if (R.n_hist > 1) {
     const int m = R.n_hist - 1;
@@ -599,6 +693,9 @@ void sem_default_opts(sem_opts* o) {
   o->device = -1;
   o->verbose = 0;
   o->apply_kernel = 0;
+  o->coarse_solver = 0;
+  o->coarse_rtol = 1e-10;
+  o->coarse_maxit = 20000;
 }
 
 int sem_reference_nodes(int p, double* rst) {
@@ -754,7 +851,7 @@ int sem_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose
 int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
   if (!c || !r || !z) return SEM_EINVAL;
   try {
-    launch_coarse(c, r, z);
+    coarse_solve(c, r, z);
   } catch (const SemError& e) {
     return fail(e);
   }

@@ -64,8 +64,13 @@ struct DeviceLevel {
 struct Coarse {
   int64_t nc = 0;               // free coarse nodes
   int32_t* fidx = nullptr;      // [nc] compact -> level gid
-  double* Ainv = nullptr;       // [nc][nc] row-major, symmetric
+  double* Ainv = nullptr;       // [nc][nc] row-major, symmetric (dense path)
   double* x = nullptr;          // [nc] work
+  // iterative path (reading O9): Jacobi-preconditioned CG on the P=1 operator
+  int iterative = 0;
+  double* dinv = nullptr;       // [n] inverse diagonal, 0 on Dirichlet nodes
+  double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+  int64_t iters = 0;            // inner iterations since the last reset
 };
 
 }  // namespace sem
@@ -78,9 +83,9 @@ struct sem_ctx {
   int P = 0;
   std::vector<sem::DeviceLevel> L;
   sem::Coarse C;
-  double* scal = nullptr;       // device scalars [16]
+  double* scal = nullptr;       // device scalars [32]
   double* hscal = nullptr;      // pinned host scalars [16]
-  double *pw = nullptr, *qw = nullptr, *zw = nullptr, *bw = nullptr, *xw = nullptr;  // solver work
+  double *pw = nullptr, *qw = nullptr, *zw = nullptr, *bw = nullptr, *xw = nullptr, *rw_old = nullptr;  // solver work
   double *host_in = nullptr, *host_in2 = nullptr, *host_out = nullptr;               // device staging for *_host
   int64_t launches = 0;
   int64_t device_bytes = 0;
@@ -110,9 +115,12 @@ void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);
 int launch_geometry(sem_ctx* c, int level, const double* d_xfine, const double* d_gmat, int Nf, const double* d_w);
 void launch_elem_matrices(sem_ctx* c, int level, const double* d_D, double* Ae, int e0, int ne);
 void launch_assemble_blocks(sem_ctx* c, int level, const int32_t* d_idx, const int64_t* d_off, const int32_t* d_elist,
-                            const int64_t* d_eoff, const double* Ae, int k0, int nb, int npad, double* B);
+                            const int64_t* d_eoff, const double* Ae, int ebase, int k0, int nb, int npad, double* B);
 void launch_pack_tiles(sem_ctx* c, int level, const double* Binv, int k0, int nb, int npad, const int64_t* d_off);
 void launch_assemble_coarse(sem_ctx* c, const double* Ae, const int32_t* d_cmap, double* A, int64_t nc);
 void launch_symmetrize(sem_ctx* c, double* A, int64_t n);
 void launch_set_identity(sem_ctx* c, double* X, int nb, int npad);
+void launch_diag_accum_range(sem_ctx* c, const int32_t* conn, int N, int ne, const double* Ae, double* diag);
+void launch_invert_masked(sem_ctx* c, int level, double* d);
+void launch_jacobi_dot(sem_ctx* c, int64_t n, const double* dinv, const double* r, double* z, double* out2);
 }  // namespace sem

@@ -548,12 +548,13 @@ void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* 
   c->launches++;
 }
 
-// p = z + beta p, beta = num / den   (mode 0); p = z (mode 1)
+// p = z + beta p: beta = num[0] / den (mode 0); p = z (mode 1);
+// beta = (num[0] - num[1]) / den (mode 2, flexible CG: z^T (r - r_old) / delta)
 __global__ void k_xpby(int64_t n, double* __restrict__ p, const double* __restrict__ z, const double* num,
                        const double* den, int mode) {
-  const double beta = mode ? 0.0 : *num / *den;
+  const double beta = mode == 1 ? 0.0 : (mode == 2 ? (num[0] - num[1]) / *den : num[0] / *den);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = mode ? z[i] : fma(beta, p[i], z[i]);
+    p[i] = mode == 1 ? z[i] : fma(beta, p[i], z[i]);
 }
 
 void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den,
@@ -572,6 +573,54 @@ void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y) {
   k_axpy<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, x, y);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
+}
+
+// z = dinv .* r; out2[0] += z.r; out2[1] += r.r
+__global__ void k_jacobi_dot(int64_t n, const double* __restrict__ d, const double* __restrict__ r,
+                             double* __restrict__ z, double* out2) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = r[i], zi = d[i] * ri;
+    z[i] = zi;
+    s0 = fma(zi, ri, s0);
+    s1 = fma(ri, ri, s1);
+  }
+  block_sum2_atomic(s0, s1, out2, out2 + 1);
+}
+
+void launch_jacobi_dot(sem_ctx* c, int64_t n, const double* dinv, const double* r, double* z, double* out2) {
+  CUDA_CHECK(cudaMemsetAsync(out2, 0, 2 * sizeof(double), c->stream));
+  k_jacobi_dot<<<grid_for(n, 256), 256, 0, c->stream>>>(n, dinv, r, z, out2);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// diag[g] += Ae[e][n][n] over free nodes (setup)
+__global__ void k_diag_accum(int64_t E, int N, const int32_t* __restrict__ conn, const double* __restrict__ Ae,
+                             double* __restrict__ diag) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= E * N) return;
+  const int64_t e = idx / N;
+  const int n = (int)(idx % N);
+  const int c = conn[idx];
+  if (c >= 0) atomicAdd(diag + c, Ae[(e * N + n) * N + n]);
+}
+
+void launch_diag_accum_range(sem_ctx* c, const int32_t* conn, int N, int ne, const double* Ae, double* diag) {
+  const int64_t tot = (int64_t)ne * N;
+  k_diag_accum<<<(int)((tot + 255) / 256), 256, 0, c->stream>>>(ne, N, conn, Ae, diag);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void k_invert_masked(int64_t n, const uint8_t* __restrict__ dmask, double* d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = (dmask[i] || d[i] == 0.0) ? 0.0 : 1.0 / d[i];
+}
+
+void launch_invert_masked(sem_ctx* c, int level, double* d) {
+  const DeviceLevel& L = c->L[level];
+  k_invert_masked<<<grid_for(L.n, 256), 256, 0, c->stream>>>(L.n, L.dmask, d);
+  CUDA_CHECK(cudaGetLastError());
 }
 
 // phi = free ? uF : phiD
@@ -682,8 +731,8 @@ void launch_elem_matrices(sem_ctx* c, int level, const double* D, double* Ae, in
 // Dirichlet-eliminated A on subdomain k); padded to npad with the identity.
 __global__ void k_assemble_blocks(int N, const int32_t* __restrict__ conn, const int32_t* __restrict__ idx,
                                   const int64_t* __restrict__ off, const int32_t* __restrict__ elist,
-                                  const int64_t* __restrict__ eoff, const double* __restrict__ Ae, int k0,
-                                  int npad, double* __restrict__ B) {
+                                  const int64_t* __restrict__ eoff, const double* __restrict__ Ae, int ebase,
+                                  int k0, int npad, double* __restrict__ B) {
   extern __shared__ int ism[];
   int* sidx = ism;              // [npad]
   int* pos = ism + npad;        // [N]
@@ -717,7 +766,7 @@ __global__ void k_assemble_blocks(int N, const int32_t* __restrict__ conn, const
     }
     __syncthreads();
     const int nl = nloc;
-    const double* A = Ae + (size_t)e * N * N;
+    const double* A = Ae + (size_t)(e - ebase) * N * N;
     for (int pr = threadIdx.x; pr < nl * nl; pr += blockDim.x) {
       const int i = loc[pr / nl], j = loc[pr % nl];
       Bk[(size_t)pos[i] * npad + pos[j]] += A[(size_t)i * N + j];
@@ -727,10 +776,10 @@ __global__ void k_assemble_blocks(int N, const int32_t* __restrict__ conn, const
 }
 
 void launch_assemble_blocks(sem_ctx* c, int level, const int32_t* idx, const int64_t* off, const int32_t* elist,
-                            const int64_t* eoff, const double* Ae, int k0, int nb, int npad, double* B) {
+                            const int64_t* eoff, const double* Ae, int ebase, int k0, int nb, int npad, double* B) {
   const DeviceLevel& L = c->L[level];
   const int smem = (npad + 2 * L.N) * (int)sizeof(int);
-  k_assemble_blocks<<<nb, 256, smem, c->stream>>>(L.N, L.conn, idx, off, elist, eoff, Ae, k0, npad, B);
+  k_assemble_blocks<<<nb, 256, smem, c->stream>>>(L.N, L.conn, idx, off, elist, eoff, Ae, ebase, k0, npad, B);
   CUDA_CHECK(cudaGetLastError());
 }
 

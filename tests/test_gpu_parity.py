@@ -280,3 +280,21 @@ def test_not_converged_flag(c1):
     phiD = torch.from_numpy(m.phi(*lev.xyz.T)[perm]).cuda()
     phi, rep = s.solve(phiD, tol=1e-14, check=False)
     assert not rep["converged"] and rep["iters"] == 1
+
+
+def test_iterative_coarse_solver(c2):
+    """Reading O9 for large P=1 problems: Jacobi-PCG coarse solve (coarse_solver=1)
+    agrees with the exact coarse solve to its tolerance, and the flexible outer
+    PCG still reaches the sparse-direct solution to 1e-10."""
+    m = c2.m
+    s = make_solver(m, coarse_solver=1, coarse_rtol=1e-12)
+    last = c2.mg.levels[-1]
+    li = c2.nl - 1
+    r = random_vector(last.A.shape[0], seed=12)
+    z = s.coarse_solve(c2.free_to_lib(li, r))
+    assert rel(c2.lib_to_free(li, z), last.coarse_lu.solve(r)) <= 1e-9
+    lev, perm = c2.levels[0]
+    phiD = m.phi(*lev.xyz.T)
+    phi, rep = s.solve(c2.to_lib(0, phiD), tol=1e-13)
+    assert rep["converged"] and rep["coarse_iters"] > 0
+    assert rel(c2.to_orc(0, phi), sem.solve_direct(lev, phiD)) <= SOLVE_TOL
