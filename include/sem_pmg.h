@@ -93,6 +93,15 @@ typedef struct {
                                  flexible), 2 dense                                                  */
   double coarse_rtol;         /* relative tolerance of the iterative coarse solve, default 1e-10      */
   int coarse_maxit;           /* iteration cap of the iterative coarse solve, default 20000           */
+  int nranks;                 /* partitioned solve over nranks column partitions (default 1)         */
+  int rank;                   /* this process's rank when nccl_id != NULL                            */
+  const void *nccl_id;        /* ncclUniqueId (128 bytes) shared by all ranks (sem_nccl_unique_id on
+                                 rank 0, broadcast by the caller): one rank per process and GPU, NCCL
+                                 exchanges.  NULL with nranks > 1: all nranks partitions emulated in
+                                 this process on one device (validation of the partitioned path).
+                                 In both modes every vector argument of the compute calls stays a
+                                 GLOBAL vector (library numbering of the whole mesh), replicated on
+                                 every rank; outputs are complete on every rank.                    */
 } sem_opts;
 
 typedef struct {
@@ -192,6 +201,9 @@ int sem_schwarz(sem_ctx *ctx, int level, const double *r, double *u, int transpo
 /* z = A_1^-1 r on the coarsest level (exact coarse solve); z = 0 on Dirichlet. */
 int sem_coarse_solve(sem_ctx *ctx, const double *r, double *z);
 
+/* Generate an NCCL unique id (128 bytes) for opts.nccl_id (call on rank 0). */
+int sem_nccl_unique_id(void *id_out);
+
 /* Number of kernel launches the library enqueued since the last reset. */
 int64_t sem_launch_count(const sem_ctx *ctx, int reset);
 
@@ -209,6 +221,16 @@ int sem_host_numbering(const sem_mesh *mesh, int p, int64_t *n_dof, int64_t *n_f
  * weights of eq 4.6 (0 on Dirichlet nodes).  Two-call pattern as above. */
 int sem_host_schwarz(const sem_mesh *mesh, int p, int overlap, int64_t *total, int64_t *off,
                      int32_t *idx, double *W);
+/* Column partition used by the partitioned solve (opts.nranks > 1), level
+ * `level` of the default schedule of order p (>= 2), seen from `rank`:
+ * sizes[5] = {elements held, elements owned, local nodes, neighbours, exchange
+ * entries}; elems [held] global element ids (owned first), gid [local nodes]
+ * global node ids, owned [local nodes] (each global node owned by exactly one
+ * rank), nbr [neighbours] ranks, xoff [neighbours+1], xidx [entries] local ids
+ * of the nodes shared with each neighbour in ascending global id.  Two-call
+ * pattern (NULL arrays first). */
+int sem_host_partition(const sem_mesh *mesh, int p, int nranks, int rank, int level, int64_t *sizes,
+                       int32_t *elems, int32_t *gid, uint8_t *owned, int32_t *nbr, int64_t *xoff, int32_t *xidx);
 /* Reference operator matrices of order p: B0, Br, Bs [(p+1)^2][Nt] (triangle
  * basis / d/dr / d/ds at the collapsed cubature), Bt, Dt [p+1][p+1] (1D basis /
  * derivative at vertical Gauss points), w [(p+1)^3] cubature weights. */

@@ -11,8 +11,10 @@ from ._capi import (  # noqa: F401
     Solver,
     default_opts,
     host_numbering,
+    host_partition,
     host_reference,
     host_schwarz,
+    nccl_unique_id,
     reference_nodes,
 )
 

@@ -26,7 +26,8 @@ class SemOpts(C.Structure):
                 ("outer", C.c_int), ("levels", C.POINTER(C.c_int)), ("n_levels", C.c_int),
                 ("atol", C.c_double), ("imax", C.c_int), ("stream", C.c_void_p), ("device", C.c_int),
                 ("verbose", C.c_int), ("apply_kernel", C.c_int), ("coarse_solver", C.c_int),
-                ("coarse_rtol", C.c_double), ("coarse_maxit", C.c_int)]
+                ("coarse_rtol", C.c_double), ("coarse_maxit", C.c_int), ("nranks", C.c_int), ("rank", C.c_int),
+                ("nccl_id", C.c_void_p)]
 
 
 class SemReport(C.Structure):
@@ -65,6 +66,7 @@ _lib.sem_prolong.argtypes = [_vp, C.c_int, _vp, _vp]
 _lib.sem_restrict.argtypes = [_vp, C.c_int, _vp, _vp]
 _lib.sem_schwarz.argtypes = [_vp, C.c_int, _vp, _vp, C.c_int]
 _lib.sem_coarse_solve.argtypes = [_vp, _vp, _vp]
+_lib.sem_nccl_unique_id.argtypes = [_vp]
 _lib.sem_launch_count.argtypes = [_vp, C.c_int]
 _lib.sem_launch_count.restype = C.c_int64
 _lib.sem_destroy.argtypes = [_vp]
@@ -76,8 +78,10 @@ _lib.sem_host_numbering.argtypes = [C.POINTER(SemMesh), C.c_int, C.POINTER(C.c_i
                                     _vp, _vp, _vp]
 _lib.sem_host_schwarz.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.POINTER(C.c_int64), _vp, _vp, _vp]
 _lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.sem_host_partition.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
+                                    _vp, _vp, _vp]
 
-EXPORTS = ["sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+EXPORTS = ["sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
            "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
            "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
            "sem_destroy", "sem_strerror", "sem_last_error"]
@@ -154,6 +158,25 @@ def host_schwarz(vertices, prisms, face_tag, p, overlap):
     return [idx[off[k]:off[k + 1]] for k in range(E)], W
 
 
+def host_partition(vertices, prisms, face_tag, p, nranks, rank, level=0):
+    """sem_host_partition: dict(elems, E_own, gid, owned, nbr, xidx=[per neighbour local ids])."""
+    m, keep = _mesh_struct(vertices, prisms, face_tag)
+    sizes = np.zeros(5, dtype=np.int64)
+    vp = lambda a: C.c_void_p(a.ctypes.data)
+    _check(_lib.sem_host_partition(C.byref(m), p, nranks, rank, level, vp(sizes), None, None, None, None, None, None),
+           "sem_host_partition")
+    elems = np.zeros(sizes[0], dtype=np.int32)
+    gid = np.zeros(sizes[2], dtype=np.int32)
+    owned = np.zeros(sizes[2], dtype=np.uint8)
+    nbr = np.zeros(sizes[3], dtype=np.int32)
+    xoff = np.zeros(sizes[3] + 1, dtype=np.int64)
+    xidx = np.zeros(max(1, sizes[4]), dtype=np.int32)
+    _check(_lib.sem_host_partition(C.byref(m), p, nranks, rank, level, vp(sizes), vp(elems), vp(gid), vp(owned),
+                                   vp(nbr), vp(xoff), vp(xidx)), "sem_host_partition")
+    return dict(elems=elems, E_own=int(sizes[1]), gid=gid, owned=owned.astype(bool), nbr=nbr.tolist(),
+                xidx=[xidx[xoff[j]:xoff[j + 1]] for j in range(len(nbr))])
+
+
 def host_reference(p):
     """sem_host_reference: dict of B0, Br, Bs [(p+1)^2][Nt], Bt, Dt [p+1][p+1], w [(p+1)^3]."""
     nt, qt, n1 = (p + 1) * (p + 2) // 2, (p + 1) ** 2, p + 1
@@ -162,6 +185,13 @@ def host_reference(p):
     _check(_lib.sem_host_reference(p, *[C.c_void_p(out[k].ctypes.data) for k in ("B0", "Br", "Bs", "Bt", "Dt", "w")]),
            "sem_host_reference")
     return out
+
+
+def nccl_unique_id() -> bytes:
+    """sem_nccl_unique_id: 128 opaque bytes to broadcast to every rank."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.sem_nccl_unique_id(C.cast(buf, C.c_void_p)), "sem_nccl_unique_id")
+    return buf.raw
 
 
 def _ptr(t):
@@ -175,7 +205,7 @@ class Solver:
     """sem_setup(mesh, p) + the compute calls of include/sem_pmg.h."""
 
     def __init__(self, vertices, prisms, face_tag, p: int, node_xyz=None, *, levels=None, stream=None,
-                 **opts):
+                 nccl_id: bytes | None = None, **opts):
         import torch
         self._torch = torch
         o = SemOpts()
@@ -189,6 +219,10 @@ class Solver:
             self._levels = (C.c_int * len(levels))(*levels)
             o.levels = self._levels
             o.n_levels = len(levels)
+        self._nccl = None
+        if nccl_id is not None:
+            self._nccl = C.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = C.cast(self._nccl, C.c_void_p)
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream

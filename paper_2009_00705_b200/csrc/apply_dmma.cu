@@ -365,9 +365,10 @@ static void apply_dmma_P(sem_ctx* c, const DeviceLevel& L, const double* u, doub
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, D::T, D::SMEM));
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const int nbatch = (c->E + D::NE - 1) / D::NE;
+  if (c->E_own == 0) return;
+  const int nbatch = (c->E_own + D::NE - 1) / D::NE;
   const int grid = nbatch < grid_max ? nbatch : grid_max;
-  kern<<<grid, D::T, D::SMEM, c->stream>>>(c->E, nbatch, L.conn, L.G, L.frag, u, y, flags);
+  kern<<<grid, D::T, D::SMEM, c->stream>>>(c->E_own, nbatch, L.conn, L.G, L.frag, u, y, flags);
   CUDA_CHECK(cudaGetLastError());
 }
 

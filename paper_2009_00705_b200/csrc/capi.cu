@@ -14,12 +14,14 @@
 #include <vector>
 
 #include "internal.h"
+#include "partition.h"
+#include "setup_util.h"
 
 using namespace sem;
 
 static thread_local std::string g_last_error;
 
-namespace {
+namespace sem {
 
 #define CUBLAS_CHECK(x)                                                                  \
   do {                                                                                   \
@@ -31,57 +33,6 @@ namespace {
     cusolverStatus_t _s = (x);                                                           \
     if (_s != CUSOLVER_STATUS_SUCCESS) throw SemError(SEM_ECUDA, std::string(#x) + " failed"); \
   } while (0)
-
-template <class T>
-T* dalloc(sem_ctx* c, size_t count) {
-  if (count == 0) count = 1;
-  void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw SemError(SEM_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
-  }
-  c->allocs.push_back(p);
-  c->device_bytes += (int64_t)(count * sizeof(T));
-  return (T*)p;
-}
-
-template <class T>
-T* upload(sem_ctx* c, const std::vector<T>& v) {
-  T* d = dalloc<T>(c, v.size());
-  if (!v.empty()) CUDA_CHECK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-  return d;
-}
-
-// scratch allocation freed at the end of setup
-struct Scratch {
-  std::vector<void*> ptrs;
-  template <class T>
-  T* get(size_t count) {
-    void* p = nullptr;
-    if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      throw SemError(SEM_ENOMEM, "setup scratch cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
-    }
-    ptrs.push_back(p);
-    return (T*)p;
-  }
-  template <class T>
-  T* put(const std::vector<T>& v) {
-    T* d = get<T>(v.size());
-    if (!v.empty()) CUDA_CHECK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-    return d;
-  }
-  void release(void* p) {
-    auto it = std::find(ptrs.begin(), ptrs.end(), p);
-    if (it != ptrs.end()) { cudaFree(p); ptrs.erase(it); }
-  }
-  ~Scratch() {
-    for (void* p : ptrs) cudaFree(p);
-  }
-};
 
 std::vector<int> schedule_for(int p, const sem_opts& o) {
   std::vector<int> s;
@@ -107,13 +58,11 @@ double now_ms() {
 }
 
 // ------------------------------------------------------------------ Schwarz setup
-void setup_schwarz(sem_ctx* c, int li, const LevelTopo& topo, int overlap, cublasHandle_t blas,
-                   cusolverDnHandle_t sol, const double* d_D, int verbose) {
+void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas, cusolverDnHandle_t sol,
+                   const double* d_D, int verbose) {
   DeviceLevel& L = c->L[li];
-  const int E = c->E;
+  const int E = c->E_own;  // one subdomain per owned element
   double t0 = now_ms();
-  int nth = std::min(32, std::max(1, omp_get_max_threads()));
-  SchwarzTopo S = schwarz_topology(topo, E, overlap, nth);
   double t1 = now_ms();
   // padded index lists and tile offsets
   std::vector<int64_t> poff(E + 1, 0), toff(E + 1, 0);
@@ -157,7 +106,7 @@ void setup_schwarz(sem_ctx* c, int li, const LevelTopo& topo, int overlap, cubla
   int64_t max_range = 1;
   for (int k = 0; k < E; ++k)
     max_range = std::max<int64_t>(max_range, S.elist[S.eoff[k + 1] - 1] - S.elist[S.eoff[k]] + 1);
-  int64_t cap = std::min<int64_t>(E, std::max<int64_t>((int64_t)(freeb * 0.25 / ae_elem), max_range));
+  int64_t cap = std::min<int64_t>(c->E, std::max<int64_t>((int64_t)(freeb * 0.25 / ae_elem), max_range));
   double* Ae = sc.get<double>((size_t)cap * L.N * L.N);
   CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
   size_t per = (size_t)npad * npad * 8 * 2 + 64;
@@ -285,24 +234,19 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }
 
-void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
-  const double t_start = now_ms();
+void check_opts(const sem_opts& o) {
+  if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
+      o.apply_kernel > 1 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
+      o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
+    throw SemError(SEM_EINVAL, "bad options");
+}
+
+void prepare_global(const sem_mesh* mesh, int p, const sem_opts& o, GlobalModel& gm) {
   if (!mesh || !mesh->prism || !mesh->face_tag || mesh->n_prism <= 0 || (!mesh->xyz && !mesh->node_xyz))
     throw SemError(SEM_EINVAL, "mesh arrays missing");
   if (p < 1 || p > 8) throw SemError(SEM_EINVAL, "order p must be in 1..8");
-  if (opts) c->opts = *opts;
-  else sem_default_opts(&c->opts);
-  const sem_opts& o = c->opts;
-  if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
-      o.apply_kernel > 1 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) || o.coarse_maxit < 1)
-    throw SemError(SEM_EINVAL, "bad options");
-  if (o.device >= 0) CUDA_CHECK(cudaSetDevice(o.device));
-  CUDA_CHECK(cudaGetDevice(&c->device));
-  c->stream = (cudaStream_t)o.stream;
-  c->E = mesh->n_prism;
-  c->P = p;
-  const int E = c->E;
-  HostMesh hm;
+  const int E = mesh->n_prism;
+  HostMesh& hm = gm.hm;
   hm.nv = mesh->n_vert;
   hm.E = E;
   hm.prism.assign(mesh->prism, mesh->prism + (size_t)E * 6);
@@ -310,12 +254,12 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   for (auto v : hm.prism)
     if (v < 0 || v >= hm.nv) throw SemError(SEM_EINVAL, "prism vertex index out of range");
   if (mesh->xyz) hm.xyz.assign(mesh->xyz, mesh->xyz + (size_t)hm.nv * 3);
-  const std::vector<int> sched = schedule_for(p, o);
-  const int nl = (int)sched.size();
-  if (nl > 16) throw SemError(SEM_EINVAL, "too many levels");
-  // fine nodal map X [E][N_P][3]
+  gm.P = p;
+  gm.sched = schedule_for(p, o);
+  if (gm.sched.size() > 16) throw SemError(SEM_EINVAL, "too many levels");
   const int Nf = n_prism(p);
-  std::vector<double> X((size_t)E * Nf * 3);
+  gm.X.resize((size_t)E * Nf * 3);
+  std::vector<double>& X = gm.X;
   if (mesh->node_xyz) {
     std::copy(mesh->node_xyz, mesh->node_xyz + X.size(), X.begin());
   } else {  // straight-sided: linear wedge map from the 6 vertices
@@ -337,11 +281,36 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   }
   double tm = now_ms();
   Entities ent;
-  if (sched[0] >= 2) ent = build_entities(hm);
-  std::vector<LevelTopo> topo(nl);
-  for (int li = 0; li < nl; ++li) topo[li] = number_level(hm, ent, sched[li]);
+  if (gm.sched[0] >= 2) ent = build_entities(hm);
+  gm.topo.resize(gm.sched.size());
+  for (size_t li = 0; li < gm.sched.size(); ++li) gm.topo[li] = number_level(hm, ent, gm.sched[li]);
   if (o.verbose) fprintf(stderr, "[sem] numbering %.0f ms\n", now_ms() - tm);
+}
 
+// Device data of the levels lids (indices into gm.topo, finest first) for the
+// whole mesh (part == nullptr; gsch = global Schwarz topologies, computed here
+// when null) or for one rank's partition.
+void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lids, const LocalPart* part,
+                  const std::vector<SchwarzTopo>* gsch) {
+  const sem_opts& o = c->opts;
+  const int p = gm.P;
+  const int Nf = n_prism(p);
+  const int nl = (int)lids.size();
+  const int E = part ? (int)part->elems.size() : gm.hm.E;
+  c->E = E;
+  c->E_own = part ? part->E_own : E;
+  c->P = p;
+  // finest nodal map of the held elements
+  std::vector<double> Xl;
+  const std::vector<double>* Xp = &gm.X;
+  if (part) {
+    Xl.resize((size_t)E * Nf * 3);
+    for (int i = 0; i < E; ++i)
+      std::copy(gm.X.begin() + (size_t)part->elems[i] * Nf * 3, gm.X.begin() + ((size_t)part->elems[i] + 1) * Nf * 3,
+                Xl.begin() + (size_t)i * Nf * 3);
+    Xp = &Xl;
+  }
+  const std::vector<double>& X = *Xp;
   c->L.resize(nl);
   cublasHandle_t blas;
   cusolverDnHandle_t sol;
@@ -362,20 +331,33 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   double* d_X = sc.put(X);
   for (int li = 0; li < nl; ++li) {
     DeviceLevel& L = c->L[li];
-    const LevelTopo& T = topo[li];
-    L.p = sched[li];
+    const int lid = lids[li];
+    const LevelTopo& GT = gm.topo[lid];
+    const std::vector<int32_t>& conn = part ? part->L[lid].conn : GT.conn;
+    const std::vector<uint8_t>& dir = part ? part->L[lid].dir : GT.dir;
+    const std::vector<uint8_t>& own = part ? part->L[lid].owner : GT.owner;
+    L.p = gm.sched[lid];
     L.ref = make_level_ref(L.p);
     L.N = L.ref.N;
     L.Q = L.ref.Q;
-    L.n = T.n;
-    L.nfree = T.nfree;
+    L.n = part ? part->L[lid].n : GT.n;
+    L.nfree = part ? part->L[lid].nfree : GT.nfree;
     // signed connectivity: Dirichlet nodes as ~gid
-    std::vector<int32_t> sc_conn(T.conn.size());
-    for (size_t t = 0; t < T.conn.size(); ++t) sc_conn[t] = T.dir[T.conn[t]] ? ~T.conn[t] : T.conn[t];
+    std::vector<int32_t> sc_conn(conn.size());
+    for (size_t t = 0; t < conn.size(); ++t) sc_conn[t] = dir[conn[t]] ? ~conn[t] : conn[t];
     L.conn = upload(c, sc_conn);
-    L.owner = upload(c, T.owner);
-    L.dmask = upload(c, T.dir);
-    L.dir_host = T.dir;
+    L.owner = upload(c, own);
+    L.dmask = upload(c, dir);
+    L.dir_host = dir;
+    if (part) {
+      L.gid_host = part->L[lid].gid;
+      L.owned_host = part->L[lid].owned;
+      std::vector<uint8_t> of(L.n);
+      for (int64_t i = 0; i < L.n; ++i) of[i] = part->L[lid].owned[i] && !dir[i];
+      L.ownfree = upload(c, of);
+      L.owned_dev = upload(c, part->L[lid].owned);
+      L.gid = upload(c, part->L[lid].gid);
+    }
     // reference matrices: B0 Br Bs [qt][ntp], Bt Dt [n1][n1]
     const LevelRef& R = L.ref;
     const int ntp = R.nt | 1;
@@ -392,7 +374,7 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
     }
     L.mats = upload(c, mats);
     L.frag = upload(c, dmma_fragments(R));
-    // geometric factors from the finest nodal map
+    // geometric factors from the finest nodal map (all held elements)
     L.G = dalloc<double>(c, (size_t)E * 6 * L.Q);
     {
       Scratch s2;
@@ -411,7 +393,8 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
         for (int l = 0; l < n1l; ++l)
           for (int m = 0; m < ntl; ++m) {
             const int n = m + ntl * l;
-            if (!T.owner[(size_t)e * L.N + n]) continue;
+            // every (e, n) writes the same position (up to rounding); the owner's wins in the global build
+            if (!part && !own[(size_t)e * L.N + n]) continue;
             double x[3] = {0, 0, 0};
             for (int lf = 0; lf < n1f; ++lf)
               for (int mf = 0; mf < ntf; ++mf) {
@@ -422,7 +405,7 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
                 x[1] += w * Xn[1];
                 x[2] += w * Xn[2];
               }
-            const int32_t g = T.conn[(size_t)e * L.N + n];
+            const int32_t g = conn[(size_t)e * L.N + n];
             L.xyz[3 * (size_t)g] = x[0];
             L.xyz[3 * (size_t)g + 1] = x[1];
             L.xyz[3 * (size_t)g + 2] = x[2];
@@ -430,24 +413,35 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
     }
     if (li + 1 < nl) {
       std::vector<double> It, I1;
-      transfer_matrices(L.p, sched[li + 1], It, I1);
+      transfer_matrices(L.p, gm.sched[lids[li + 1]], It, I1);
       L.Itri = upload(c, It);
       L.I1 = upload(c, I1);
     }
     L.u = dalloc<double>(c, L.n);
     L.f = dalloc<double>(c, L.n);
     L.r = dalloc<double>(c, L.n);
+    if (part) L.d = dalloc<double>(c, L.n);
   }
   sc.release(d_X);
-  // smoothers (all but the coarsest) and the coarse inverse
+  // smoothers (all but the coarsest) and, in the global build, the coarse solver
   for (int li = 0; li < nl; ++li) {
     Scratch s2;
     double* d_D = s2.put(c->L[li].ref.Dfull);
+    const int lid = lids[li];
     if (li + 1 < nl) {
-      int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
-      setup_schwarz(c, li, topo[li], ov, blas, sol, d_D, o.verbose);
-    } else {
-      setup_coarse(c, topo[li], sol, d_D);
+      double t0 = now_ms();
+      if (part) {
+        setup_schwarz(c, li, part->L[lid].S, blas, sol, d_D, o.verbose);
+      } else if (gsch) {
+        setup_schwarz(c, li, (*gsch)[lid], blas, sol, d_D, o.verbose);
+      } else {
+        const int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
+        SchwarzTopo S = schwarz_topology(gm.topo[lid], E, ov, std::min(32, std::max(1, omp_get_max_threads())));
+        if (o.verbose) fprintf(stderr, "[sem] level p=%d schwarz topology %.0f ms\n", c->L[li].p, now_ms() - t0);
+        setup_schwarz(c, li, S, blas, sol, d_D, o.verbose);
+      }
+    } else if (!part) {
+      setup_coarse(c, gm.topo[lid], sol, d_D);
     }
   }
   // solver work
@@ -465,6 +459,27 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   CUDA_CHECK(cudaMallocHost(&c->hscal, 32 * sizeof(double)));
   CUDA_CHECK(cudaEventCreate(&c->ev0));
   CUDA_CHECK(cudaEventCreate(&c->ev1));
+}
+
+void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
+  const double t_start = now_ms();
+  if (opts) c->opts = *opts;
+  else sem_default_opts(&c->opts);
+  const sem_opts& o = c->opts;
+  check_opts(o);
+  if (o.device >= 0) CUDA_CHECK(cudaSetDevice(o.device));
+  CUDA_CHECK(cudaGetDevice(&c->device));
+  c->stream = (cudaStream_t)o.stream;
+  GlobalModel gm;
+  prepare_global(mesh, p, o, gm);
+  c->E_global = gm.hm.E;
+  if (o.nranks > 1) {
+    setup_distributed(c, gm);
+  } else {
+    std::vector<int> lids(gm.sched.size());
+    for (size_t i = 0; i < lids.size(); ++i) lids[i] = (int)i;
+    build_levels(c, gm, lids, nullptr, nullptr);
+  }
   CUDA_CHECK(cudaDeviceSynchronize());
   c->launches = 0;
   c->setup_ms = now_ms() - t_start;
@@ -673,7 +688,7 @@ int fail(const SemError& e) {
   return e.code;
 }
 
-}  // namespace
+}  // namespace sem
 
 // ====================================================================== C ABI
 extern "C" {
@@ -696,6 +711,9 @@ void sem_default_opts(sem_opts* o) {
   o->coarse_solver = 0;
   o->coarse_rtol = 1e-10;
   o->coarse_maxit = 20000;
+  o->nranks = 1;
+  o->rank = 0;
+  o->nccl_id = nullptr;
 }
 
 int sem_reference_nodes(int p, double* rst) {
@@ -726,6 +744,11 @@ int sem_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx** out) 
 int sem_get_info(const sem_ctx* c, sem_info* info) {
   if (!c || !info) return SEM_EINVAL;
   memset(info, 0, sizeof(*info));
+  if (c->dist) {
+    dist_info(c, info);
+    info->setup_ms = c->setup_ms;
+    return SEM_OK;
+  }
   info->n_dof = c->L[0].n;
   info->n_free = c->L[0].nfree;
   info->n_elem = c->E;
@@ -745,8 +768,9 @@ int sem_get_info(const sem_ctx* c, sem_info* info) {
 }
 
 int sem_node_xyz(const sem_ctx* c, int level, double* xyz, int on_device) {
-  if (!c || !xyz || level < 0 || level >= (int)c->L.size()) return SEM_EINVAL;
-  const auto& v = c->L[level].xyz;
+  const int nl = c ? (c->dist ? dist_levels(c) : (int)c->L.size()) : 0;
+  if (!c || !xyz || level < 0 || level >= nl) return SEM_EINVAL;
+  const auto& v = c->dist ? dist_xyz(c, level) : c->L[level].xyz;
   if (on_device) {
     if (cudaMemcpy(xyz, v.data(), v.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return SEM_ECUDA;
   } else {
@@ -756,8 +780,9 @@ int sem_node_xyz(const sem_ctx* c, int level, double* xyz, int on_device) {
 }
 
 int sem_dirichlet_mask(const sem_ctx* c, int level, uint8_t* mask, int on_device) {
-  if (!c || !mask || level < 0 || level >= (int)c->L.size()) return SEM_EINVAL;
-  const auto& v = c->L[level].dir_host;
+  const int nl = c ? (c->dist ? dist_levels(c) : (int)c->L.size()) : 0;
+  if (!c || !mask || level < 0 || level >= nl) return SEM_EINVAL;
+  const auto& v = c->dist ? dist_dir(c, level) : c->L[level].dir_host;
   if (on_device) {
     if (cudaMemcpy(mask, v.data(), v.size(), cudaMemcpyHostToDevice) != cudaSuccess) return SEM_ECUDA;
   } else {
@@ -767,7 +792,15 @@ int sem_dirichlet_mask(const sem_ctx* c, int level, uint8_t* mask, int on_device
 }
 
 int sem_apply_laplace(sem_ctx* c, const double* u, double* y, int level, int masked) {
-  if (!c || !u || !y || u == y || level < 0 || level >= (int)c->L.size()) return SEM_EINVAL;
+  if (!c || !u || !y || u == y) return SEM_EINVAL;
+  if (c->dist) {
+    try {
+      return dist_apply(c, u, y, level, masked);
+    } catch (const SemError& e) {
+      return fail(e);
+    }
+  }
+  if (level < 0 || level >= (int)c->L.size()) return SEM_EINVAL;
   try {
     if (masked) {
       launch_init_masked(c, level, u, y, 0);
@@ -785,6 +818,7 @@ int sem_apply_laplace(sem_ctx* c, const double* u, double* y, int level, int mas
 int pmg_vcycle(sem_ctx* c, const double* r, double* z) {
   if (!c || !r || !z || r == z) return SEM_EINVAL;
   try {
+    if (c->dist) return dist_vcycle(c, r, z);
     vcycle(c, 0, r, z);
   } catch (const SemError& e) {
     return fail(e);
@@ -795,6 +829,10 @@ int pmg_vcycle(sem_ctx* c, const double* r, double* z) {
 int laplace_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
   if (!c) return SEM_EINVAL;
   try {
+    if (c->dist) {
+      if (!phiD || !phi || !(tol >= 0.0)) return SEM_EINVAL;
+      return dist_solve(c, rhs, phiD, tol, phi, rep);
+    }
     return do_solve(c, rhs, phiD, tol, phi, rep);
   } catch (const SemError& e) {
     return fail(e);
@@ -805,11 +843,19 @@ int laplace_solve_host(sem_ctx* c, const double* rhs_host, const double* phiD_ho
                        sem_report* rep) {
   if (!c || !phiD_host || !phi_host) return SEM_EINVAL;
   try {
-    const int64_t n = c->L[0].n;
+    sem_info inf;
+    sem_get_info(c, &inf);
+    const int64_t n = inf.n_dof;
+    if (c->dist && !c->host_in) {
+      c->host_in = dalloc<double>(c, n);
+      c->host_in2 = dalloc<double>(c, n);
+      c->host_out = dalloc<double>(c, n);
+    }
     if (rhs_host)
       CUDA_CHECK(cudaMemcpyAsync(c->host_in2, rhs_host, n * 8, cudaMemcpyHostToDevice, c->stream));
     CUDA_CHECK(cudaMemcpyAsync(c->host_in, phiD_host, n * 8, cudaMemcpyHostToDevice, c->stream));
-    int st = do_solve(c, rhs_host ? c->host_in2 : nullptr, c->host_in, tol, c->host_out, rep);
+    int st = c->dist ? dist_solve(c, rhs_host ? c->host_in2 : nullptr, c->host_in, tol, c->host_out, rep)
+                     : do_solve(c, rhs_host ? c->host_in2 : nullptr, c->host_in, tol, c->host_out, rep);
     CUDA_CHECK(cudaMemcpyAsync(phi_host, c->host_out, n * 8, cudaMemcpyDeviceToHost, c->stream));
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
     return st;
@@ -819,6 +865,7 @@ int laplace_solve_host(sem_ctx* c, const double* rhs_host, const double* phiD_ho
 }
 
 int sem_prolong(sem_ctx* c, int level, const double* uc, double* uf) {
+  if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !uc || !uf || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
   try {
     launch_prolong(c, level, uc, uf);
@@ -829,6 +876,7 @@ int sem_prolong(sem_ctx* c, int level, const double* uc, double* uf) {
 }
 
 int sem_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
+  if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !rf || !rc || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
   try {
     launch_restrict(c, level, rf, rc);
@@ -839,6 +887,7 @@ int sem_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
 }
 
 int sem_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose) {
+  if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !r || !u || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
   try {
     launch_schwarz(c, level, r, u, transpose);
@@ -849,6 +898,7 @@ int sem_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose
 }
 
 int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
+  if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !r || !z) return SEM_EINVAL;
   try {
     coarse_solve(c, r, z);
@@ -858,8 +908,19 @@ int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
   return SEM_OK;
 }
 
+int sem_nccl_unique_id(void* id_out) {
+  if (!id_out) return SEM_EINVAL;
+  try {
+    nccl_unique_id(id_out);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
 int64_t sem_launch_count(const sem_ctx* c, int reset) {
   if (!c) return -1;
+  if (c->dist) return dist_launches(c, reset) + c->launches;
   int64_t v = c->launches;
   if (reset) const_cast<sem_ctx*>(c)->launches = 0;
   return v;
@@ -868,6 +929,7 @@ int64_t sem_launch_count(const sem_ctx* c, int reset) {
 void sem_destroy(sem_ctx* c) {
   if (!c) return;
   cudaDeviceSynchronize();
+  dist_destroy(c);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hscal) cudaFreeHost(c->hscal);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -923,6 +985,50 @@ int sem_host_schwarz(const sem_mesh* mesh, int p, int overlap, int64_t* total, i
     if (off) std::copy(S.off.begin(), S.off.end(), off);
     if (idx) std::copy(S.idx.begin(), S.idx.end(), idx);
     if (W) std::copy(S.W.begin(), S.W.end(), W);
+  } catch (const SemError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SEM_EINVAL;
+  }
+  return SEM_OK;
+}
+
+int sem_host_partition(const sem_mesh* mesh, int p, int nranks, int rank, int level, int64_t* sizes,
+                       int32_t* elems, int32_t* gid, uint8_t* owned, int32_t* nbr, int64_t* xoff, int32_t* xidx) {
+  if (p < 2 || p > 8 || nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks || !sizes) return SEM_EINVAL;
+  try {
+    sem_opts o;
+    sem_default_opts(&o);
+    o.nranks = nranks;
+    GlobalModel gm;
+    prepare_global(mesh, p, o, gm);
+    if (level < 0 || level >= (int)gm.sched.size()) return SEM_EINVAL;
+    std::vector<int> epart;
+    std::vector<SchwarzTopo> sch;
+    compute_partition(gm, o, epart, sch);
+    LocalPart P = extract_part(gm.topo, sch, epart, rank, nranks);
+    const LocalLevel& L = P.L[level];
+    int64_t nx = 0;
+    for (auto& v : L.xidx) nx += (int64_t)v.size();
+    sizes[0] = (int64_t)P.elems.size();
+    sizes[1] = P.E_own;
+    sizes[2] = L.n;
+    sizes[3] = (int64_t)L.nbr.size();
+    sizes[4] = nx;
+    if (elems) std::copy(P.elems.begin(), P.elems.end(), elems);
+    if (gid) std::copy(L.gid.begin(), L.gid.end(), gid);
+    if (owned) std::copy(L.owned.begin(), L.owned.end(), owned);
+    if (nbr) std::copy(L.nbr.begin(), L.nbr.end(), nbr);
+    if (xoff || xidx) {
+      int64_t o2 = 0;
+      if (xoff) xoff[0] = 0;
+      for (size_t j = 0; j < L.xidx.size(); ++j) {
+        if (xidx) std::copy(L.xidx[j].begin(), L.xidx[j].end(), xidx + o2);
+        o2 += (int64_t)L.xidx[j].size();
+        if (xoff) xoff[j + 1] = o2;
+      }
+    }
   } catch (const SemError& e) {
     return fail(e);
   } catch (const std::exception& e) {

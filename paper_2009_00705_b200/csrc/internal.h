@@ -59,7 +59,22 @@ struct DeviceLevel {
   double *u = nullptr, *f = nullptr, *r = nullptr;
   std::vector<double> xyz;      // host [n][3]
   std::vector<uint8_t> dir_host;
+  // partitioned solve (dist.cu)
+  std::vector<int32_t> gid_host;     // local -> global node id
+  std::vector<uint8_t> owned_host;   // node owned by this rank
+  int32_t* gid = nullptr;            // device copy of gid_host
+  uint8_t* ownfree = nullptr;        // owned and free (dots, single-count RHS)
+  uint8_t* owned_dev = nullptr;      // owned (gather of global outputs)
+  double* d = nullptr;               // partial-sum work vector
+  // neighbour exchange of shared nodes
+  std::vector<int> nbr;
+  std::vector<int64_t> xoff;         // [nbr+1] offsets into xidx / send / recv
+  int32_t* xidx = nullptr;           // concatenated local ids
+  int32_t* xnbr = nullptr;           // neighbour slot of every entry (unused by NCCL path)
+  double *sendbuf = nullptr, *recvbuf = nullptr;
 };
+
+struct Dist;  // dist.cu
 
 struct Coarse {
   int64_t nc = 0;               // free coarse nodes
@@ -73,13 +88,26 @@ struct Coarse {
   int64_t iters = 0;            // inner iterations since the last reset
 };
 
+// dist.cu (partitioned solve; c->dist != nullptr)
+int dist_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep);
+int dist_vcycle(sem_ctx* c, const double* r, double* z);
+int dist_apply(sem_ctx* c, const double* u, double* y, int level, int masked);
+void dist_info(const sem_ctx* c, sem_info* info);
+const std::vector<double>& dist_xyz(const sem_ctx* c, int level);
+const std::vector<uint8_t>& dist_dir(const sem_ctx* c, int level);
+int dist_levels(const sem_ctx* c);
+int64_t dist_launches(const sem_ctx* c, int reset);
+void dist_destroy(sem_ctx* c);
+void nccl_unique_id(void* out);
 }  // namespace sem
 
 struct sem_ctx {
   sem_opts opts;
   int device = 0;
   cudaStream_t stream = nullptr;
-  int E = 0;
+  int E_global = 0;             // elements of the whole mesh
+  int E = 0;                    // elements held (owned + halo in a partition)
+  int E_own = 0;                // elements owned (applied); the first E_own of the E
   int P = 0;
   std::vector<sem::DeviceLevel> L;
   sem::Coarse C;
@@ -87,6 +115,8 @@ struct sem_ctx {
   double* hscal = nullptr;      // pinned host scalars [16]
   double *pw = nullptr, *qw = nullptr, *zw = nullptr, *bw = nullptr, *xw = nullptr, *rw_old = nullptr;  // solver work
   double *host_in = nullptr, *host_in2 = nullptr, *host_out = nullptr;               // device staging for *_host
+  // ---- partitioned solve (dist.cu): nranks > 1
+  sem::Dist* dist = nullptr;
   int64_t launches = 0;
   int64_t device_bytes = 0;
   double setup_ms = 0.0;
@@ -107,7 +137,7 @@ void launch_coarse(sem_ctx* c, const double* r, double* z);
 void launch_dot2(sem_ctx* c, int64_t n, const double* a, const double* b, const double* d, const double* e,
                  const uint8_t* mask, double* out2);
 void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* p, const double* q,
-                     const double* num, const double* den, double* rr);
+                     const double* num, const double* den, double* rr, const uint8_t* mask = nullptr);
 void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den, int mode);
 void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi);
 void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);
@@ -123,4 +153,15 @@ void launch_set_identity(sem_ctx* c, double* X, int nb, int npad);
 void launch_diag_accum_range(sem_ctx* c, const int32_t* conn, int N, int ne, const double* Ae, double* diag);
 void launch_invert_masked(sem_ctx* c, int level, double* d);
 void launch_jacobi_dot(sem_ctx* c, int64_t n, const double* dinv, const double* r, double* z, double* out2);
+// dist.cu (partitioned solve; c->dist != nullptr)
+int dist_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep);
+int dist_vcycle(sem_ctx* c, const double* r, double* z);
+int dist_apply(sem_ctx* c, const double* u, double* y, int level, int masked);
+void dist_info(const sem_ctx* c, sem_info* info);
+const std::vector<double>& dist_xyz(const sem_ctx* c, int level);
+const std::vector<uint8_t>& dist_dir(const sem_ctx* c, int level);
+int dist_levels(const sem_ctx* c);
+int64_t dist_launches(const sem_ctx* c, int reset);
+void dist_destroy(sem_ctx* c);
+void nccl_unique_id(void* out);
 }  // namespace sem

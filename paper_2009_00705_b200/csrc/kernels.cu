@@ -190,8 +190,9 @@ static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y
     CUDA_CHECK(cudaFuncSetAttribute(k_apply<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
     attr = true;
   }
-  const int grid = (c->E + D::NE - 1) / D::NE;
-  k_apply<P><<<grid, D::T, D::SMEM, c->stream>>>(c->E, L.conn, L.G, L.mats, u, y, flags);
+  if (c->E_own == 0) return;
+  const int grid = (c->E_own + D::NE - 1) / D::NE;
+  k_apply<P><<<grid, D::T, D::SMEM, c->stream>>>(c->E_own, L.conn, L.G, L.mats, u, y, flags);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -218,14 +219,16 @@ void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) 
 // ============================================================== masked vector init
 // mode 0: dst = free ? 0 : src     (masked apply: identity rows on Dirichlet nodes)
 // mode 1: dst = free ? src : 0     (residual / RHS restricted to free nodes)
-__global__ void k_init_masked(int64_t n, const uint8_t* __restrict__ dmask, const double* __restrict__ src,
-                              double* __restrict__ dst, int mode) {
+// mode 2: dst = owned&free ? src : 0   (partitioned: each global node counted once)
+// mode 3: dst = Dirichlet ? src : dst  (identity rows, free entries kept)
+__global__ void k_init_masked(int64_t n, const uint8_t* __restrict__ dmask, const uint8_t* __restrict__ ownfree,
+                              const double* __restrict__ src, double* __restrict__ dst, int mode) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const bool dir = dmask[i];
-    double v;
-    if (mode == 0) v = dir ? (src ? src[i] : 0.0) : 0.0;
-    else v = dir ? 0.0 : (src ? src[i] : 0.0);
-    dst[i] = v;
+    if (mode == 0) dst[i] = dir ? (src ? src[i] : 0.0) : 0.0;
+    else if (mode == 1) dst[i] = dir ? 0.0 : (src ? src[i] : 0.0);
+    else if (mode == 2) dst[i] = ownfree[i] ? (src ? src[i] : 0.0) : 0.0;
+    else if (dir) dst[i] = src[i];
   }
 }
 
@@ -238,7 +241,8 @@ static int grid_for(int64_t n, int threads) {
 
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode) {
   const DeviceLevel& L = c->L[level];
-  k_init_masked<<<grid_for(L.n, 256), 256, 0, c->stream>>>(L.n, L.dmask, src, dst, mode);
+  if (mode == 2 && !L.ownfree) mode = 1;  // single domain: every free node is owned
+  k_init_masked<<<grid_for(L.n, 256), 256, 0, c->stream>>>(L.n, L.dmask, L.ownfree, src, dst, mode);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }
@@ -347,7 +351,8 @@ void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int trans
     CUDA_CHECK(cudaFuncSetAttribute(k_schwarz, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = smem;
   }
-  k_schwarz<<<c->E, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u, transpose, npad);
+  if (c->E_own == 0) return;
+  k_schwarz<<<c->E_own, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u, transpose, npad);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }
@@ -423,7 +428,8 @@ void launch_prolong(sem_ctx* c, int level, const double* uc, double* uf) {
   const DeviceLevel& F = c->L[level];
   const DeviceLevel& C = c->L[level + 1];
   const int smem = (C.N + F.ref.nt * C.ref.n1) * (int)sizeof(double);
-  k_prolong<<<c->E, 128, smem, c->stream>>>(c->E, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
+  if (c->E_own == 0) return;
+  k_prolong<<<c->E_own, 128, smem, c->stream>>>(c->E_own, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
                                             F.Itri, F.I1, uc, uf);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
@@ -434,7 +440,8 @@ void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
   const DeviceLevel& C = c->L[level + 1];
   CUDA_CHECK(cudaMemsetAsync(rc, 0, sizeof(double) * C.n, c->stream));
   const int smem = (F.N + F.ref.nt * C.ref.n1) * (int)sizeof(double);
-  k_restrict<<<c->E, 128, smem, c->stream>>>(c->E, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
+  if (c->E_own == 0) return;
+  k_restrict<<<c->E_own, 128, smem, c->stream>>>(c->E_own, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
                                              F.Itri, F.I1, rf, rc);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
@@ -507,11 +514,13 @@ __device__ __forceinline__ void block_sum2_atomic(double a, double b, double* ou
   }
 }
 
-// out2[0] += a.b ; out2[1] += d.e (if d)
+// out2[0] += a.b ; out2[1] += d.e (if d); over mask[i] != 0 only (if mask)
 __global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
-                       const double* __restrict__ d, const double* __restrict__ e, double* out2) {
+                       const double* __restrict__ d, const double* __restrict__ e, const uint8_t* __restrict__ mask,
+                       double* out2) {
   double s0 = 0.0, s1 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (mask && !mask[i]) continue;
     s0 = fma(a[i], b[i], s0);
     if (d) s1 = fma(d[i], e[i], s1);
   }
@@ -519,31 +528,32 @@ __global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __
 }
 
 void launch_dot2(sem_ctx* c, int64_t n, const double* a, const double* b, const double* d, const double* e,
-                 const uint8_t*, double* out2) {
+                 const uint8_t* mask, double* out2) {
   CUDA_CHECK(cudaMemsetAsync(out2, 0, sizeof(double) * (d ? 2 : 1), c->stream));
-  k_dot2<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, b, d, e, out2);
+  k_dot2<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, b, d, e, mask, out2);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }
 
 // alpha = num / den; u += alpha p; r -= alpha q; rr += r.r
 __global__ void k_axpy_pcg(int64_t n, double* __restrict__ u, double* __restrict__ r, const double* __restrict__ p,
-                           const double* __restrict__ q, const double* num, const double* den, double* rr) {
+                           const double* __restrict__ q, const double* num, const double* den, double* rr,
+                           const uint8_t* __restrict__ mask) {
   const double alpha = *num / *den;
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     u[i] = fma(alpha, p[i], u[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
-    s = fma(ri, ri, s);
+    if (!mask || mask[i]) s = fma(ri, ri, s);
   }
   block_sum2_atomic(s, 0.0, rr, nullptr);
 }
 
 void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* p, const double* q,
-                     const double* num, const double* den, double* rr) {
+                     const double* num, const double* den, double* rr, const uint8_t* mask) {
   CUDA_CHECK(cudaMemsetAsync(rr, 0, sizeof(double), c->stream));
-  k_axpy_pcg<<<grid_for(n, 256), 256, 0, c->stream>>>(n, u, r, p, q, num, den, rr);
+  k_axpy_pcg<<<grid_for(n, 256), 256, 0, c->stream>>>(n, u, r, p, q, num, den, rr, mask);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }

@@ -1,0 +1,81 @@
+"""Partitioned solve validated on one GPU: nranks column
+partitions emulated in one process (exchanges as device copies, the same code
+path as the NCCL transport).  Results must equal the single-domain solver's
+(same arithmetic up to summation order) and the oracle's."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2009_00705_b200 as lib  # noqa: E402
+from oracle import sem  # noqa: E402
+from tests._mapping import lib_to_oracle  # noqa: E402
+from workloads import config2, random_vector  # noqa: E402
+from workloads.configs import basin  # noqa: E402
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def mk(m, **kw):
+    return lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)), **kw)
+
+
+MESHES = {
+    "c3s": lambda: basin("c3s", 5, 32.0 * 6 / 64, 6, 3, seed=3),
+    "c2": lambda: config2(),
+}
+
+
+@pytest.fixture(scope="module", params=list(MESHES))
+def pair(request):
+    m = MESHES[request.param]()
+    return m, mk(m)
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_partitioned_matches_single_domain(pair, nranks):
+    m, s1 = pair
+    sd = mk(m, nranks=nranks)
+    assert sd.info["n_dof"] == s1.info["n_dof"] and sd.info["level_p"] == s1.info["level_p"]
+    np.testing.assert_array_equal(sd.node_xyz(0), s1.node_xyz(0))
+    n = s1.info["n_dof"]
+    mask = torch.from_numpy(s1.dirichlet_mask(0)).cuda()
+    # operator, every level, raw and masked
+    for li, nl in enumerate(s1.info["level_n_dof"]):
+        u = torch.from_numpy(random_vector(nl, seed=40 + li)).cuda()
+        for masked in (False, True):
+            y1 = s1.apply(u, level=li, masked=masked).cpu().numpy()
+            yd = sd.apply(u, level=li, masked=masked).cpu().numpy()
+            assert rel(yd, y1) <= 1e-13, (li, masked)
+    # one V-cycle
+    r = torch.from_numpy(random_vector(n, seed=3)).cuda().masked_fill(mask, 0.0)
+    z1 = s1.vcycle(r).cpu().numpy()
+    zd = sd.vcycle(r).cpu().numpy()
+    assert rel(zd, z1) <= 1e-12
+    # full solve
+    xyz = s1.node_xyz(0)
+    phiD = torch.from_numpy(m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])).cuda()
+    p1, r1 = s1.solve(phiD, 1e-12)
+    pd, rd = sd.solve(phiD, 1e-12)
+    assert rd["converged"] and abs(rd["iters"] - r1["iters"]) <= 1
+    assert rel(pd.cpu().numpy(), p1.cpu().numpy()) <= 1e-10
+    sd.close()
+
+
+def test_partitioned_solve_matches_oracle():
+    m = MESHES["c3s"]()
+    sd = mk(m, nranks=4)
+    lev = sem.build_system(m, m.p)
+    perm = lib_to_oracle(sd.node_xyz(0), lev.xyz)
+    phiD = m.phi(*lev.xyz.T)
+    phi, rep = sd.solve(torch.from_numpy(np.ascontiguousarray(phiD[perm])).cuda(), tol=1e-13)
+    got = np.zeros(lev.n)
+    got[perm] = phi.cpu().numpy()
+    assert rep["converged"] and rel(got, sem.solve_direct(lev, phiD)) <= 1e-10
+    sd.close()
