@@ -8,8 +8,8 @@ prisms, p = 5, 4.2 M DOF), inputs resident in HBM.  Metric: Laplace solve
 MDOF/s (free DOF / solve time).  See DESIGN.md §"Measurement".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-N > 1 runs under torchrun: every rank solves its own copy (replicas; the
-partitioned solve is NEXT, DESIGN.md §"Multi-GPU").
+N > 1 runs under torchrun: the same config-3 problem is partitioned by columns
+over the N ranks (one GPU each; NCCL halo exchange), strong scaling.
 """
 import argparse
 import json
@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="validation only: run the partitioned solve with R emulated ranks on one GPU")
     return ap.parse_args()
 
 
@@ -156,13 +158,6 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ GPU arm
-def schwarz_alg_bytes(s, level=0):
-    """Algorithmic bytes of one Schwarz sweep: the packed symmetric inverses
-    n_k(n_k+1)/2 * 8 B, the subdomain index lists, and one read of r, W, u and
-    one write of u per node (DESIGN.md §"Roofline")."""
-    return s._alg_schwarz_bytes
-
-
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -171,20 +166,26 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    import numpy as np
     import torch
     torch.cuda.set_device(local)
     dist = None
+    nccl_id = None
+    import paper_2009_00705_b200 as lib
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import paper_2009_00705_b200 as lib
-    from paper_2009_00705_b200.metrics import schwarz_bytes_model, apply_bytes_model
+        obj = [lib.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
 
     m = make_mesh(args.config)
     t0 = time.perf_counter()
-    s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
-                   verbose=int(os.environ.get("SEM_VERBOSE", "0")))
+    kw = dict(verbose=int(os.environ.get("SEM_VERBOSE", "0")))
+    if world > 1:
+        kw.update(nranks=world, rank=rank, nccl_id=nccl_id)
+    elif args.emulate_ranks > 1:
+        kw.update(nranks=args.emulate_ranks)
+    s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)), **kw)
     setup_s = time.perf_counter() - t0
     info = s.info
     xyz = s.node_xyz(0)
@@ -198,7 +199,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    reps = []
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(args.warmup):
         _, rep = s.solve(phiD, args.tol, out=phi)
     barrier()
@@ -206,6 +213,7 @@ def main():
     clk.start()
     s.launches(reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
     ev0.record(stream)
     for _ in range(args.steps):
         _, rep = s.solve(phiD, args.tol, out=phi)
@@ -213,53 +221,30 @@ def main():
     ev1.record(stream)
     barrier()
     launches = s.launches()
-    ms_total = ev0.elapsed_time(ev1)
     clocks = clk.stop()
-    if dist is not None:
-        t = torch.tensor([ms_total], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-    ms_step = ms_total / args.steps
+    ms_step = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     n_free = info["n_free"]
-    value = n_free * world / (ms_step * 1e-3) / 1e6
+    value = n_free / (ms_step * 1e-3) / 1e6          # one problem solved by all ranks together
 
-    # ---- dominant kernel: Schwarz sweep on the finest level, timed alone on the solve's stream
-    res = {}
-    r0 = torch.randn(info["n_dof"], dtype=torch.float64, device="cuda")
-    u0 = s.empty(0)
-    nrep = 20
-    for _ in range(3):
-        s.schwarz(0, r0, u0)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(nrep):
-        s.schwarz(0, r0, u0)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    t_schwarz = e0.elapsed_time(e1) / nrep * 1e-3
-    sb = schwarz_bytes_model(s, m)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    # ---- dominant kernel (Schwarz sweep, finest level) and the operator, timed alone on the solve's stream
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {"hbm_gbs": 6650.0}
     peak = peaks["hbm_gbs"]
-    ach = sb / t_schwarz / 1e9
-    roof = {"kernel": "k_schwarz (level 0, one sweep)", "bound": "hbm", "achieved": ach, "peak": peak,
-            "unit": "GB/s", "frac": ach / peak, "traffic": None, "alg_bytes_per_launch": sb,
-            "launch_us": t_schwarz * 1e6,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback"}
-    # ---- operator apply (north_star: >= 60 % of HBM)
-    for _ in range(3):
-        s.apply(r0, out=u0)
-    e0.record(stream)
-    for _ in range(nrep):
-        s.apply(r0, out=u0)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    t_apply = e0.elapsed_time(e1) / nrep * 1e-3
-    ab = apply_bytes_model(s, m)
-    apply = {"kernel": "k_apply<5> (+memset)", "MDOF_s": info["n_dof"] / t_apply / 1e6, "us": t_apply * 1e6,
-             "achieved_GBs": ab / t_apply / 1e9, "frac": ab / t_apply / 1e9 / peak, "alg_bytes_per_launch": ab,
-             "flops_per_launch": s._apply_flops if hasattr(s, "_apply_flops") else None}
-    # ---- end to end through the public host API
+    us_s, b_s = s.bench_kernel("schwarz", 0, 20)
+    us_a, b_a = s.bench_kernel("apply", 0, 20)
+    ach = b_s / (us_s * 1e-6) / 1e9
+    roof = {"kernel": "k_schwarz (level 0, one sweep" + (", this rank's partition)" if world > 1 else ")"),
+            "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+            "alg_bytes_per_launch": b_s, "launch_us": us_s,
+            "traffic_note": "ncu dram__bytes_read+write per launch in profiles/schwarz_r1_raw.csv (28.9 GB, N=1)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "when" in peaks else "fallback 6650 GB/s"}
+    if world == 1:
+        roof["traffic"] = 28.92e9
+    ach_a = b_a / (us_a * 1e-6) / 1e9
+    apply = {"kernel": "k_apply_dmma<%d> (FP64 tensor cores)" % m.p, "us": us_a, "alg_bytes_per_launch": b_a,
+             "achieved_GBs": ach_a, "frac": ach_a / peak,
+             "MDOF_s": info["n_dof"] / us_a if world == 1 else None}
+    # ---- end to end through the public host API (pinned host buffers, H2D + D2H inside)
     e2e = None
     if not args.no_e2e:
         ph = torch.from_numpy(phiD_h).pin_memory()
@@ -270,12 +255,8 @@ def main():
         for _ in range(args.steps):
             s.solve_host(ph, args.tol, out_h)
         barrier()
-        t_e2e = (time.perf_counter() - t0) / args.steps
-        if dist is not None:
-            t = torch.tensor([t_e2e], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
-        e2e = {"value": n_free * world / t_e2e / 1e6, "unit": "MDOF/s",
+        t_e2e = max_over_ranks((time.perf_counter() - t0) / args.steps)
+        e2e = {"value": n_free / t_e2e / 1e6, "unit": "MDOF/s",
                "h2d_bytes_per_step": info["n_dof"] * 8, "d2h_bytes_per_step": info["n_dof"] * 8,
                "ms_per_step": t_e2e * 1e3, "api": "laplace_solve_host (pinned host buffers)"}
     cpu = None
@@ -286,21 +267,24 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "MDOF/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config], "p": m.p, "n_dof": info["n_dof"], "n_free": n_free,
                        "n_elem": info["n_elem"], "levels": info["level_p"], "tol": args.tol, "nu": [3, 3],
                        "smoother": "additive Schwarz, overlap 1, exact dense local inverses (eq 4.4-4.6)",
-                       "outer": "PCG (Alg 4.3)", "coarse": f"dense inverse, {info['coarse_n']} free P=1 DOF",
+                       "outer": "PCG (Alg 4.3)", "coarse": f"P=1, {info['coarse_n']} free DOF "
+                       + ("(dense inverse)" if info["coarse_n"] <= 46000 else "(Jacobi-PCG)"),
                        "l2": "inputs larger than L2: each V-cycle streams "
                              f"{sum(info['schwarz_bytes']) / 1e9:.1f} GB of Schwarz inverses",
-                       "parallelism": "replicas" if world > 1 else "single GPU",
-                       "setup_s": setup_s},
+                       "parallelism": f"column partition x{world} (NCCL halo exchange)" if world > 1
+                       else (f"{args.emulate_ranks} emulated ranks on 1 GPU (validation, not a scaling number)"
+                             if args.emulate_ranks > 1 else "single GPU"), "setup_s": setup_s},
             "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "q_mean": rep["q_mean"],
             "roofline": roof, "apply": apply, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
         }
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 

@@ -201,6 +201,13 @@ int sem_schwarz(sem_ctx *ctx, int level, const double *r, double *u, int transpo
 /* z = A_1^-1 r on the coarsest level (exact coarse solve); z = 0 on Dirichlet. */
 int sem_coarse_solve(sem_ctx *ctx, const double *r, double *z);
 
+/* Time `reps` back-to-back launches of one hot kernel on the ctx's stream with
+ * CUDA events (after 3 warm-ups), on this rank's partition in a partitioned
+ * ctx: kernel 0 = one Schwarz sweep (k_schwarz) on `level` (not the coarsest),
+ * 1 = one operator apply (k_apply) on `level`.  mean_us: mean duration;
+ * alg_bytes: algorithmic bytes per launch. */
+int sem_bench_kernel(sem_ctx *ctx, int kernel, int level, int reps, double *mean_us, double *alg_bytes);
+
 /* Generate an NCCL unique id (128 bytes) for opts.nccl_id (call on rank 0). */
 int sem_nccl_unique_id(void *id_out);
 

@@ -67,6 +67,7 @@ _lib.sem_restrict.argtypes = [_vp, C.c_int, _vp, _vp]
 _lib.sem_schwarz.argtypes = [_vp, C.c_int, _vp, _vp, C.c_int]
 _lib.sem_coarse_solve.argtypes = [_vp, _vp, _vp]
 _lib.sem_nccl_unique_id.argtypes = [_vp]
+_lib.sem_bench_kernel.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 _lib.sem_launch_count.argtypes = [_vp, C.c_int]
 _lib.sem_launch_count.restype = C.c_int64
 _lib.sem_destroy.argtypes = [_vp]
@@ -81,7 +82,7 @@ _lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.sem_host_partition.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp]
 
-EXPORTS = ["sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+EXPORTS = ["sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
            "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
            "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
            "sem_destroy", "sem_strerror", "sem_last_error"]
@@ -325,6 +326,13 @@ class Solver:
         z = self.empty(self.info["n_levels"] - 1) if out is None else out
         _check(_lib.sem_coarse_solve(self._ctx, _ptr(r), _ptr(z)), "sem_coarse_solve")
         return z
+
+    def bench_kernel(self, kernel: str, level=0, reps=20):
+        """sem_bench_kernel: (mean microseconds, algorithmic bytes) of 'schwarz' or 'apply'."""
+        us, b = C.c_double(), C.c_double()
+        _check(_lib.sem_bench_kernel(self._ctx, {"schwarz": 0, "apply": 1}[kernel], level, reps, C.byref(us),
+                                     C.byref(b)), "sem_bench_kernel")
+        return us.value, b.value
 
     def launches(self, reset=False) -> int:
         return int(_lib.sem_launch_count(self._ctx, int(reset)))

@@ -908,6 +908,39 @@ int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
   return SEM_OK;
 }
 
+int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_us, double* alg_bytes) {
+  if (!c || reps < 1 || kernel < 0 || kernel > 1) return SEM_EINVAL;
+  try {
+    sem_ctx* t = c->dist ? dist_part0(c) : c;
+    if (level < 0 || level >= (int)t->L.size()) return SEM_EINVAL;
+    if (kernel == 0 && level + 1 >= (int)t->L.size()) return SEM_EINVAL;
+    DeviceLevel& L = t->L[level];
+    CUDA_CHECK(cudaMemsetAsync(L.f, 0, sizeof(double) * L.n, t->stream));
+    CUDA_CHECK(cudaMemsetAsync(L.u, 0, sizeof(double) * L.n, t->stream));
+    auto run = [&]() {
+      if (kernel == 0) launch_schwarz(t, level, L.f, L.u, 0);
+      else launch_apply(t, level, L.f, L.u, 0);
+    };
+    for (int i = 0; i < 3; ++i) run();
+    CUDA_CHECK(cudaEventRecord(t->ev0, t->stream));
+    for (int i = 0; i < reps; ++i) run();
+    CUDA_CHECK(cudaEventRecord(t->ev1, t->stream));
+    CUDA_CHECK(cudaEventSynchronize(t->ev1));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, t->ev0, t->ev1));
+    if (mean_us) *mean_us = 1e3 * ms / reps;
+    if (alg_bytes) {
+      if (kernel == 0)
+        *alg_bytes = 8.0 * L.packed + 4.0 * L.nk_sum + 32.0 * L.n;
+      else
+        *alg_bytes = (double)t->E_own * (48.0 * L.Q + 4.0 * L.N) + 16.0 * L.n;
+    }
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
 int sem_nccl_unique_id(void* id_out) {
   if (!id_out) return SEM_EINVAL;
   try {

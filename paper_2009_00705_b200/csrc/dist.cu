@@ -676,6 +676,7 @@ void dist_info(const sem_ctx* c, sem_info* info) {
 const std::vector<double>& dist_xyz(const sem_ctx* c, int level) { return c->dist->gxyz[level]; }
 const std::vector<uint8_t>& dist_dir(const sem_ctx* c, int level) { return c->dist->gdir[level]; }
 int dist_levels(const sem_ctx* c) { return (int)c->dist->gn.size(); }
+sem_ctx* dist_part0(const sem_ctx* c) { return c->dist->parts[0]; }
 
 int64_t dist_launches(const sem_ctx* c, int reset) {
   Dist& D = *c->dist;

@@ -96,6 +96,7 @@ void dist_info(const sem_ctx* c, sem_info* info);
 const std::vector<double>& dist_xyz(const sem_ctx* c, int level);
 const std::vector<uint8_t>& dist_dir(const sem_ctx* c, int level);
 int dist_levels(const sem_ctx* c);
+sem_ctx* dist_part0(const sem_ctx* c);
 int64_t dist_launches(const sem_ctx* c, int reset);
 void dist_destroy(sem_ctx* c);
 void nccl_unique_id(void* out);
@@ -161,6 +162,7 @@ void dist_info(const sem_ctx* c, sem_info* info);
 const std::vector<double>& dist_xyz(const sem_ctx* c, int level);
 const std::vector<uint8_t>& dist_dir(const sem_ctx* c, int level);
 int dist_levels(const sem_ctx* c);
+sem_ctx* dist_part0(const sem_ctx* c);
 int64_t dist_launches(const sem_ctx* c, int reset);
 void dist_destroy(sem_ctx* c);
 void nccl_unique_id(void* out);
