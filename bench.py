@@ -238,7 +238,7 @@ def main():
             "alg_bytes_per_launch": b_s, "launch_us": us_s,
             "traffic_note": "ncu dram__bytes_read+write per launch in profiles/schwarz_r1_raw.csv (28.9 GB, N=1)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "when" in peaks else "fallback 6650 GB/s"}
-    if world == 1:
+    if world == 1 and args.emulate_ranks <= 1 and args.config == "config3":
         roof["traffic"] = 28.92e9
     ach_a = b_a / (us_a * 1e-6) / 1e9
     apply = {"kernel": "k_apply_dmma<%d> (FP64 tensor cores)" % m.p, "us": us_a, "alg_bytes_per_launch": b_a,
