@@ -82,7 +82,9 @@ def _worker(rank, world, port, results):
 
 def test_partitioned_apply_and_dots_gloo():
     port = _free_port()
-    mgr = mp.Manager()
+    # spawn, not fork: the parent may already hold OpenMP / CUDA-runtime threads
+    # (libsem_pmg loaded by earlier tests), and a forked manager deadlocks on them
+    mgr = mp.get_context("spawn").Manager()
     results = mgr.dict()
     mp.spawn(_worker, args=(WORLD, port, results), nprocs=WORLD, join=True)
     assert len(results) == WORLD
