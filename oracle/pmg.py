@@ -25,6 +25,7 @@ import numpy as np
 import scipy.sparse as sp
 from scipy.sparse.linalg import splu
 
+from . import fdm
 from . import refelem as R
 from . import sem
 
@@ -115,6 +116,21 @@ def build_smoother(level: sem.Level, AFF: sp.csr_matrix, overlap: int) -> Smooth
     return Smoother(sets=sets, inv=inv, W=1.0 / count)
 
 
+def build_fdm_smoother(mesh, level: sem.Level, overlap: int) -> Smoother:
+    """eq 4.4 with the FDM local inverses of reading O33 (oracle/fdm.py)."""
+    F = level.free
+    fid = np.full(level.n, -1, dtype=np.int64)
+    fid[F] = np.arange(len(F))
+    sets, inv = [], []
+    count = np.zeros(len(F))
+    for ids, Binv in fdm.fdm_blocks(mesh, level, overlap):
+        I = fid[ids]
+        sets.append(I)
+        inv.append(Binv)
+        count[I] += 1.0
+    return Smoother(sets=sets, inv=inv, W=1.0 / count)
+
+
 @dataclasses.dataclass
 class MGLevel:
     level: sem.Level
@@ -128,7 +144,7 @@ class PMG:
     """Hierarchy of Alg 4.1 built from the oracle discretisation."""
 
     def __init__(self, mesh, p: int | None = None, schedule=None, overlap: int = 1,
-                 nu1: int = 3, nu2: int = 3, literal: bool = False):
+                 nu1: int = 3, nu2: int = 3, literal: bool = False, local_solve: str = "dense"):
         p = p or mesh.p
         self.schedule = list(schedule) if schedule else R.level_schedule(p)
         self.nu1, self.nu2, self.literal = nu1, nu2, literal
@@ -146,7 +162,11 @@ class PMG:
             if li == len(self.levels) - 1:
                 ml.coarse_lu = splu(ml.A.tocsc())
             else:
-                ml.smoother = build_smoother(ml.level, ml.A, overlap)
+                ov = overlap if overlap >= 0 else (ml.level.p + 2) // 2   # refined: ceil((P+1)/2)
+                if local_solve == "fdm":
+                    ml.smoother = build_fdm_smoother(mesh, ml.level, ov)
+                else:
+                    ml.smoother = build_smoother(ml.level, ml.A, ov)
 
     def smooth(self, li, u, f, nu, post):
         ml = self.levels[li]
