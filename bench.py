@@ -34,6 +34,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config3", choices=["config1", "config2", "config3"])
     ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--smoother", default="dense", choices=["dense", "fdm"],
+                    help="Schwarz local solves: exact dense inverses (eq 4.4) or FDM (reading O33)")
+    ap.add_argument("--overlap", type=int, default=1, help="Schwarz overlap (-1 = refined ceil((P+1)/2), P:536)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--emulate-ranks", type=int, default=0,
@@ -180,7 +183,8 @@ def main():
 
     m = make_mesh(args.config)
     t0 = time.perf_counter()
-    kw = dict(verbose=int(os.environ.get("SEM_VERBOSE", "0")))
+    kw = dict(verbose=int(os.environ.get("SEM_VERBOSE", "0")), overlap=args.overlap,
+              local_solve=1 if args.smoother == "fdm" else 0)
     if world > 1:
         kw.update(nranks=world, rank=rank, nccl_id=nccl_id)
     elif args.emulate_ranks > 1:
@@ -233,12 +237,12 @@ def main():
     us_s, b_s = s.bench_kernel("schwarz", 0, 20)
     us_a, b_a = s.bench_kernel("apply", 0, 20)
     ach = b_s / (us_s * 1e-6) / 1e9
-    roof = {"kernel": "k_schwarz (level 0, one sweep" + (", this rank's partition)" if world > 1 else ")"),
+    roof = {"kernel": ("k_fdm" if args.smoother == "fdm" else "k_schwarz") + " (level 0, one sweep" + (", this rank's partition)" if world > 1 else ")"),
             "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
             "alg_bytes_per_launch": b_s, "launch_us": us_s,
             "traffic_note": "ncu dram__bytes_read+write per launch in profiles/schwarz_r1_raw.csv (28.9 GB, N=1)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "when" in peaks else "fallback 6650 GB/s"}
-    if world == 1 and args.emulate_ranks <= 1 and args.config == "config3":
+    if world == 1 and args.emulate_ranks <= 1 and args.config == "config3" and args.smoother == "dense":
         roof["traffic"] = 28.92e9
     ach_a = b_a / (us_a * 1e-6) / 1e9
     apply = {"kernel": "k_apply_dmma<%d> (FP64 tensor cores)" % m.p, "us": us_a, "alg_bytes_per_launch": b_a,
@@ -272,7 +276,9 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config], "p": m.p, "n_dof": info["n_dof"], "n_free": n_free,
                        "n_elem": info["n_elem"], "levels": info["level_p"], "tol": args.tol, "nu": [3, 3],
-                       "smoother": "additive Schwarz, overlap 1, exact dense local inverses (eq 4.4-4.6)",
+                       "smoother": f"additive Schwarz, overlap {args.overlap}, " + (
+                           "exact dense local inverses (eq 4.4-4.6)" if args.smoother == "dense" else
+                           "FDM local solves of K_h(x)M_v + M_h(x)K_v (reading O33)"),
                        "outer": "PCG (Alg 4.3)", "coarse": f"P=1, {info['coarse_n']} free DOF "
                        + ("(dense inverse)" if info["coarse_n"] <= 46000 else "(Jacobi-PCG)"),
                        "l2": "inputs larger than L2: each V-cycle streams "

@@ -102,6 +102,12 @@ typedef struct {
                                  In both modes every vector argument of the compute calls stays a
                                  GLOBAL vector (library numbering of the whole mesh), replicated on
                                  every rank; outputs are complete on every rank.                    */
+  int local_solve;            /* Schwarz local solves: 0 (default) exact dense inverses of R_k A R_k^T
+                                 (eq 4.4); 1 fast diagonalisation of the separable operator
+                                 K_h (x) M_v + M_h (x) K_v on the product subdomain (reading O33,
+                                 Lottes & Fischer [FL05]): exact on straight prisms with flat
+                                 layers, needs a layered mesh (SEM_EUNSUPPORTED otherwise) and
+                                 nranks = 1.  Same subdomains (O15) and weights (eq 4.6).            */
 } sem_opts;
 
 typedef struct {
@@ -228,6 +234,12 @@ int sem_host_numbering(const sem_mesh *mesh, int p, int64_t *n_dof, int64_t *n_f
  * weights of eq 4.6 (0 on Dirichlet nodes).  Two-call pattern as above. */
 int sem_host_schwarz(const sem_mesh *mesh, int p, int overlap, int64_t *total, int64_t *off,
                      int32_t *idx, double *W);
+/* Subdomains of the FDM local solves (opts.local_solve = 1, reading O33) on
+ * level order p with `overlap`: off [n_prism+1], idx [total] sorted free node
+ * ids of each product subdomain H_k x V_k, W [n_dof] (eq 4.6).  Needs a layered
+ * mesh (SEM_EUNSUPPORTED otherwise).  Two-call pattern as above. */
+int sem_host_fdm(const sem_mesh *mesh, int p, int overlap, int64_t *total, int64_t *off, int32_t *idx,
+                 double *W);
 /* Column partition used by the partitioned solve (opts.nranks > 1), level
  * `level` of the default schedule of order p (>= 2), seen from `rank`:
  * sizes[5] = {elements held, elements owned, local nodes, neighbours, exchange

@@ -11,6 +11,7 @@ from ._capi import (  # noqa: F401
     Solver,
     default_opts,
     host_numbering,
+    host_fdm,
     host_partition,
     host_reference,
     host_schwarz,

@@ -27,7 +27,7 @@ class SemOpts(C.Structure):
                 ("atol", C.c_double), ("imax", C.c_int), ("stream", C.c_void_p), ("device", C.c_int),
                 ("verbose", C.c_int), ("apply_kernel", C.c_int), ("coarse_solver", C.c_int),
                 ("coarse_rtol", C.c_double), ("coarse_maxit", C.c_int), ("nranks", C.c_int), ("rank", C.c_int),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("local_solve", C.c_int)]
 
 
 class SemReport(C.Structure):
@@ -78,11 +78,12 @@ _lib.sem_last_error.restype = C.c_char_p
 _lib.sem_host_numbering.argtypes = [C.POINTER(SemMesh), C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                     _vp, _vp, _vp]
 _lib.sem_host_schwarz.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.POINTER(C.c_int64), _vp, _vp, _vp]
+_lib.sem_host_fdm.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.POINTER(C.c_int64), _vp, _vp, _vp]
 _lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.sem_host_partition.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp]
 
-EXPORTS = ["sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+EXPORTS = ["sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
            "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
            "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
            "sem_destroy", "sem_strerror", "sem_last_error"]
@@ -156,6 +157,21 @@ def host_schwarz(vertices, prisms, face_tag, p, overlap):
     W = np.zeros(dirm.size)
     _check(_lib.sem_host_schwarz(C.byref(m), p, overlap, None, C.c_void_p(off.ctypes.data),
                                  C.c_void_p(idx.ctypes.data), C.c_void_p(W.ctypes.data)), "sem_host_schwarz")
+    return [idx[off[k]:off[k + 1]] for k in range(E)], W
+
+
+def host_fdm(vertices, prisms, face_tag, p, overlap, node_xyz=None):
+    """sem_host_fdm: (list of FDM subdomain node arrays, W)."""
+    m, keep = _mesh_struct(vertices, prisms, face_tag, node_xyz)
+    tot = C.c_int64()
+    _check(_lib.sem_host_fdm(C.byref(m), p, overlap, C.byref(tot), None, None, None), "sem_host_fdm")
+    E = keep[1].shape[0]
+    _, dirm, _ = host_numbering(vertices, prisms, face_tag, p)
+    off = np.zeros(E + 1, dtype=np.int64)
+    idx = np.zeros(max(1, tot.value), dtype=np.int32)
+    W = np.zeros(dirm.size)
+    _check(_lib.sem_host_fdm(C.byref(m), p, overlap, None, C.c_void_p(off.ctypes.data),
+                             C.c_void_p(idx.ctypes.data), C.c_void_p(W.ctypes.data)), "sem_host_fdm")
     return [idx[off[k]:off[k + 1]] for k in range(E)], W
 
 

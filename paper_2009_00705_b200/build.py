@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = ["csrc/refelem.cpp", "csrc/topology.cpp", "csrc/partition.cpp", "csrc/kernels.cu", "csrc/apply_dmma.cu",
-       "csrc/capi.cu", "csrc/dist.cu"]
+       "csrc/capi.cu", "csrc/dist.cu", "csrc/fdm.cpp", "csrc/fdm.cu"]
 LIB = os.path.join(HERE, "libsem_pmg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -16,7 +16,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(HERE, s) for s in SRC]
-    deps = srcs + [os.path.join(HERE, "csrc", h) for h in ("internal.h", "refelem.h", "topology.h", "partition.h", "setup_util.h")] + \
+    deps = srcs + [os.path.join(HERE, "csrc", h) for h in ("internal.h", "refelem.h", "topology.h", "partition.h", "setup_util.h", "fdm.h")] + \
         [os.path.join(ROOT, "include", "sem_pmg.h")]
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps):
         return LIB

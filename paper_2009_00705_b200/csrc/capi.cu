@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "fdm.h"
 #include "internal.h"
 #include "partition.h"
 #include "setup_util.h"
@@ -234,7 +235,12 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }
 
+void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cublasHandle_t blas, int verbose);
+
 void check_opts(const sem_opts& o) {
+  if (o.local_solve < 0 || o.local_solve > 1) throw SemError(SEM_EINVAL, "bad options: local_solve");
+  if (o.local_solve == 1 && o.nranks > 1)
+    throw SemError(SEM_EUNSUPPORTED, "FDM local solves are single-domain only (nranks = 1)");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
       o.apply_kernel > 1 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
       o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
@@ -434,6 +440,11 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
         setup_schwarz(c, li, part->L[lid].S, blas, sol, d_D, o.verbose);
       } else if (gsch) {
         setup_schwarz(c, li, (*gsch)[lid], blas, sol, d_D, o.verbose);
+      } else if (o.local_solve == 1) {
+        const int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
+        FdmTopo F = fdm_topology(gm.hm, gm.topo[lid], gm.X, p, ov);
+        if (o.verbose) fprintf(stderr, "[sem] level p=%d FDM topology %.0f ms\n", c->L[li].p, now_ms() - t0);
+        setup_fdm(c, li, F, sol, blas, o.verbose);
       } else {
         const int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
         SchwarzTopo S = schwarz_topology(gm.topo[lid], E, ov, std::min(32, std::max(1, omp_get_max_threads())));
@@ -930,7 +941,9 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
     CUDA_CHECK(cudaEventElapsedTime(&ms, t->ev0, t->ev1));
     if (mean_us) *mean_us = 1e3 * ms / reps;
     if (alg_bytes) {
-      if (kernel == 0)
+      if (kernel == 0 && L.fdm)
+        *alg_bytes = (double)L.schwarz_bytes + 32.0 * L.n;
+      else if (kernel == 0)
         *alg_bytes = 8.0 * L.packed + 4.0 * L.nk_sum + 32.0 * L.n;
       else
         *alg_bytes = (double)t->E_own * (48.0 * L.Q + 4.0 * L.N) + 16.0 * L.n;
@@ -1062,6 +1075,40 @@ int sem_host_partition(const sem_mesh* mesh, int p, int nranks, int rank, int le
         if (xoff) xoff[j + 1] = o2;
       }
     }
+  } catch (const SemError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SEM_EINVAL;
+  }
+  return SEM_OK;
+}
+
+int sem_host_fdm(const sem_mesh* mesh, int p, int overlap, int64_t* total, int64_t* off, int32_t* idx, double* W) {
+  if (p < 1 || p > 8 || overlap < 0) return SEM_EINVAL;
+  try {
+    sem_opts o;
+    sem_default_opts(&o);
+    int lv[1] = {p};
+    if (p == 1) { o.levels = lv; o.n_levels = 1; }
+    GlobalModel gm;
+    prepare_global(mesh, p, o, gm);
+    FdmTopo F = fdm_topology(gm.hm, gm.topo[0], gm.X, p, overlap);
+    const int E = gm.hm.E;
+    std::vector<int64_t> o2(E + 1, 0);
+    std::vector<int32_t> all;
+    for (int e = 0; e < E; ++e) {
+      std::vector<int32_t> s;
+      for (int64_t t = F.ioff[e]; t < F.ioff[e + 1]; ++t)
+        if (F.idx[t] >= 0) s.push_back(F.idx[t]);
+      std::sort(s.begin(), s.end());
+      all.insert(all.end(), s.begin(), s.end());
+      o2[e + 1] = (int64_t)all.size();
+    }
+    if (total) *total = (int64_t)all.size();
+    if (off) std::copy(o2.begin(), o2.end(), off);
+    if (idx) std::copy(all.begin(), all.end(), idx);
+    if (W) std::copy(F.W.begin(), F.W.end(), W);
   } catch (const SemError& e) {
     return fail(e);
   } catch (const std::exception& e) {

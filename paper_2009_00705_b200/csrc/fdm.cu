@@ -1,0 +1,562 @@
+// FDM local solves of the Schwarz smoother on the GPU (reading O33; fdm.h).
+//
+// Setup: per column the generalised eigenproblem K_h S_h = M_h S_h L_h of its
+// horizontal patch, per element K_v S_v = M_v S_v L_v of its vertical box
+// (S^T M S = I), batched on the GPU: Cholesky M = L L^T (cuSOLVER
+// potrfBatched), C = L^-1 K L^-T (cuBLAS trsmBatched), C = Q L Q^T (cuSOLVER
+// XsyevBatched), S = L^-T Q.
+//
+// Apply (one sweep of eq 4.4 with the FDM local inverses):
+//   x = R_k r (x W for S^-T) ;  x <- (S_h (x) S_v)^T x ;  x /= (l_h,a + l_v,b) ;
+//   x <- (S_h (x) S_v) x ;  u += R_k^T x (x W for S^-1).
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "fdm.h"
+#include "internal.h"
+#include "setup_util.h"
+
+namespace sem {
+
+#define CUBLAS_OK(x)                                                                     \
+  do {                                                                                   \
+    cublasStatus_t _s = (x);                                                             \
+    if (_s != CUBLAS_STATUS_SUCCESS) throw SemError(SEM_ECUDA, std::string(#x) + " failed"); \
+  } while (0)
+#define CUSOLVER_OK(x)                                                                   \
+  do {                                                                                   \
+    cusolverStatus_t _s = (x);                                                           \
+    if (_s != CUSOLVER_STATUS_SUCCESS)                                                   \
+      throw SemError(SEM_ECUDA, std::string(#x) + " failed (status " + std::to_string((int)_s) + ")"); \
+  } while (0)
+
+__global__ void k_unpack_pairs(int n, const int64_t* __restrict__ off, const double* __restrict__ K,
+                               const double* __restrict__ M, double* __restrict__ Kp, double* __restrict__ Mp) {
+  const int b = blockIdx.x;
+  const double* k = K + off[b];
+  const double* m = M + off[b];
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) {  // symmetric: row-major = column-major
+    Kp[(size_t)b * n * n + t] = k[t];
+    Mp[(size_t)b * n * n + t] = m[t];
+  }
+}
+
+// S (column-major [n][n], eigenvectors in columns) -> packed row-major S[i][a] (i node, a mode)
+__global__ void k_pack_modes(int n, const int64_t* __restrict__ off, const int64_t* __restrict__ loff,
+                             const double* __restrict__ Sp, const double* __restrict__ Wp, double* __restrict__ S,
+                             double* __restrict__ lam) {
+  const int b = blockIdx.x;
+  const double* sp = Sp + (size_t)b * n * n;
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+    const int i = t / n, a = t % n;
+    S[off[b] + t] = sp[i + (size_t)n * a];
+  }
+  for (int a = threadIdx.x; a < n; a += blockDim.x) lam[loff[b] + a] = Wp[(size_t)b * n + a];
+}
+
+// Generalised symmetric-definite eigenproblems K S = M S L for packed problems
+// (sizes n[b], row-major blocks at off[b]); S packed the same way (device dS),
+// eigenvalues at loff[b] (device dlam).  Problems are batched by size (no
+// padding, so the eigensolver's backward error stays relative to each problem).
+static void batched_geneig(sem_ctx* c, cusolverDnHandle_t sol, cublasHandle_t blas, const std::vector<int32_t>& n,
+                           const std::vector<int64_t>& off, const std::vector<double>& K, const std::vector<double>& M,
+                           const std::vector<int64_t>& loff, double* dS, double* dlam) {
+  const int nb_all = (int)n.size();
+  if (nb_all == 0) return;
+  Scratch s0;
+  double* dK = s0.put(K);
+  double* dM = s0.put(M);
+  std::vector<std::vector<int>> bysize(*std::max_element(n.begin(), n.end()) + 1);
+  for (int b = 0; b < nb_all; ++b) bysize[n[b]].push_back(b);
+  cusolverDnParams_t params;
+  CUSOLVER_OK(cusolverDnCreateParams(&params));
+  struct PG {
+    cusolverDnParams_t p;
+    ~PG() { cusolverDnDestroyParams(p); }
+  } pg{params};
+  const double one = 1.0;
+  for (int np = 1; np < (int)bysize.size(); ++np) {
+    const std::vector<int>& list = bysize[np];
+    if (list.empty()) continue;
+    size_t freeb = 0, totb = 0;
+    CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
+    const size_t per = (size_t)np * np * 8 * 2 + (size_t)np * 8 + 64;
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>(std::min<size_t>((size_t)(freeb * 0.3) / per, 16384),
+                                                                list.size()));
+    Scratch sc;
+    double* Kp = sc.get<double>((size_t)chunk * np * np);
+    double* Mp = sc.get<double>((size_t)chunk * np * np);
+    double* Wp = sc.get<double>((size_t)chunk * np);
+    double** pK = sc.get<double*>(chunk);
+    double** pM = sc.get<double*>(chunk);
+    int* info = sc.get<int>(chunk);
+    {
+      std::vector<double*> hK(chunk), hM(chunk);
+      for (int i = 0; i < chunk; ++i) {
+        hK[i] = Kp + (size_t)i * np * np;
+        hM[i] = Mp + (size_t)i * np * np;
+      }
+      CUDA_CHECK(cudaMemcpy(pK, hK.data(), chunk * sizeof(double*), cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(pM, hM.data(), chunk * sizeof(double*), cudaMemcpyHostToDevice));
+    }
+    std::vector<int> hinfo(chunk);
+    for (size_t b0 = 0; b0 < list.size(); b0 += chunk) {
+      const int nb = (int)std::min<size_t>(chunk, list.size() - b0);
+      std::vector<int64_t> o(nb), lo(nb);
+      for (int i = 0; i < nb; ++i) {
+        o[i] = off[list[b0 + i]];
+        lo[i] = loff[list[b0 + i]];
+      }
+      Scratch s2;
+      const int64_t* doff = s2.put(o);
+      const int64_t* dloff = s2.put(lo);
+      k_unpack_pairs<<<nb, 256, 0, c->stream>>>(np, doff, dK, dM, Kp, Mp);
+      CUDA_CHECK(cudaGetLastError());
+      CUSOLVER_OK(cusolverDnDpotrfBatched(sol, CUBLAS_FILL_MODE_LOWER, np, pM, np, info, nb));
+      CUDA_CHECK(cudaMemcpyAsync(hinfo.data(), info, nb * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      for (int i = 0; i < nb; ++i)
+        if (hinfo[i] != 0)
+          throw SemError(SEM_ESINGULAR, "FDM mass matrix not SPD (potrf info " + std::to_string(hinfo[i]) + ")");
+      // C = L^-1 K L^-T
+      CUBLAS_OK(cublasDtrsmBatched(blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                                   np, np, &one, (const double* const*)pM, np, pK, np, nb));
+      CUBLAS_OK(cublasDtrsmBatched(blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                   np, np, &one, (const double* const*)pM, np, pK, np, nb));
+      // C = Q L Q^T
+      size_t wdev = 0, whost = 0;
+      CUSOLVER_OK(cusolverDnXsyevBatched_bufferSize(sol, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np,
+                                                    CUDA_R_64F, Kp, np, CUDA_R_64F, Wp, CUDA_R_64F, &wdev, &whost, nb));
+      void* bdev = s2.get<char>(wdev);
+      std::vector<char> bhost(std::max<size_t>(whost, 1));
+      CUSOLVER_OK(cusolverDnXsyevBatched(sol, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np, CUDA_R_64F,
+                                         Kp, np, CUDA_R_64F, Wp, CUDA_R_64F, bdev, wdev, bhost.data(), whost, info,
+                                         nb));
+      CUDA_CHECK(cudaMemcpyAsync(hinfo.data(), info, nb * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      for (int i = 0; i < nb; ++i)
+        if (hinfo[i] != 0)
+          throw SemError(SEM_ESINGULAR, "FDM eigensolver failed (info " + std::to_string(hinfo[i]) + ")");
+      // S = L^-T Q
+      CUBLAS_OK(cublasDtrsmBatched(blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                   np, np, &one, (const double* const*)pM, np, pK, np, nb));
+      k_pack_modes<<<nb, 256, 0, c->stream>>>(np, doff, dloff, Kp, Wp, dS, dlam);
+      CUDA_CHECK(cudaGetLastError());
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    }
+  }
+}
+
+constexpr int FDM_NT = 8;     // n-tiles (of 8 box columns) per work unit
+constexpr int FDM_NC = 8 * FDM_NT;
+constexpr int FDM_LD = 72;    // shared-memory row stride in doubles (= 8 mod 16: conflict-free B-fragment reads)
+
+// S_v, l_v of every element zero-padded to [nvp][nvp] / [nvp] (pad eigenvalue 1)
+__global__ void k_pad_vertical(int E, int nvp, const int32_t* __restrict__ nv, const int64_t* __restrict__ voff,
+                               const int64_t* __restrict__ lvoff, const double* __restrict__ Sv,
+                               const double* __restrict__ lv, double* __restrict__ Svp, double* __restrict__ lvp) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int n = nv[e];
+  for (int a = 0; a < nvp; ++a) {
+    lvp[(size_t)e * nvp + a] = a < n ? lv[lvoff[e] + a] : 1.0;
+    for (int b = 0; b < nvp; ++b)
+      Svp[((size_t)e * nvp + a) * nvp + b] = (a < n && b < n) ? Sv[voff[e] + a * n + b] : 0.0;
+  }
+}
+
+void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cublasHandle_t blas, int verbose) {
+  DeviceLevel& L = c->L[li];
+  const double t0 = now_ms();
+  const int E = (int)F.col.size();
+  const int ncol = F.ncol;
+  // horizontal (per column) and vertical (per element) eigenpairs
+  std::vector<int32_t> nh(ncol), nv(E);
+  std::vector<int64_t> lhoff(ncol), lvoff(E);
+  for (int q = 0; q < ncol; ++q) {
+    nh[q] = (int32_t)(F.hoff[q + 1] - F.hoff[q]);
+    lhoff[q] = F.hoff[q];
+  }
+  int64_t acc = 0;
+  for (int e = 0; e < E; ++e) {
+    nv[e] = F.nv[e];
+    lvoff[e] = acc;
+    acc += nv[e];
+  }
+  L.f_Sh = dalloc<double>(c, F.moff[ncol]);
+  L.f_lh = dalloc<double>(c, F.hoff[ncol]);
+  L.f_Sv = dalloc<double>(c, F.voff[E]);
+  L.f_lv = dalloc<double>(c, acc);
+  batched_geneig(c, sol, blas, nh, std::vector<int64_t>(F.moff.begin(), F.moff.end() - 1), F.Kh, F.Mh, lhoff, L.f_Sh,
+                 L.f_lh);
+  batched_geneig(c, sol, blas, nv, std::vector<int64_t>(F.voff.begin(), F.voff.end() - 1), F.Kv, F.Mv, lvoff, L.f_Sv,
+                 L.f_lv);
+  L.f_col = upload(c, F.col);
+  L.f_hoff = upload(c, F.hoff);
+  L.f_moff = upload(c, F.moff);
+  L.f_nv = upload(c, F.nv);
+  L.f_voff = upload(c, F.voff);
+  L.f_lvoff = upload(c, lvoff);
+  L.f_ioff = upload(c, F.ioff);
+  L.f_idx = upload(c, F.idx);
+  L.W = upload(c, F.W);
+  L.f_colel = upload(c, F.colel);
+  L.f_nzc = upload(c, F.nzc);
+  L.f_cioff = upload(c, F.cioff);
+  L.f_cidx = upload(c, F.cidx);
+  L.f_z0 = upload(c, F.z0);
+  {  // column-batched kernel: every element's box padded to NVT n-tiles of 8 columns,
+     // work units = runs of <= FDM_NT / NVT consecutive elements of one column
+    const int nvt = (F.nv_max + 7) / 8, nvp = 8 * nvt;
+    L.f_nvt = nvt;
+    L.f_mt = (F.nh_max + 7) / 8;
+    std::vector<int4> units;
+    const int per = FDM_NT / nvt;
+    for (int q = 0; q < ncol; ++q)
+      for (int64_t j = F.cfirst[q]; j < F.cfirst[q + 1]; j += per)
+        units.push_back(make_int4(q, (int)j, (int)std::min<int64_t>(per, F.cfirst[q + 1] - j), 0));
+    L.f_units = upload(c, units);
+    L.f_nunits = (int)units.size();
+    L.f_Svp = dalloc<double>(c, (size_t)E * nvp * nvp);
+    L.f_lvp = dalloc<double>(c, (size_t)E * nvp);
+    k_pad_vertical<<<(E + 127) / 128, 128, 0, c->stream>>>(E, nvp, L.f_nv, L.f_voff, L.f_lvoff, L.f_Sv, L.f_lv,
+                                                          L.f_Svp, L.f_lvp);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  }
+  L.fdm = 1;
+  L.f_nh_max = F.nh_max;
+  L.f_nv_max = F.nv_max;
+  L.nk_sum = 0;
+  for (int32_t g : F.idx) L.nk_sum += (g >= 0);
+  // algorithmic bytes of one sweep (column-batched kernel): per column S_h, l_h and the patch
+  // node ids [n_h][Z_c+1]; per element S_v, l_v
+  L.schwarz_bytes = 8 * (F.moff[ncol] + F.hoff[ncol] + F.voff[E] + acc) + 4 * F.cioff[ncol];
+  L.packed = 0;
+  if (verbose)
+    fprintf(stderr, "[sem] level p=%d FDM: %d columns, n_h max %d, n_v max %d, %.1f MiB, %.0f ms\n", L.p, ncol,
+            F.nh_max, F.nv_max, L.schwarz_bytes / 1048576.0, now_ms() - t0);
+}
+
+// ---------------------------------------------------------------- apply
+// One CTA per subdomain k.  Box x[a][b], a over the column's patch (n_h), b
+// over the element's vertical range (n_v).
+__global__ void __launch_bounds__(256) k_fdm(const int32_t* __restrict__ col, const int64_t* __restrict__ hoff,
+                                             const int64_t* __restrict__ moff, const int32_t* __restrict__ nvv,
+                                             const int64_t* __restrict__ voff, const int64_t* __restrict__ lvoff,
+                                             const int64_t* __restrict__ ioff, const int32_t* __restrict__ idx,
+                                             const double* __restrict__ Sh, const double* __restrict__ lh,
+                                             const double* __restrict__ Sv, const double* __restrict__ lv,
+                                             const double* __restrict__ W, const double* __restrict__ r,
+                                             double* __restrict__ u, int transpose, int box_max) {
+  extern __shared__ double sm[];
+  const int k = blockIdx.x;
+  const int c = col[k];
+  const int nh = (int)(hoff[c + 1] - hoff[c]);
+  const int nv = nvv[k];
+  const int nb = nh * nv;
+  double* X = sm;             // [nh][nv]
+  double* T = sm + box_max;   // [nh][nv]
+  double* sv = T + box_max;   // [nv][nv]
+  const int32_t* id = idx + ioff[k];
+  const double* S = Sh + moff[c];      // S[i][a]
+  const double* Lh = lh + hoff[c];
+  const double* Lv = lv + lvoff[k];
+  for (int t = threadIdx.x; t < nv * nv; t += blockDim.x) sv[t] = Sv[voff[k] + t];
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    const int g = id[t];
+    double v = 0.0;
+    if (g >= 0) {
+      v = r[g];
+      if (transpose) v *= W[g];
+    }
+    X[t] = v;
+  }
+  __syncthreads();
+  // T[a][b] = sum_i S[i][a] X[i][b]
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    const int a = t / nv, b = t % nv;
+    double s = 0.0;
+    for (int i = 0; i < nh; ++i) s = fma(__ldg(S + (size_t)i * nh + a), X[i * nv + b], s);
+    T[t] = s;
+  }
+  __syncthreads();
+  // X[a][j] = sum_b T[a][b] S_v[b][j] / (l_h,a + l_v,j)
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    const int a = t / nv, j = t % nv;
+    double s = 0.0;
+    for (int b = 0; b < nv; ++b) s = fma(T[a * nv + b], sv[b * nv + j], s);
+    X[t] = s / (__ldg(Lh + a) + __ldg(Lv + j));
+  }
+  __syncthreads();
+  // T[a][b] = sum_j X[a][j] S_v[b][j]
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    const int a = t / nv, b = t % nv;
+    double s = 0.0;
+    for (int j = 0; j < nv; ++j) s = fma(X[a * nv + j], sv[b * nv + j], s);
+    T[t] = s;
+  }
+  __syncthreads();
+  // y[i][b] = sum_a S[i][a] T[a][b]; u += R_k^T y
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    const int g = id[t];
+    if (g < 0) continue;
+    const int i = t / nv, b = t % nv;
+    double s = 0.0;
+    const double* Si = S + (size_t)i * nh;
+    for (int a = 0; a < nh; ++a) s = fma(__ldg(Si + a), T[a * nv + b], s);
+    if (!transpose) s *= W[g];
+    atomicAdd(u + g, s);
+  }
+}
+
+
+__device__ __forceinline__ void fdm_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Column-batched FDM sweep on FP64 tensor cores.  One CTA per work unit = a run
+// of consecutive layers of one column: they share S_h, l_h and the patch.
+// Each element's box is padded to NVT n-tiles of 8 columns and the boxes are
+// laid side by side in B [n_h][unit columns], so every contraction is a small
+// GEMM on mma.sync.m8n8k4.f64 (fragments: A a0 = A[lane>>2][lane&3], B b0 =
+// B[lane&3][lane>>2], C c_i = C[lane>>2][2(lane&3)+i]):
+//   T  = S_h^T B                          (per warp job: one m-tile x one element)
+//   T <- ((T S_v) ./ (l_h + l_v)) S_v^T   (same warp, in registers: the C fragment
+//                                          is re-laid out as an A fragment by shuffles)
+//   Y  = S_h T
+// then every column node sums the boxes holding it (<= 3) and is scattered.
+// MT = ceil(n_h_max / 8) m-tiles (k padded to 8 MT), NVT = ceil(n_v_max / 8).
+template <int NVT>
+__device__ __forceinline__ double c_to_a(const double (&acc)[NVT][2], int kt, int lane) {
+  // A fragment (row lane>>2, col kt*4 + (lane&3)) of the 8 x 8NVT tile held as C fragments
+  const int src = (lane & ~3) | (((kt & 1) << 1) + ((lane & 3) >> 1));
+  const double x0 = __shfl_sync(0xffffffffu, acc[kt >> 1][0], src);
+  const double x1 = __shfl_sync(0xffffffffu, acc[kt >> 1][1], src);
+  return (lane & 1) ? x1 : x0;
+}
+
+template <int MT, int NVT>
+__global__ void __launch_bounds__(256) k_fdm_col(const int4* __restrict__ units, const int32_t* __restrict__ colel,
+                                                 const int64_t* __restrict__ hoff, const int64_t* __restrict__ moff,
+                                                 const int64_t* __restrict__ cioff, const int32_t* __restrict__ nzc,
+                                                 const int32_t* __restrict__ cidx, const int32_t* __restrict__ z0,
+                                                 const int32_t* __restrict__ nvv, const double* __restrict__ Sh,
+                                                 const double* __restrict__ lh, const double* __restrict__ Svp,
+                                                 const double* __restrict__ lvp, const double* __restrict__ W,
+                                                 const double* __restrict__ r, double* __restrict__ u, int transpose) {
+  constexpr int ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, EMAX = FDM_NT / NVT, LD = FDM_LD;
+  extern __shared__ __align__(16) double sm[];
+  double* Bc = sm;              // [ROWS][LD]  boxes, later Y
+  double* Tm = Bc + ROWS * LD;  // [ROWS][LD]  column block R[h][z - zlo] first, then T
+  __shared__ int ez0[EMAX], env[EMAX], eid[EMAX];
+  const int4 U = units[blockIdx.x];
+  const int c = U.x, first = U.y, cnt = U.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nh = (int)(hoff[c + 1] - hoff[c]);
+  const int nz = nzc[c];
+  const int32_t* ci = cidx + cioff[c];
+  const double* S = Sh + moff[c];
+  const double* Lh = lh + hoff[c];
+  if (tid < cnt) {
+    const int e = colel[first + tid];
+    eid[tid] = e;
+    ez0[tid] = z0[e];
+    env[tid] = nvv[e];
+  }
+  __syncthreads();
+  const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
+  // 1. gather the unit's column block R[h][z] (x W for S^-T) into Tm
+  for (int t = tid; t < nh * nzu; t += blockDim.x) {
+    const int h = t / nzu, zz = t - h * nzu;
+    const int g = ci[h * nz + zlo + zz];
+    double v = 0.0;
+    if (g >= 0) {
+      v = r[g];
+      if (transpose) v *= W[g];
+    }
+    Tm[h * LD + zz] = v;
+  }
+  __syncthreads();
+  // 2. expand into padded boxes B[h][j*NVP + b] (zero rows >= nh, zero padding columns)
+  for (int t = tid; t < ROWS * FDM_NC; t += blockDim.x) {
+    const int h = t / FDM_NC, col = t - h * FDM_NC, j = col / NVP, b = col - j * NVP;
+    double v = 0.0;
+    if (h < nh && j < cnt && b < env[j]) v = Tm[h * LD + ez0[j] - zlo + b];
+    Bc[h * LD + col] = v;
+  }
+  __syncthreads();
+  // 3. T = S_h^T B, vertical transform in registers, T -> Tm
+  for (int job = warp; job < MT * cnt; job += 8) {
+    const int mt = job / cnt, j = job - mt * cnt;
+    const int e = eid[j];
+    double acc[NVT][2];
+#pragma unroll
+    for (int n = 0; n < NVT; ++n) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const int i = kt * 4 + (lane & 3), a = mt * 8 + (lane >> 2);
+      const double af = (i < nh && a < nh) ? __ldg(S + i * nh + a) : 0.0;
+      const double* bp = Bc + (kt * 4 + (lane & 3)) * LD + j * NVP + (lane >> 2);
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) fdm_dmma(acc[n][0], acc[n][1], af, bp[8 * n]);
+    }
+    // V = T S_v (k over b)
+    const double* sv = Svp + (size_t)e * NVP * NVP;
+    double v[NVT][2];
+#pragma unroll
+    for (int n = 0; n < NVT; ++n) v[n][0] = v[n][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < 2 * NVT; ++kt) {
+      const double a = c_to_a<NVT>(acc, kt, lane);
+#pragma unroll
+      for (int n = 0; n < NVT; ++n)
+        fdm_dmma(v[n][0], v[n][1], a, __ldg(sv + (kt * 4 + (lane & 3)) * NVP + n * 8 + (lane >> 2)));
+    }
+    // V ./= (l_h,a + l_v,jj)
+    {
+      const int a = mt * 8 + (lane >> 2);
+      const double la = a < nh ? __ldg(Lh + a) : 1.0;
+      const double* lv = lvp + (size_t)e * NVP;
+#pragma unroll
+      for (int n = 0; n < NVT; ++n)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) v[n][i] /= (la + __ldg(lv + n * 8 + 2 * (lane & 3) + i));
+    }
+    // T = V S_v^T (k over jj): B[k=jj][n=b] = S_v[b][jj]
+#pragma unroll
+    for (int n = 0; n < NVT; ++n) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < 2 * NVT; ++kt) {
+      const double a = c_to_a<NVT>(v, kt, lane);
+#pragma unroll
+      for (int n = 0; n < NVT; ++n)
+        fdm_dmma(acc[n][0], acc[n][1], a, __ldg(sv + (n * 8 + (lane >> 2)) * NVP + kt * 4 + (lane & 3)));
+    }
+#pragma unroll
+    for (int n = 0; n < NVT; ++n)
+      *reinterpret_cast<double2*>(Tm + (mt * 8 + (lane >> 2)) * LD + j * NVP + n * 8 + 2 * (lane & 3)) =
+          make_double2(acc[n][0], acc[n][1]);
+  }
+  __syncthreads();
+  // 4. Y = S_h T -> Bc   (A[m=i][k=a] = S[i][a]); rows a >= nh of T are zero
+  for (int job = warp; job < MT * cnt; job += 8) {
+    const int mt = job / cnt, j = job - mt * cnt;
+    double acc[NVT][2];
+#pragma unroll
+    for (int n = 0; n < NVT; ++n) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const int i = mt * 8 + (lane >> 2), a = kt * 4 + (lane & 3);
+      const double af = (i < nh && a < nh) ? __ldg(S + i * nh + a) : 0.0;
+      const double* bp = Tm + (kt * 4 + (lane & 3)) * LD + j * NVP + (lane >> 2);
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) fdm_dmma(acc[n][0], acc[n][1], af, bp[8 * n]);
+    }
+#pragma unroll
+    for (int n = 0; n < NVT; ++n)
+      *reinterpret_cast<double2*>(Bc + (mt * 8 + (lane >> 2)) * LD + j * NVP + n * 8 + 2 * (lane & 3)) =
+          make_double2(acc[n][0], acc[n][1]);
+  }
+  __syncthreads();
+  // 5. every column node of the unit sums the boxes holding it, scatter (x W for S^-1)
+  for (int t = tid; t < nh * nzu; t += blockDim.x) {
+    const int h = t / nzu, zz = t - h * nzu;
+    const int g = ci[h * nz + zlo + zz];
+    if (g < 0) continue;
+    const int z = zlo + zz;
+    double s = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < cnt; ++j) {
+      const int dz = z - ez0[j];
+      if (dz >= 0 && dz < env[j]) s += Bc[h * LD + j * NVP + dz];
+    }
+    if (!transpose) s *= W[g];
+    atomicAdd(u + g, s);
+  }
+}
+
+template <int MT, int NVT>
+static void fdm_col_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
+  {
+    const cudaError_t pending = cudaGetLastError();
+    if (pending != cudaSuccess)
+      throw SemError(SEM_ECUDA, std::string("error pending before the FDM sweep: ") + cudaGetErrorString(pending));
+  }
+  const int smem = 2 * 8 * MT * FDM_LD * (int)sizeof(double);
+  static int attr = 0;  // opt in whenever the request grows (static smem counts against the 48 KB default)
+  if (smem > attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_fdm_col<MT, NVT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  k_fdm_col<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
+                                                            L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
+                                                            L.f_Svp, L.f_lvp, L.W, r, u, transpose);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+template <int NVT>
+static void fdm_col_dispatch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
+  switch (L.f_mt) {
+    case 1: fdm_col_launch<1, NVT>(c, L, r, u, transpose); break;
+    case 2: fdm_col_launch<2, NVT>(c, L, r, u, transpose); break;
+    case 3: fdm_col_launch<3, NVT>(c, L, r, u, transpose); break;
+    case 4: fdm_col_launch<4, NVT>(c, L, r, u, transpose); break;
+    case 5: fdm_col_launch<5, NVT>(c, L, r, u, transpose); break;
+    case 6: fdm_col_launch<6, NVT>(c, L, r, u, transpose); break;
+    case 7: fdm_col_launch<7, NVT>(c, L, r, u, transpose); break;
+    case 8: fdm_col_launch<8, NVT>(c, L, r, u, transpose); break;
+    case 9: fdm_col_launch<9, NVT>(c, L, r, u, transpose); break;
+    case 10: fdm_col_launch<10, NVT>(c, L, r, u, transpose); break;
+    case 11: fdm_col_launch<11, NVT>(c, L, r, u, transpose); break;
+    case 12: fdm_col_launch<12, NVT>(c, L, r, u, transpose); break;
+    case 13: fdm_col_launch<13, NVT>(c, L, r, u, transpose); break;
+    case 14: fdm_col_launch<14, NVT>(c, L, r, u, transpose); break;
+    case 15: fdm_col_launch<15, NVT>(c, L, r, u, transpose); break;
+    default: fdm_col_launch<16, NVT>(c, L, r, u, transpose); break;
+  }
+}
+
+static int fdm_simple() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("SEM_FDM_SIMPLE");
+    v = (s && atoi(s)) ? 1 : 0;
+  }
+  return v;
+}
+
+void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose) {
+  const DeviceLevel& L = c->L[level];
+  if (c->E_own == 0) return;
+  if (!fdm_simple() && L.f_mt <= 16 && L.f_nvt <= 3) {
+    if (L.f_nvt == 1) fdm_col_dispatch<1>(c, L, r, u, transpose);
+    else if (L.f_nvt == 2) fdm_col_dispatch<2>(c, L, r, u, transpose);
+    else fdm_col_dispatch<3>(c, L, r, u, transpose);
+    c->launches++;
+    return;
+  }
+  const int box = L.f_nh_max * L.f_nv_max;
+  const int smem = (2 * box + L.f_nv_max * L.f_nv_max) * (int)sizeof(double);
+  static int attr = 0;
+  if (smem > attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_fdm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  k_fdm<<<c->E_own, 256, smem, c->stream>>>(L.f_col, L.f_hoff, L.f_moff, L.f_nv, L.f_voff, L.f_lvoff, L.f_ioff,
+                                            L.f_idx, L.f_Sh, L.f_lh, L.f_Sv, L.f_lv, L.W, r, u, transpose, box);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+}  // namespace sem

@@ -49,6 +49,20 @@ struct DeviceLevel {
   int64_t* tile_off = nullptr;  // [E+1] offsets in doubles into tiles
   double* tiles = nullptr;
   double* W = nullptr;          // [n]
+  // FDM local solves (opts.local_solve = 1; fdm.cu, reading O33)
+  int fdm = 0, f_nh_max = 0, f_nv_max = 0;
+  int32_t* f_col = nullptr;     // [E] column of every element
+  int64_t *f_hoff = nullptr, *f_moff = nullptr;   // [ncol+1] patch / S_h offsets
+  int32_t* f_nv = nullptr;      // [E] vertical box size
+  int64_t *f_voff = nullptr, *f_lvoff = nullptr, *f_ioff = nullptr;   // [E(+1)] S_v / l_v / index offsets
+  int32_t* f_idx = nullptr;     // box node ids (h outer, z inner), -1 = absent / Dirichlet
+  double *f_Sh = nullptr, *f_lh = nullptr, *f_Sv = nullptr, *f_lv = nullptr;
+  // column-batched kernel: work units (column, first element slot, elements, box columns)
+  int4* f_units = nullptr;
+  int f_nunits = 0, f_mt = 0, f_nvt = 0;
+  double *f_Svp = nullptr, *f_lvp = nullptr;   // [E][8 nvt][8 nvt] / [E][8 nvt] zero-padded S_v, l_v
+  int32_t *f_colel = nullptr, *f_nzc = nullptr, *f_cidx = nullptr, *f_z0 = nullptr;
+  int64_t* f_cioff = nullptr;
   int64_t schwarz_bytes = 0;
   int64_t nk_sum = 0, packed = 0;
   int max_tiles_1d = 0;
@@ -132,6 +146,7 @@ void launch_apply_dmma(sem_ctx* c, int level, const double* u, double* y, int fl
 std::vector<double> dmma_fragments(const LevelRef& R);
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);
 void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose);
+void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose);
 void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc);
 void launch_prolong(sem_ctx* c, int level, const double* uc, double* uf);
 void launch_coarse(sem_ctx* c, const double* r, double* z);

@@ -344,6 +344,10 @@ __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sid
 
 void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose) {
   const DeviceLevel& L = c->L[level];
+  if (L.fdm) {
+    launch_fdm(c, level, r, u, transpose);
+    return;
+  }
   const int npad = 16 * L.max_tiles_1d;
   const int smem = 9 * npad * (int)sizeof(double);
   static int attr_set = 0;

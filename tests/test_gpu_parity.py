@@ -47,7 +47,8 @@ class Case:
             perm = lib_to_oracle(self.s.node_xyz(li), lev.xyz)
             self.levels.append((lev, perm))
         self.mg = pmg.PMG(m, schedule=self.s.info["level_p"], nu1=kw.get("nu1", 3), nu2=kw.get("nu2", 3),
-                          overlap=kw.get("overlap", 1), literal=bool(kw.get("literal_smoother", 0))) if build_mg else None
+                          overlap=kw.get("overlap", 1), literal=bool(kw.get("literal_smoother", 0)),
+                          local_solve="fdm" if kw.get("local_solve", 0) == 1 else "dense") if build_mg else None
 
     def to_lib(self, li, v_orc_full):
         lev, perm = self.levels[li]

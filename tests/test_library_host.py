@@ -97,3 +97,32 @@ def test_host_numbering_rejects_bad_input():
     tags[0, 0] = 7
     with pytest.raises(lib.SemError):
         lib.host_numbering(m.vertices, m.prisms, tags, 2)
+
+
+@pytest.mark.parametrize("p,overlap", [(3, 0), (3, 1), (2, 2), (4, 3)])
+def test_fdm_sets_match_oracle(p, overlap):
+    """FDM product subdomains H_k x V_k (reading O33): the library (prism stacking)
+    and the oracle (lines found by coordinates) build the same node sets and W."""
+    from oracle import fdm
+    m = config3(p=p, n=4, nz=3)
+    conn, dirm, _ = lib.host_numbering(m.vertices, m.prisms, m.face_tag, p)
+    lev = sem.build_level(m, p)
+    perm = lib_to_oracle(lib_node_xyz(m, conn, lib.reference_nodes(p)), lev.xyz)
+    sets, W = lib.host_fdm(m.vertices, m.prisms, m.face_tag, p, overlap,
+                           node_xyz=m.node_xyz(lib.reference_nodes(m.p)))
+    blocks = fdm.fdm_blocks(m, lev, overlap)
+    cnt = np.zeros(lev.n)
+    for k, (ids, _) in enumerate(blocks):
+        np.testing.assert_array_equal(np.sort(perm[sets[k]]), np.sort(ids))
+        cnt[ids] += 1
+    Wo = np.where(lev.dirichlet, 0.0, 1.0 / np.maximum(cnt, 1))
+    np.testing.assert_allclose(W, Wo[perm], rtol=0, atol=0)
+
+
+def test_fdm_rejects_unlayered_mesh():
+    """Two prisms on the same bottom triangle: not a stack of layers."""
+    m = config1(p=2, nx=1, ny=1, nz=2)
+    prisms = m.prisms.copy()
+    prisms[1, :3] = prisms[0, :3]
+    with pytest.raises(lib.SemError):
+        lib.host_fdm(m.vertices, prisms, m.face_tag, 2, 1)

@@ -1,0 +1,17 @@
+"""Time one FDM sweep (k_fdm_col) and one operator apply on a config, finest level."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2009_00705_b200 as lib
+from workloads import config3
+
+ov = int(os.environ.get("OV", "1"))
+m = config3()
+s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
+               local_solve=1, overlap=ov, verbose=1)
+for li in range(s.info["n_levels"] - 1):
+    us, b = s.bench_kernel("schwarz", li, int(os.environ.get("REPS", "20")))
+    print(f"level {li} p={s.info['level_p'][li]} fdm sweep {us:.1f} us  alg {b/1e6:.1f} MB  {b/us/1e3:.0f} GB/s")
