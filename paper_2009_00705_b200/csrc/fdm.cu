@@ -157,6 +157,7 @@ static void batched_geneig(sem_ctx* c, cusolverDnHandle_t sol, cublasHandle_t bl
 
 constexpr int FDM_NT = 8;     // n-tiles (of 8 box columns) per work unit
 constexpr int FDM_NC = 8 * FDM_NT;
+constexpr int FDM_LDR_MAX = 76;  // column-block row stride bound of the warp kernel (= 4 mod 8)
 constexpr int FDM_LD = 72;    // shared-memory row stride in doubles (= 8 mod 16: conflict-free B-fragment reads)
 
 // S_v, l_v of every element zero-padded to [nvp][nvp] / [nvp] (pad eigenvalue 1)
@@ -219,12 +220,29 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
     L.f_nvt = nvt;
     L.f_mt = (F.nh_max + 7) / 8;
     std::vector<int4> units;
-    const int per = FDM_NT / nvt;
+    L.f_warp = (L.f_mt <= 8 && nvt <= 2) ? 1 : 0;
+    const int per = L.f_warp ? 8 : FDM_NT / nvt;
     for (int q = 0; q < ncol; ++q)
       for (int64_t j = F.cfirst[q]; j < F.cfirst[q + 1]; j += per)
         units.push_back(make_int4(q, (int)j, (int)std::min<int64_t>(per, F.cfirst[q + 1] - j), 0));
     L.f_units = upload(c, units);
     L.f_nunits = (int)units.size();
+    int nzu_max = 1;
+    for (const int4& un : units) {
+      const int e0 = F.colel[un.y], e1 = F.colel[un.y + un.z - 1];
+      nzu_max = std::max(nzu_max, F.z0[e1] + F.nv[e1] - F.z0[e0]);
+    }
+    L.f_ldr = nzu_max + ((4 - nzu_max % 8) + 8) % 8;  // >= nzu_max, = 4 mod 8
+    if (L.f_ldr > FDM_LDR_MAX && L.f_warp) {  // rebuild with the column kernel's units
+      L.f_warp = 0;
+      units.clear();
+      const int per2 = FDM_NT / nvt;
+      for (int q = 0; q < ncol; ++q)
+        for (int64_t j = F.cfirst[q]; j < F.cfirst[q + 1]; j += per2)
+          units.push_back(make_int4(q, (int)j, (int)std::min<int64_t>(per2, F.cfirst[q + 1] - j), 0));
+      L.f_units = upload(c, units);
+      L.f_nunits = (int)units.size();
+    }
     L.f_Svp = dalloc<double>(c, (size_t)E * nvp * nvp);
     L.f_lvp = dalloc<double>(c, (size_t)E * nvp);
     k_pad_vertical<<<(E + 127) / 128, 128, 0, c->stream>>>(E, nvp, L.f_nv, L.f_voff, L.f_lvoff, L.f_Sv, L.f_lv,
@@ -486,6 +504,243 @@ __global__ void __launch_bounds__(256) k_fdm_col(const int4* __restrict__ units,
   }
 }
 
+// Warp-per-element FDM sweep (MT <= 8, NVT <= 2).  One CTA per work unit of
+// <= 8 consecutive layers of one column; warp j runs the whole local solve of
+// element j in registers on mma.sync.m8n8k4.f64:
+//   B1 = box of element j from the column block Rc (shared)
+//   T  = S_h^T B1      A = S^T from shared S, B = B1 (registers)
+//   T <- ((T S_v) ./ (l_h + l_v)) S_v^T       C -> A fragments by shuffles
+//   Y  = S_h T          A = S from shared S, B = T (C -> B fragments by shuffles)
+//   Yacc[h][z] += Y     (shared atomics: neighbouring boxes overlap in z)
+// then every column node is scattered once.  Row strides = 4 mod 8 doubles:
+// conflict-free for both fragment patterns (4 rows x 8 and 8 rows x 4).
+template <int MT, int NVT>
+__global__ void __launch_bounds__(256, NVT == 1 ? 3 : 1) k_fdm_warp(const int4* __restrict__ units, const int32_t* __restrict__ colel,
+                                                  const int64_t* __restrict__ hoff, const int64_t* __restrict__ moff,
+                                                  const int64_t* __restrict__ cioff, const int32_t* __restrict__ nzc,
+                                                  const int32_t* __restrict__ cidx, const int32_t* __restrict__ z0,
+                                                  const int32_t* __restrict__ nvv, const double* __restrict__ Sh,
+                                                  const double* __restrict__ lh, const double* __restrict__ Svp,
+                                                  const double* __restrict__ lvp, const double* __restrict__ W,
+                                                  const double* __restrict__ r, double* __restrict__ u, int transpose,
+                                                  int ldr) {
+  constexpr int ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
+  extern __shared__ __align__(16) double sm[];
+  double* Ss = sm;                  // [ROWS][LDS]  S_h (row i node, col a mode), zero padded
+  double* Rc = Ss + ROWS * LDS;     // [ROWS][ldr]  column block, later the accumulator
+  __shared__ int ez0[8], env[8], eid[8];
+  const int4 U = units[blockIdx.x];
+  const int c = U.x, first = U.y, cnt = U.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nh = (int)(hoff[c + 1] - hoff[c]);
+  const int nz = nzc[c];
+  const int32_t* ci = cidx + cioff[c];
+  const double* S = Sh + moff[c];
+  if (tid < cnt) {
+    const int e = colel[first + tid];
+    eid[tid] = e;
+    ez0[tid] = z0[e];
+    env[tid] = nvv[e];
+  }
+  {  // S_h -> shared (all loads in flight before the stores)
+    constexpr int IS = (ROWS * ROWS + 255) / 256;
+    double tmp[IS];
+#pragma unroll
+    for (int k = 0; k < IS; ++k) {
+      const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
+      tmp[k] = (t < ROWS * ROWS && i < nh && a < nh) ? __ldg(S + i * nh + a) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < IS; ++k) {
+      const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
+      if (t < ROWS * ROWS) Ss[i * LDS + a] = tmp[k];
+    }
+  }
+  __syncthreads();
+  const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
+  // column block gather in batches of 8 items per thread: node ids, values (x W), stores
+  for (int base = 0; base < ROWS * ldr; base += 256 * 8) {
+    int gid[8];
+    double val[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = base + tid + 256 * k, h = t / ldr, zz = t - h * ldr;
+      gid[k] = (h < nh && zz < nzu) ? __ldg(ci + h * nz + zlo + zz) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) val[k] = gid[k] >= 0 ? r[gid[k]] : 0.0;
+    if (transpose) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (gid[k] >= 0) val[k] *= __ldg(W + gid[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = base + tid + 256 * k;
+      if (t < ROWS * ldr) Rc[t] = val[k];
+    }
+  }
+  __syncthreads();
+  const bool active = warp < cnt;
+  const int j = active ? warp : 0;
+  const int zb = ez0[j] - zlo, nvj = env[j];
+  double b1[KT][NVT];
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int n = 0; n < NVT; ++n) {
+      const int col = n * 8 + (lane >> 2);
+      b1[kt][n] = (active && col < nvj) ? Rc[(kt * 4 + (lane & 3)) * ldr + zb + col] : 0.0;
+    }
+  __syncthreads();
+  for (int t = tid; t < ROWS * ldr; t += 256) Rc[t] = 0.0;  // Rc becomes the accumulator
+  __syncthreads();
+  if (active) {
+    const int e = eid[j];
+    // T = S_h^T B1
+    double T[MT][NVT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) T[mt][n][0] = T[mt][n][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const double af = Ss[(kt * 4 + (lane & 3)) * LDS + mt * 8 + (lane >> 2)];
+#pragma unroll
+        for (int n = 0; n < NVT; ++n) fdm_dmma(T[mt][n][0], T[mt][n][1], af, b1[kt][n]);
+      }
+    }
+    // vertical: T <- ((T S_v) ./ (l_h + l_v)) S_v^T, per m-tile
+    const double* sv = Svp + (size_t)e * NVP * NVP;
+    const double* lv = lvp + (size_t)e * NVP;
+    double s1[2 * NVT][NVT], s2[2 * NVT][NVT], lvv[NVT][2];
+#pragma unroll
+    for (int kt = 0; kt < 2 * NVT; ++kt)
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) {
+        s1[kt][n] = __ldg(sv + (kt * 4 + (lane & 3)) * NVP + n * 8 + (lane >> 2));
+        s2[kt][n] = __ldg(sv + (n * 8 + (lane >> 2)) * NVP + kt * 4 + (lane & 3));
+      }
+#pragma unroll
+    for (int n = 0; n < NVT; ++n)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) lvv[n][i] = __ldg(lv + n * 8 + 2 * (lane & 3) + i);
+    const double* Lh = lh + hoff[c];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      double v[NVT][2];
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) v[n][0] = v[n][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < 2 * NVT; ++kt) {
+        const double a = c_to_a<NVT>(T[mt], kt, lane);
+#pragma unroll
+        for (int n = 0; n < NVT; ++n) fdm_dmma(v[n][0], v[n][1], a, s1[kt][n]);
+      }
+      const int ah = mt * 8 + (lane >> 2);
+      const double la = ah < nh ? __ldg(Lh + ah) : 1.0;
+#pragma unroll
+      for (int n = 0; n < NVT; ++n)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) v[n][i] /= (la + lvv[n][i]);
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) T[mt][n][0] = T[mt][n][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < 2 * NVT; ++kt) {
+        const double a = c_to_a<NVT>(v, kt, lane);
+#pragma unroll
+        for (int n = 0; n < NVT; ++n) fdm_dmma(T[mt][n][0], T[mt][n][1], a, s2[kt][n]);
+      }
+    }
+    // B fragments of T for Y = S_h T: B[k=a][n=col] = T[a][col]
+    double b2[KT][NVT];
+    {
+      const int cr = (lane >> 2) & 1;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const int src = ((((kt & 1) << 2) + (lane & 3)) << 2) | ((lane >> 2) >> 1);
+#pragma unroll
+        for (int n = 0; n < NVT; ++n) {
+          const double x0 = __shfl_sync(0xffffffffu, T[kt >> 1][n][0], src);
+          const double x1 = __shfl_sync(0xffffffffu, T[kt >> 1][n][1], src);
+          b2[kt][n] = cr ? x1 : x0;
+        }
+      }
+    }
+    // Y = S_h T, accumulated into the column block
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      double y[NVT][2];
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) y[n][0] = y[n][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const double af = Ss[(mt * 8 + (lane >> 2)) * LDS + kt * 4 + (lane & 3)];
+#pragma unroll
+        for (int n = 0; n < NVT; ++n) fdm_dmma(y[n][0], y[n][1], af, b2[kt][n]);
+      }
+      const int i = mt * 8 + (lane >> 2);
+      if (i < nh) {
+#pragma unroll
+        for (int n = 0; n < NVT; ++n)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = n * 8 + 2 * (lane & 3) + q;
+            if (col < nvj) atomicAdd(Rc + i * ldr + zb + col, y[n][q]);
+          }
+      }
+    }
+  }
+  __syncthreads();
+  for (int base = 0; base < nh * ldr; base += 256 * 8) {  // scatter every column node of the unit once
+    int gid[8];
+    double val[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = base + tid + 256 * k, h = t / ldr, zz = t - h * ldr;
+      gid[k] = (h < nh && zz < nzu) ? __ldg(ci + h * nz + zlo + zz) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) val[k] = gid[k] >= 0 ? Rc[base + tid + 256 * k] : 0.0;
+    if (!transpose) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (gid[k] >= 0) val[k] *= __ldg(W + gid[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (gid[k] >= 0) atomicAdd(u + gid[k], val[k]);
+  }
+}
+
+template <int MT, int NVT>
+static void fdm_warp_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
+  const int smem = (8 * MT * (8 * MT + 4) + 8 * MT * L.f_ldr) * (int)sizeof(double);
+  static int attr = 0;
+  if (smem > attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_fdm_warp<MT, NVT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  k_fdm_warp<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
+                                                             L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
+                                                             L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_ldr);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+template <int NVT>
+static void fdm_warp_dispatch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
+  switch (L.f_mt) {
+    case 1: fdm_warp_launch<1, NVT>(c, L, r, u, transpose); break;
+    case 2: fdm_warp_launch<2, NVT>(c, L, r, u, transpose); break;
+    case 3: fdm_warp_launch<3, NVT>(c, L, r, u, transpose); break;
+    case 4: fdm_warp_launch<4, NVT>(c, L, r, u, transpose); break;
+    case 5: fdm_warp_launch<5, NVT>(c, L, r, u, transpose); break;
+    case 6: fdm_warp_launch<6, NVT>(c, L, r, u, transpose); break;
+    case 7: fdm_warp_launch<7, NVT>(c, L, r, u, transpose); break;
+    default: fdm_warp_launch<8, NVT>(c, L, r, u, transpose); break;
+  }
+}
+
 template <int MT, int NVT>
 static void fdm_col_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
   {
@@ -539,6 +794,12 @@ static int fdm_simple() {
 void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose) {
   const DeviceLevel& L = c->L[level];
   if (c->E_own == 0) return;
+  if (!fdm_simple() && L.f_warp) {
+    if (L.f_nvt == 1) fdm_warp_dispatch<1>(c, L, r, u, transpose);
+    else fdm_warp_dispatch<2>(c, L, r, u, transpose);
+    c->launches++;
+    return;
+  }
   if (!fdm_simple() && L.f_mt <= 16 && L.f_nvt <= 3) {
     if (L.f_nvt == 1) fdm_col_dispatch<1>(c, L, r, u, transpose);
     else if (L.f_nvt == 2) fdm_col_dispatch<2>(c, L, r, u, transpose);

@@ -17,9 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="config3")
 ap.add_argument("--mode", default="step", choices=["step", "schwarz", "apply", "vcycle"])
 ap.add_argument("--tol", type=float, default=1e-8)
+ap.add_argument("--smoother", default="dense", choices=["dense", "fdm"])
+ap.add_argument("--overlap", type=int, default=1)
 a = ap.parse_args()
 m = {"config1": config1, "config2": config2, "config3": config3}[a.config]()
-s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)))
+s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
+               local_solve=1 if a.smoother == "fdm" else 0, overlap=a.overlap)
 xyz = s.node_xyz(0)
 phiD = torch.from_numpy(m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])).cuda()
 phi, rep = s.solve(phiD, a.tol)
