@@ -37,6 +37,8 @@ def parse():
     ap.add_argument("--smoother", default="dense", choices=["dense", "fdm"],
                     help="Schwarz local solves: exact dense inverses (eq 4.4) or FDM (reading O33)")
     ap.add_argument("--overlap", type=int, default=1, help="Schwarz overlap (-1 = refined ceil((P+1)/2), P:536)")
+    ap.add_argument("--mixed", type=int, default=0,
+                    help="1: FP32 storage of the exact Schwarz / coarse inverses, FP64 arithmetic (P:35)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--emulate-ranks", type=int, default=0,
@@ -184,7 +186,7 @@ def main():
     m = make_mesh(args.config)
     t0 = time.perf_counter()
     kw = dict(verbose=int(os.environ.get("SEM_VERBOSE", "0")), overlap=args.overlap,
-              local_solve=1 if args.smoother == "fdm" else 0)
+              local_solve=1 if args.smoother == "fdm" else 0, mixed_precision=args.mixed)
     if world > 1:
         kw.update(nranks=world, rank=rank, nccl_id=nccl_id)
     elif args.emulate_ranks > 1:
@@ -242,7 +244,7 @@ def main():
             "alg_bytes_per_launch": b_s, "launch_us": us_s,
             "traffic_note": "ncu dram__bytes_read+write per launch in profiles/schwarz_r1_raw.csv (28.9 GB, N=1)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "when" in peaks else "fallback 6650 GB/s"}
-    if world == 1 and args.emulate_ranks <= 1 and args.config == "config3" and args.smoother == "dense":
+    if world == 1 and args.emulate_ranks <= 1 and args.config == "config3" and args.smoother == "dense" and not args.mixed:
         roof["traffic"] = 28.92e9
     ach_a = b_a / (us_a * 1e-6) / 1e9
     apply = {"kernel": "k_apply_dmma<%d> (FP64 tensor cores)" % m.p, "us": us_a, "alg_bytes_per_launch": b_a,

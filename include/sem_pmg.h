@@ -108,6 +108,11 @@ typedef struct {
                                  Lottes & Fischer [FL05]): exact on straight prisms with flat
                                  layers, needs a layered mesh (SEM_EUNSUPPORTED otherwise) and
                                  nranks = 1.  Same subdomains (O15) and weights (eq 4.6).            */
+  int mixed_precision;        /* 0 (default): everything stored and computed in FP64.  1: the exact
+                                 dense Schwarz inverses and the dense coarse inverse are STORED in FP32
+                                 (rounded once at setup) and applied with FP64 arithmetic -- the
+                                 mixed-precision multigrid of P:35; the preconditioner stays a fixed
+                                 symmetric linear operator, the outer PCG and the operator stay FP64. */
 } sem_opts;
 
 typedef struct {

@@ -84,6 +84,7 @@ void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas
   L.schwarz_bytes = toff[E] * 8;
   size_t freeb = 0, totb = 0;
   CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
+  if (c->opts.mixed_precision) L.schwarz_bytes /= 2;
   if ((size_t)L.schwarz_bytes > freeb * 0.92)
     throw SemError(SEM_ENOMEM, "dense Schwarz inverses of level p=" + std::to_string(L.p) + " need " +
                                    std::to_string(L.schwarz_bytes >> 20) + " MiB of " + std::to_string(freeb >> 20) +
@@ -91,7 +92,8 @@ void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas
   L.sidx = upload(c, pidx);
   L.sidx_off = upload(c, poff);
   L.tile_off = upload(c, toff);
-  L.tiles = dalloc<double>(c, (size_t)toff[E]);
+  if (c->opts.mixed_precision) L.tiles32 = dalloc<float>(c, (size_t)toff[E]);
+  else L.tiles = dalloc<double>(c, (size_t)toff[E]);
   L.W = upload(c, S.W);
 
   Scratch sc;
@@ -208,9 +210,9 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
   c->C.nc = nc;
   c->C.fidx = upload(c, fidx);
   c->C.x = dalloc<double>(c, nc);
-  c->C.Ainv = dalloc<double>(c, (size_t)nc * nc);
-  if (nc == 0) return;
   Scratch sc;
+  c->C.Ainv = c->opts.mixed_precision ? sc.get<double>((size_t)nc * nc) : dalloc<double>(c, (size_t)nc * nc);
+  if (nc == 0) return;
   double* Ae = sc.get<double>((size_t)E * L.N * L.N);
   launch_elem_matrices(c, (int)c->L.size() - 1, d_D, Ae, 0, E);
   int32_t* d_cmap = sc.put(cmap);
@@ -232,6 +234,12 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
   if (hinfo != 0) throw SemError(SEM_ESINGULAR, "coarse inverse failed (info " + std::to_string(hinfo) + ")");
   launch_symmetrize(c, c->C.Ainv, nc);
+  if (c->opts.mixed_precision) {  // FP32 storage of the exact inverse, FP64 arithmetic
+    c->C.Ainv32 = dalloc<float>(c, (size_t)nc * nc);
+    launch_to_float(c, nc * nc, c->C.Ainv, c->C.Ainv32);
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    c->C.Ainv = nullptr;  // scratch, freed on return
+  }
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }
 
@@ -239,6 +247,7 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
 
 void check_opts(const sem_opts& o) {
   if (o.local_solve < 0 || o.local_solve > 1) throw SemError(SEM_EINVAL, "bad options: local_solve");
+  if (o.mixed_precision < 0 || o.mixed_precision > 1) throw SemError(SEM_EINVAL, "bad options: mixed_precision");
   if (o.local_solve == 1 && o.nranks > 1)
     throw SemError(SEM_EUNSUPPORTED, "FDM local solves are single-domain only (nranks = 1)");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
@@ -944,7 +953,7 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
       if (kernel == 0 && L.fdm)
         *alg_bytes = (double)L.schwarz_bytes + 32.0 * L.n;
       else if (kernel == 0)
-        *alg_bytes = 8.0 * L.packed + 4.0 * L.nk_sum + 32.0 * L.n;
+        *alg_bytes = (L.tiles32 ? 4.0 : 8.0) * L.packed + 4.0 * L.nk_sum + 32.0 * L.n;
       else
         *alg_bytes = (double)t->E_own * (48.0 * L.Q + 4.0 * L.N) + 16.0 * L.n;
     }

@@ -48,6 +48,7 @@ struct DeviceLevel {
   int64_t* sidx_off = nullptr;  // [E+1] (padded offsets)
   int64_t* tile_off = nullptr;  // [E+1] offsets in doubles into tiles
   double* tiles = nullptr;
+  float* tiles32 = nullptr;     // opts.mixed_precision: FP32 copy of the packed inverses (tiles unused)
   double* W = nullptr;          // [n]
   // FDM local solves (opts.local_solve = 1; fdm.cu, reading O33)
   int fdm = 0, f_nh_max = 0, f_nv_max = 0;
@@ -94,6 +95,7 @@ struct Coarse {
   int64_t nc = 0;               // free coarse nodes
   int32_t* fidx = nullptr;      // [nc] compact -> level gid
   double* Ainv = nullptr;       // [nc][nc] row-major, symmetric (dense path)
+  float* Ainv32 = nullptr;      // opts.mixed_precision: FP32 storage of Ainv (Ainv freed)
   double* x = nullptr;          // [nc] work
   // iterative path (reading O9): Jacobi-preconditioned CG on the P=1 operator
   int iterative = 0;
@@ -157,6 +159,7 @@ void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* 
 void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den, int mode);
 void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi);
 void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);
+void launch_to_float(sem_ctx* c, int64_t n, const double* a, float* b);
 // setup kernels
 int launch_geometry(sem_ctx* c, int level, const double* d_xfine, const double* d_gmat, int Nf, const double* d_w);
 void launch_elem_matrices(sem_ctx* c, int level, const double* d_D, double* Ae, int e0, int ne);

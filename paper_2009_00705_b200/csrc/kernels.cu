@@ -254,9 +254,10 @@ void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, i
 // 256-byte loads; row sums are reduced with a value-halving shuffle butterfly,
 // column sums (the symmetric half) accumulated per lane; per-warp private
 // accumulators in shared memory avoid atomics.
+template <class TT>
 __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sidx, const int64_t* __restrict__ sidx_off,
                                                  const int64_t* __restrict__ tile_off,
-                                                 const double* __restrict__ tiles, const double* __restrict__ W,
+                                                 const TT* __restrict__ tiles, const double* __restrict__ W,
                                                  const double* __restrict__ r, double* __restrict__ u, int transpose,
                                                  int npad_max) {
   extern __shared__ double sm[];
@@ -279,18 +280,16 @@ __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sid
   for (int i = tid; i < 8 * np; i += 256) yw[(i / np) * npad_max + (i % np)] = 0.0;
   __syncthreads();
   double* y = yw + warp * npad_max;
-  const double* tk = tiles + tile_off[k];
+  const TT* tk = tiles + tile_off[k];
   const int ntiles = T * (T + 1) / 2;
   const int r0 = lane >> 4, cc = lane & 15;
-  for (int t = warp; t < ntiles; t += 8) {
-    int I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  auto tile_ij = [](int t, int& I, int& J) {
+    I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     while (I * (I + 1) / 2 > t) --I;
-    const int J = t - I * (I + 1) / 2;
-    const double* A = tk + (size_t)t * 256;
-    double a[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) a[m] = __ldg(A + 32 * m + lane);
+    J = t - I * (I + 1) / 2;
+  };
+  auto tile_apply = [&](const double (&a)[8], int I, int J) {
     const double xc = x[16 * J + cc];
     double v[8];
 #pragma unroll
@@ -329,6 +328,15 @@ __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sid
       const int m = (b1 ? 1 : 0) + (b2 ? 2 : 0) + (b3 ? 4 : 0);
       y[16 * I + 2 * m + r0] += k1;
     }
+  };
+  for (int t = warp; t < ntiles; t += 8) {
+    const TT* A = tk + (size_t)t * 256;
+    double a[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) a[m] = (double)__ldg(A + 32 * m + lane);
+    int I, J;
+    tile_ij(t, I, J);
+    tile_apply(a, I, J);
   }
   __syncthreads();
   for (int i = tid; i < np; i += 256) {
@@ -350,13 +358,23 @@ void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int trans
   }
   const int npad = 16 * L.max_tiles_1d;
   const int smem = 9 * npad * (int)sizeof(double);
-  static int attr_set = 0;
-  if (smem > 48 * 1024 && smem > attr_set) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_schwarz, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = smem;
-  }
+  static int attr_set = 0, attr_set32 = 0;
   if (c->E_own == 0) return;
-  k_schwarz<<<c->E_own, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u, transpose, npad);
+  if (L.tiles32) {  // mixed precision: FP32 storage of the exact inverses, FP64 arithmetic
+    if (smem > 48 * 1024 && smem > attr_set32) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_schwarz<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr_set32 = smem;
+    }
+    k_schwarz<float><<<c->E_own, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles32, L.W, r, u,
+                                                         transpose, npad);
+  } else {
+    if (smem > 48 * 1024 && smem > attr_set) {
+      CUDA_CHECK(cudaFuncSetAttribute(k_schwarz<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr_set = smem;
+    }
+    k_schwarz<double><<<c->E_own, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u,
+                                                          transpose, npad);
+  }
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }
@@ -459,22 +477,23 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ idx, const doubl
 }
 
 // one warp per row of the dense symmetric inverse; z[fidx[i]] = sum_j Ainv[i][j] x[j]
-__global__ void __launch_bounds__(256) k_coarse_gemv(int64_t n, const double* __restrict__ A,
+template <class TA>
+__global__ void __launch_bounds__(256) k_coarse_gemv(int64_t n, const TA* __restrict__ A,
                                                      const double* __restrict__ x, const int32_t* __restrict__ fidx,
                                                      double* __restrict__ z) {
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8ll + (threadIdx.x >> 5);
   if (row >= n) return;
-  const double* a = A + row * n;
+  const TA* a = A + row * n;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int64_t j = lane;
   for (; j + 96 < n; j += 128) {
-    s0 = fma(__ldg(a + j), __ldg(x + j), s0);
-    s1 = fma(__ldg(a + j + 32), __ldg(x + j + 32), s1);
-    s2 = fma(__ldg(a + j + 64), __ldg(x + j + 64), s2);
-    s3 = fma(__ldg(a + j + 96), __ldg(x + j + 96), s3);
+    s0 = fma((double)__ldg(a + j), __ldg(x + j), s0);
+    s1 = fma((double)__ldg(a + j + 32), __ldg(x + j + 32), s1);
+    s2 = fma((double)__ldg(a + j + 64), __ldg(x + j + 64), s2);
+    s3 = fma((double)__ldg(a + j + 96), __ldg(x + j + 96), s3);
   }
-  for (; j < n; j += 32) s0 = fma(__ldg(a + j), __ldg(x + j), s0);
+  for (; j < n; j += 32) s0 = fma((double)__ldg(a + j), __ldg(x + j), s0);
   double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -486,7 +505,10 @@ void launch_coarse(sem_ctx* c, const double* r, double* z) {
   CUDA_CHECK(cudaMemsetAsync(z, 0, sizeof(double) * L.n, c->stream));
   k_gather<<<grid_for(c->C.nc, 256), 256, 0, c->stream>>>(c->C.nc, c->C.fidx, r, c->C.x);
   CUDA_CHECK(cudaGetLastError());
-  k_coarse_gemv<<<(int)((c->C.nc + 7) / 8), 256, 0, c->stream>>>(c->C.nc, c->C.Ainv, c->C.x, c->C.fidx, z);
+  if (c->C.Ainv32)
+    k_coarse_gemv<float><<<(int)((c->C.nc + 7) / 8), 256, 0, c->stream>>>(c->C.nc, c->C.Ainv32, c->C.x, c->C.fidx, z);
+  else
+    k_coarse_gemv<double><<<(int)((c->C.nc + 7) / 8), 256, 0, c->stream>>>(c->C.nc, c->C.Ainv, c->C.x, c->C.fidx, z);
   CUDA_CHECK(cudaGetLastError());
   c->launches += 2;
 }
@@ -799,13 +821,14 @@ void launch_assemble_blocks(sem_ctx* c, int level, const int32_t* idx, const int
 
 // copy the lower 16x16 tiles of each inverse (full npad x npad, symmetric) into
 // the streaming layout; entries beyond n_k are zeroed.
+template <class TT>
 __global__ void k_pack_tiles(const double* __restrict__ Binv, int k0, int npad, const int64_t* __restrict__ off,
-                             const int64_t* __restrict__ tile_off, double* __restrict__ tiles) {
+                             const int64_t* __restrict__ tile_off, TT* __restrict__ tiles) {
   const int k = k0 + blockIdx.x;
   const int nk = (int)(off[k + 1] - off[k]);
   const int T = (nk + 15) / 16;
   const double* B = Binv + (size_t)blockIdx.x * npad * npad;
-  double* out = tiles + tile_off[k];
+  TT* out = tiles + tile_off[k];
   const int ntiles = T * (T + 1) / 2;
   for (int64_t x = threadIdx.x; x < (int64_t)ntiles * 256; x += blockDim.x) {
     const int t = (int)(x / 256), rc = (int)(x % 256), r = rc / 16, cc = rc % 16;
@@ -813,13 +836,24 @@ __global__ void k_pack_tiles(const double* __restrict__ Binv, int k0, int npad, 
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     const int J = t - I * (I + 1) / 2;
     const int gi = 16 * I + r, gj = 16 * J + cc;
-    out[x] = (gi < nk && gj < nk) ? B[(size_t)gi * npad + gj] : 0.0;
+    out[x] = (TT)((gi < nk && gj < nk) ? B[(size_t)gi * npad + gj] : 0.0);
   }
 }
 
 void launch_pack_tiles(sem_ctx* c, int level, const double* Binv, int k0, int nb, int npad, const int64_t* off) {
   const DeviceLevel& L = c->L[level];
-  k_pack_tiles<<<nb, 256, 0, c->stream>>>(Binv, k0, npad, off, L.tile_off, L.tiles);
+  if (L.tiles32) k_pack_tiles<float><<<nb, 256, 0, c->stream>>>(Binv, k0, npad, off, L.tile_off, L.tiles32);
+  else k_pack_tiles<double><<<nb, 256, 0, c->stream>>>(Binv, k0, npad, off, L.tile_off, L.tiles);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void k_to_float(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+
+void launch_to_float(sem_ctx* c, int64_t n, const double* a, float* b) {
+  k_to_float<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, b);
   CUDA_CHECK(cudaGetLastError());
 }
 

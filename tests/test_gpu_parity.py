@@ -299,3 +299,30 @@ def test_iterative_coarse_solver(c2):
     phi, rep = s.solve(c2.to_lib(0, phiD), tol=1e-13)
     assert rep["converged"] and rep["coarse_iters"] > 0
     assert rel(c2.to_orc(0, phi), sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+
+
+def test_mixed_precision_storage(c2):
+    """mixed_precision=1: FP32 storage of the exact Schwarz and coarse
+    inverses, FP64 arithmetic.  Each step stays within FP32 rounding of the FP64
+    step; the solve still reaches the sparse-direct solution (the preconditioner is
+    a fixed symmetric linear operator)."""
+    m = c2.m
+    s = make_solver(m, mixed_precision=1)
+    assert s.info["schwarz_bytes"][0] * 2 == c2.s.info["schwarz_bytes"][0]
+    sm = c2.mg.levels[0].smoother
+    r = random_vector(len(sm.W), seed=41)
+    u = s.empty(0)
+    s.schwarz(0, c2.free_to_lib(0, r), u)
+    assert 1e-12 < rel(c2.lib_to_free(0, u), sm.apply(r)) <= 1e-5
+    nF = c2.mg.levels[0].A.shape[0]
+    x = random_vector(nF, seed=42)
+    y = random_vector(nF, seed=43)
+    vx = c2.lib_to_free(0, s.vcycle(c2.free_to_lib(0, x)))
+    vy = c2.lib_to_free(0, s.vcycle(c2.free_to_lib(0, y)))
+    assert rel(vx, c2.mg.vcycle(x)) <= 1e-5
+    assert abs(x @ vy - y @ vx) <= 1e-12 * abs(x @ vy)      # still symmetric
+    lev, perm = c2.levels[0]
+    phiD = m.phi(*lev.xyz.T)
+    phi, rep = s.solve(c2.to_lib(0, phiD), tol=1e-13)
+    assert rep["converged"]
+    assert rel(c2.to_orc(0, phi), sem.solve_direct(lev, phiD)) <= SOLVE_TOL
