@@ -86,8 +86,11 @@ typedef struct {
   void *stream;               /* cudaStream_t for every kernel; NULL = default stream               */
   int device;                 /* CUDA device ordinal used by sem_setup (default: current device)    */
   int verbose;                /* 1: setup timings to stderr                                         */
-  int apply_kernel;           /* operator kernel: 0 (default) FP64 tensor-core (DMMA) sum factorisation,
-                                 1 CUDA-core FMA sum factorisation (same arithmetic, reference variant) */
+  int apply_kernel;           /* operator kernel (all the same arithmetic, eq 3.8): 0 (default) FP64
+                                 tensor-core (DMMA) sum factorisation, one warp per element with
+                                 TMA-staged geometric factors (p <= 6; p = 7, 8 use variant 2);
+                                 1 CUDA-core FMA sum factorisation (reference variant);
+                                 2 DMMA with CTA-wide element batches                                */
   int coarse_solver;          /* P=1 solve (reading O9): 0 auto (dense inverse if <= 46,000 free
                                  nodes, else iterative), 1 iterative (Jacobi-PCG, the outer PCG becomes
                                  flexible), 2 dense                                                  */

@@ -1,0 +1,363 @@
+// Operator apply, one warp per element, on FP64 tensor cores (sm_100a DMMA).
+//
+// Same mathematics as k_apply<P> / k_apply_dmma<P> (eq 3.8, P:153-161:
+// y (+/-)= sum_e Q_e^T D^T (G (.) D Q_e u), D = [B_r (x) B_t ; B_s (x) B_t ;
+// B_0 (x) D_t]), sum-factorised vertical-first so that every stage is a small
+// GEMM on mma.sync.m8n8k4.f64 with the element's data in registers:
+//
+//   A   Ut[m][q]  = sum_l u[m][l] Bt[q][l],   Udt[m][q] = sum_l u[m][l] Dt[q][l]
+//   B   g_r[a][q] = sum_m Br[a][m] Ut[m][q],  g_s (Bs, Ut),  g_t (B0, Udt)   per a-tile
+//   G   w = G g  at every cubature point (a, q)                              per a-tile
+//   B^T Vt[m][q] += sum_a Br[a][m] w_r[a][q] + Bs[a][m] w_s[a][q],
+//       Vdt[m][q] += sum_a B0[a][m] w_t[a][q]                                per a-tile
+//   A^T y[m][l]   = sum_q Vt[m][q] Bt[q][l] + Vdt[m][q] Dt[q][l]
+//
+// (m: triangle node, l: vertical node, a: triangle cubature point, q: vertical
+// Gauss point).  Fragment layouts of m8n8k4: A a0 = A[r4][c4], B b0 = B[c4][r4],
+// C c_i = C[r4][2 c4 + i] with r4 = lane >> 2, c4 = lane & 3.  C fragments are
+// re-laid out as A or B fragments of the next stage with two shuffles.
+//
+// Data movement: the element's geometric factors (6 Q doubles, contiguous) are
+// brought into the warp's shared-memory slot by one TMA bulk copy
+// (cp.async.bulk + mbarrier), double-buffered so the next element's copy flies
+// during the current element's stages; u is gathered into registers through
+// the connectivity, y scattered with FP64 atomics.  Persistent CTAs, no CTA
+// barrier after the prologue.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdlib>
+
+#include "internal.h"
+
+namespace sem {
+
+namespace aw {
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+}  // namespace aw
+
+template <int P>
+struct AW {
+  static constexpr int N1 = P + 1, NT = N1 * (N1 + 1) / 2, QT = N1 * N1, QV = N1, Q = QT * QV, N = NT * N1;
+  static constexpr int MTM = aw::cdiv(NT, 8);   // m-tiles over triangle nodes
+  static constexpr int KM = 2 * MTM;            // k-steps over triangle nodes (padded to 8 MTM)
+  static constexpr int MTA = aw::cdiv(QT, 8);   // a-tiles over triangle cubature points
+  static constexpr int NQ = aw::cdiv(QV, 8);    // n-tiles over vertical points
+  static constexpr int KL = aw::cdiv(N1, 4);    // k-steps over vertical nodes
+  static constexpr int NL = aw::cdiv(N1, 8);    // n-tiles over vertical nodes
+  static constexpr int KQ = aw::cdiv(QV, 4);    // k-steps over vertical points
+  static constexpr int LDM = 8 * MTM + 4;       // row stride of Bm (= 4 mod 8: conflict-free both ways)
+  static constexpr int ROWSA = 8 * MTA;
+  static constexpr int BM = 3 * ROWSA * LDM;    // doubles of Bm [3][ROWSA][LDM] (Br, Bs, B0)
+  static constexpr int W = (P <= 5) ? 8 : 4;    // warps per CTA
+  static constexpr int GSZ = 6 * Q;             // doubles of one element's G
+  static constexpr int SMEM = (BM + 2 * W * GSZ) * 8 + 2 * W * 8;
+  static_assert(SMEM <= 227 * 1024, "apply_warp shared memory");
+};
+
+// host: Bm [3][ROWSA][LDM] (Br, Bs, B0 at [a][m], zero padded) followed by Bt, Dt [QV][N1]
+std::vector<double> warp_apply_mats(const LevelRef& R) {
+  auto run = [&](auto tag) {
+    using D = AW<decltype(tag)::value>;
+    std::vector<double> v(D::BM + 2 * D::QV * D::N1, 0.0);
+    const double* B[3] = {R.Br.data(), R.Bs.data(), R.B0.data()};
+    for (int c = 0; c < 3; ++c)
+      for (int a = 0; a < D::QT; ++a)
+        for (int m = 0; m < D::NT; ++m) v[(c * D::ROWSA + a) * D::LDM + m] = B[c][a * D::NT + m];
+    for (int i = 0; i < D::QV * D::N1; ++i) {
+      v[D::BM + i] = R.Bt[i];
+      v[D::BM + D::QV * D::N1 + i] = R.Dt[i];
+    }
+    return v;
+  };
+  switch (R.p) {
+    case 1: return run(std::integral_constant<int, 1>{});
+    case 2: return run(std::integral_constant<int, 2>{});
+    case 3: return run(std::integral_constant<int, 3>{});
+    case 4: return run(std::integral_constant<int, 4>{});
+    case 5: return run(std::integral_constant<int, 5>{});
+    case 6: return run(std::integral_constant<int, 6>{});
+  }
+  return {};
+}
+
+__device__ __forceinline__ void aw_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t aw_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// B fragment (k row = 4 ks + c4 of an 8-row tile, n col = r4) of a tile held as C fragments
+__device__ __forceinline__ double aw_c_to_b(double c0, double c1, int ks, int lane) {
+  const int src = ((((ks & 1) << 2) + (lane & 3)) << 2) | ((lane >> 2) >> 1);
+  const double x0 = __shfl_sync(0xffffffffu, c0, src);
+  const double x1 = __shfl_sync(0xffffffffu, c1, src);
+  return ((lane >> 2) & 1) ? x1 : x0;
+}
+// A fragment (row r4, k col = 4 ks + c4 of an 8-col tile) of a tile held as C fragments
+__device__ __forceinline__ double aw_c_to_a(double c0, double c1, int ks, int lane) {
+  const int src = (lane & ~3) | (((ks & 1) << 1) + ((lane & 3) >> 1));
+  const double x0 = __shfl_sync(0xffffffffu, c0, src);
+  const double x1 = __shfl_sync(0xffffffffu, c1, src);
+  return (lane & 1) ? x1 : x0;
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const int32_t* __restrict__ conn,
+                                                                 const double* __restrict__ G,
+                                                                 const double* __restrict__ mats,
+                                                                 const double* __restrict__ u, double* __restrict__ y,
+                                                                 int flags) {
+  using D = AW<P>;
+  extern __shared__ __align__(128) double sm[];
+  double* Bm = sm;                          // [3][ROWSA][LDM]
+  double* Gs = sm + D::BM;                  // [W][2][6 Q]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(Gs + 2 * D::W * D::GSZ);  // [W][2]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r4 = lane >> 2, c4 = lane & 3;
+  for (int i = tid; i < D::BM; i += 32 * D::W) Bm[i] = __ldg(mats + i);
+  if (lane == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(aw_smem(mbar + 2 * warp + b)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // constant B fragments of the vertical stages
+  const double* Bt = mats + D::BM;        // [q][l]
+  const double* Dt = Bt + D::QV * D::N1;
+  double fBt[D::KL][D::NQ], fDt[D::KL][D::NQ];   // stage A:  B[k=l][n=q] = Bt[q][l]
+#pragma unroll
+  for (int kl = 0; kl < D::KL; ++kl)
+#pragma unroll
+    for (int nq = 0; nq < D::NQ; ++nq) {
+      const int l = kl * 4 + c4, q = nq * 8 + r4;
+      const bool ok = l < D::N1 && q < D::QV;
+      fBt[kl][nq] = ok ? __ldg(Bt + q * D::N1 + l) : 0.0;
+      fDt[kl][nq] = ok ? __ldg(Dt + q * D::N1 + l) : 0.0;
+    }
+  double gBt[D::KQ][D::NL], gDt[D::KQ][D::NL];   // stage A^T:  B[k=q][n=l] = Bt[q][l]
+#pragma unroll
+  for (int kq = 0; kq < D::KQ; ++kq)
+#pragma unroll
+    for (int nl = 0; nl < D::NL; ++nl) {
+      const int q = kq * 4 + c4, l = nl * 8 + r4;
+      const bool ok = l < D::N1 && q < D::QV;
+      gBt[kq][nl] = ok ? __ldg(Bt + q * D::N1 + l) : 0.0;
+      gDt[kq][nl] = ok ? __ldg(Dt + q * D::N1 + l) : 0.0;
+    }
+  const double sgn = (flags & AP_NEGATE) ? -1.0 : 1.0;
+  const int stride = gridDim.x * D::W;
+  int e = blockIdx.x * D::W + warp;
+  double* gslot = Gs + (2 * warp) * D::GSZ;   // two slots of GSZ doubles
+  uint32_t phase = 0u;                          // bit b: parity of slot b's next completion
+  auto issue_G = [&](int el, int b) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+      const uint32_t bytes = (uint32_t)D::GSZ * 8u;
+      const uint32_t mb = aw_smem(mbar + 2 * warp + b);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              aw_smem(gslot + b * D::GSZ)),
+          "l"(G + (size_t)el * D::GSZ), "r"(bytes), "r"(mb)
+          : "memory");
+    }
+  };
+  int buf = 0;
+  if (e < E) issue_G(e, 0);
+  while (e < E) {
+    const int en = e + stride;
+    const int32_t* ce = conn + (size_t)e * D::N;
+    // ---- gather u as A fragments of stage A: A[m][l] = u[m][l]
+    double ua[D::MTM][D::KL];
+#pragma unroll
+    for (int mm = 0; mm < D::MTM; ++mm)
+#pragma unroll
+      for (int kl = 0; kl < D::KL; ++kl) {
+        const int m = mm * 8 + r4, l = kl * 4 + c4;
+        double v = 0.0;
+        if (m < D::NT && l < D::N1) {
+          const int g = __ldg(ce + m + D::NT * l);
+          if (g >= 0 || (flags & AP_GATHER_ALL)) v = __ldg(u + (g >= 0 ? g : ~g));
+        }
+        ua[mm][kl] = v;
+      }
+    __syncwarp();
+    if (en < E) issue_G(en, buf ^ 1);  // the other slot was released by the previous element
+    // ---- stage A: Ut, Udt [m][q]
+    double Ut[D::MTM][D::NQ][2], Udt[D::MTM][D::NQ][2];
+#pragma unroll
+    for (int mm = 0; mm < D::MTM; ++mm)
+#pragma unroll
+      for (int nq = 0; nq < D::NQ; ++nq) {
+        Ut[mm][nq][0] = Ut[mm][nq][1] = Udt[mm][nq][0] = Udt[mm][nq][1] = 0.0;
+#pragma unroll
+        for (int kl = 0; kl < D::KL; ++kl) {
+          aw_dmma(Ut[mm][nq][0], Ut[mm][nq][1], ua[mm][kl], fBt[kl][nq]);
+          aw_dmma(Udt[mm][nq][0], Udt[mm][nq][1], ua[mm][kl], fDt[kl][nq]);
+        }
+      }
+    // ---- B fragments of Ut, Udt for stage B: B[k=m][n=q]
+    double bU[D::KM][D::NQ], bD[D::KM][D::NQ];
+#pragma unroll
+    for (int km = 0; km < D::KM; ++km)
+#pragma unroll
+      for (int nq = 0; nq < D::NQ; ++nq) {
+        bU[km][nq] = aw_c_to_b(Ut[km >> 1][nq][0], Ut[km >> 1][nq][1], km, lane);
+        bD[km][nq] = aw_c_to_b(Udt[km >> 1][nq][0], Udt[km >> 1][nq][1], km, lane);
+      }
+    // ---- wait for this element's geometric factors
+    {
+      const uint32_t mb = aw_smem(mbar + 2 * warp + buf);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(mb), "r"((phase >> buf) & 1u)
+            : "memory");
+      phase ^= 1u << buf;
+    }
+    const double* Ge = gslot + buf * D::GSZ;
+    double Vt[D::MTM][D::NQ][2], Vdt[D::MTM][D::NQ][2];
+#pragma unroll
+    for (int mm = 0; mm < D::MTM; ++mm)
+#pragma unroll
+      for (int nq = 0; nq < D::NQ; ++nq) Vt[mm][nq][0] = Vt[mm][nq][1] = Vdt[mm][nq][0] = Vdt[mm][nq][1] = 0.0;
+#pragma unroll 1
+    for (int ma = 0; ma < D::MTA; ++ma) {
+      // ---- stage B for a-tile ma
+      double g[3][D::NQ][2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int nq = 0; nq < D::NQ; ++nq) g[c][nq][0] = g[c][nq][1] = 0.0;
+#pragma unroll
+      for (int km = 0; km < D::KM; ++km) {
+        const int off = (ma * 8 + r4) * D::LDM + km * 4 + c4;
+        const double ar = Bm[off], as = Bm[D::ROWSA * D::LDM + off], a0 = Bm[2 * D::ROWSA * D::LDM + off];
+#pragma unroll
+        for (int nq = 0; nq < D::NQ; ++nq) {
+          aw_dmma(g[0][nq][0], g[0][nq][1], ar, bU[km][nq]);
+          aw_dmma(g[1][nq][0], g[1][nq][1], as, bU[km][nq]);
+          aw_dmma(g[2][nq][0], g[2][nq][1], a0, bD[km][nq]);
+        }
+      }
+      // ---- w = G g at the points (a, q) of the C fragments
+#pragma unroll
+      for (int nq = 0; nq < D::NQ; ++nq)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int a = ma * 8 + r4, q = nq * 8 + 2 * c4 + i;
+          double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+          if (a < D::QT && q < D::QV) {
+            const double* gp = Ge + a + D::QT * q;
+            const double gxx = gp[0], gxy = gp[D::Q], gxz = gp[2 * D::Q], gyy = gp[3 * D::Q], gyz = gp[4 * D::Q],
+                         gzz = gp[5 * D::Q];
+            const double x0 = g[0][nq][i], x1 = g[1][nq][i], x2 = g[2][nq][i];
+            w0 = gxx * x0 + gxy * x1 + gxz * x2;
+            w1 = gxy * x0 + gyy * x1 + gyz * x2;
+            w2 = gxz * x0 + gyz * x1 + gzz * x2;
+          }
+          g[0][nq][i] = w0;
+          g[1][nq][i] = w1;
+          g[2][nq][i] = w2;
+        }
+      // ---- stage B^T: Vt += Br^T w_r + Bs^T w_s, Vdt += B0^T w_t over this a-tile (k = a)
+#pragma unroll
+      for (int ka = 0; ka < 2; ++ka) {
+        double bw[3][D::NQ];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int nq = 0; nq < D::NQ; ++nq) bw[c][nq] = aw_c_to_b(g[c][nq][0], g[c][nq][1], ka, lane);
+#pragma unroll
+        for (int mm = 0; mm < D::MTM; ++mm) {
+          const int off = (ma * 8 + ka * 4 + c4) * D::LDM + mm * 8 + r4;   // A[m][a] = B[a][m]
+          const double ar = Bm[off], as = Bm[D::ROWSA * D::LDM + off], a0 = Bm[2 * D::ROWSA * D::LDM + off];
+#pragma unroll
+          for (int nq = 0; nq < D::NQ; ++nq) {
+            aw_dmma(Vt[mm][nq][0], Vt[mm][nq][1], ar, bw[0][nq]);
+            aw_dmma(Vt[mm][nq][0], Vt[mm][nq][1], as, bw[1][nq]);
+            aw_dmma(Vdt[mm][nq][0], Vdt[mm][nq][1], a0, bw[2][nq]);
+          }
+        }
+      }
+    }
+    __syncwarp();  // every lane is done with this G slot before it is refilled
+    // ---- stage A^T: y[m][l] = Vt Bt + Vdt Dt (k = q), scatter
+#pragma unroll
+    for (int mm = 0; mm < D::MTM; ++mm) {
+      double yc[D::NL][2];
+#pragma unroll
+      for (int nl = 0; nl < D::NL; ++nl) yc[nl][0] = yc[nl][1] = 0.0;
+#pragma unroll
+      for (int kq = 0; kq < D::KQ; ++kq) {
+        const double at = aw_c_to_a(Vt[mm][kq >> 1][0], Vt[mm][kq >> 1][1], kq, lane);
+        const double ad = aw_c_to_a(Vdt[mm][kq >> 1][0], Vdt[mm][kq >> 1][1], kq, lane);
+#pragma unroll
+        for (int nl = 0; nl < D::NL; ++nl) {
+          aw_dmma(yc[nl][0], yc[nl][1], at, gBt[kq][nl]);
+          aw_dmma(yc[nl][0], yc[nl][1], ad, gDt[kq][nl]);
+        }
+      }
+      const int m = mm * 8 + r4;
+      if (m < D::NT) {
+#pragma unroll
+        for (int nl = 0; nl < D::NL; ++nl)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int l = nl * 8 + 2 * c4 + i;
+            if (l < D::N1) {
+              const int g = __ldg(ce + m + D::NT * l);
+              if (g >= 0) atomicAdd(y + g, sgn * yc[nl][i]);
+              else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~g, sgn * yc[nl][i]);
+            }
+          }
+      }
+    }
+    buf ^= 1;
+    e = en;
+  }
+}
+
+template <int P>
+static void apply_warp_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags) {
+  using D = AW<P>;
+  static int grid_max = 0;
+  if (!grid_max) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_apply_warp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
+    int per_sm = 0, sms = 0, dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_warp<P>, 32 * D::W, D::SMEM));
+    grid_max = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  if (c->E_own == 0) return;
+  const int need = (c->E_own + D::W - 1) / D::W;
+  const int grid = need < grid_max ? need : grid_max;
+  k_apply_warp<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(c->E_own, L.conn, L.G, L.wmats, u, y, flags);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags) {
+  const DeviceLevel& L = c->L[level];
+  if (!L.wmats) return false;
+  switch (L.p) {
+    case 1: apply_warp_P<1>(c, L, u, y, flags); break;
+    case 2: apply_warp_P<2>(c, L, u, y, flags); break;
+    case 3: apply_warp_P<3>(c, L, u, y, flags); break;
+    case 4: apply_warp_P<4>(c, L, u, y, flags); break;
+    case 5: apply_warp_P<5>(c, L, u, y, flags); break;
+    case 6: apply_warp_P<6>(c, L, u, y, flags); break;
+    default: return false;
+  }
+  c->launches++;
+  return true;
+}
+
+}  // namespace sem

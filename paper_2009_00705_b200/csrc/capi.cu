@@ -251,7 +251,7 @@ void check_opts(const sem_opts& o) {
   if (o.local_solve == 1 && o.nranks > 1)
     throw SemError(SEM_EUNSUPPORTED, "FDM local solves are single-domain only (nranks = 1)");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
-      o.apply_kernel > 1 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
+      o.apply_kernel > 2 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
       o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
     throw SemError(SEM_EINVAL, "bad options");
 }
@@ -389,6 +389,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
     }
     L.mats = upload(c, mats);
     L.frag = upload(c, dmma_fragments(R));
+    if (L.p <= 6) L.wmats = upload(c, warp_apply_mats(R));
     // geometric factors from the finest nodal map (all held elements)
     L.G = dalloc<double>(c, (size_t)E * 6 * L.Q);
     {

@@ -197,7 +197,8 @@ static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y
 }
 
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
-  if (c->opts.apply_kernel == 0) {
+  if (c->opts.apply_kernel == 0 && launch_apply_warp(c, level, u, y, flags)) return;
+  if (c->opts.apply_kernel != 1) {
     launch_apply_dmma(c, level, u, y, flags);
     return;
   }

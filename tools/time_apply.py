@@ -26,8 +26,9 @@ else:
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 nodes = m.node_xyz(lib.reference_nodes(m.p))
-for variant in (0, 1):
-    kw = dict(apply_kernel=variant)
+VARIANTS = {0: "warp-dmma", 1: "fma", 2: "batched-dmma"}
+for variant in [int(v) for v in os.environ.get("VARIANTS", "0,2").split(",")]:
+    kw = dict(apply_kernel=variant, local_solve=1)
     if a.levels:
         kw["levels"] = [int(x) for x in a.levels.split(",")]
     s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=nodes, overlap=0, **kw) if a.config == "config4" \
@@ -45,7 +46,7 @@ for variant in (0, 1):
     t = e0.elapsed_time(e1) / a.reps * 1e-3
     b = apply_bytes_model(s, m)
     f = apply_flops_model(m.p, s.info["n_elem"])
-    print(json.dumps({"config": a.config, "p": m.p, "variant": ["dmma", "fma"][variant], "us": t * 1e6,
+    print(json.dumps({"config": a.config, "p": m.p, "variant": VARIANTS[variant], "us": t * 1e6,
                       "MDOF_s": s.info["n_dof"] / t / 1e6, "GBs": b / t / 1e9, "frac_hbm": b / t / 1e9 / peak,
                       "TFLOPs": f / t / 1e12, "n_dof": s.info["n_dof"]}))
     s.close()
