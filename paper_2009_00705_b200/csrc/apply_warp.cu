@@ -49,7 +49,7 @@ struct AW {
   static constexpr int LDM = 8 * MTM + 4;       // row stride of Bm (= 4 mod 8: conflict-free both ways)
   static constexpr int ROWSA = 8 * MTA;
   static constexpr int BM = 3 * ROWSA * LDM;    // doubles of Bm [3][ROWSA][LDM] (Br, Bs, B0)
-  static constexpr int W = (P <= 5) ? 8 : 4;    // warps per CTA
+  static constexpr int W = (P <= 3) ? 16 : ((P <= 5) ? 8 : 4);   // warps per CTA
   static constexpr int GSZ = 6 * Q;             // doubles of one element's G
   static constexpr int SMEM = (BM + 2 * W * GSZ) * 8 + 2 * W * 8;
   static_assert(SMEM <= 227 * 1024, "apply_warp shared memory");
@@ -167,25 +167,49 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
           : "memory");
     }
   };
-  int buf = 0;
-  if (e < E) issue_G(e, 0);
-  while (e < E) {
-    const int en = e + stride;
-    const int32_t* ce = conn + (size_t)e * D::N;
-    // ---- gather u as A fragments of stage A: A[m][l] = u[m][l]
-    double ua[D::MTM][D::KL];
+  // connectivity of the A-fragment positions (m = 8 mm + r4, l = 4 kl + c4) and gather of u
+  auto load_conn_a = [&](int el, int (&cA)[D::MTM][D::KL]) {
+    const int32_t* ce = conn + (size_t)el * D::N;
 #pragma unroll
     for (int mm = 0; mm < D::MTM; ++mm)
 #pragma unroll
       for (int kl = 0; kl < D::KL; ++kl) {
         const int m = mm * 8 + r4, l = kl * 4 + c4;
-        double v = 0.0;
-        if (m < D::NT && l < D::N1) {
-          const int g = __ldg(ce + m + D::NT * l);
-          if (g >= 0 || (flags & AP_GATHER_ALL)) v = __ldg(u + (g >= 0 ? g : ~g));
-        }
-        ua[mm][kl] = v;
+        cA[mm][kl] = (m < D::NT && l < D::N1) ? __ldg(ce + m + D::NT * l) : INT_MIN;
       }
+  };
+  auto gather_u = [&](const int (&cA)[D::MTM][D::KL], double (&ua)[D::MTM][D::KL]) {
+#pragma unroll
+    for (int mm = 0; mm < D::MTM; ++mm)
+#pragma unroll
+      for (int kl = 0; kl < D::KL; ++kl) {
+        const int g = cA[mm][kl];
+        ua[mm][kl] = (g >= 0 || (g != INT_MIN && (flags & AP_GATHER_ALL))) ? __ldg(u + (g >= 0 ? g : ~g)) : 0.0;
+      }
+  };
+  int buf = 0;
+  int cA[D::MTM][D::KL];
+  double ua[D::MTM][D::KL];
+  if (e < E) {
+    issue_G(e, 0);
+    load_conn_a(e, cA);
+    gather_u(cA, ua);
+  }
+  while (e < E) {
+    const int en = e + stride;
+    const int32_t* ce = conn + (size_t)e * D::N;
+    // connectivity of this element's output positions (m = 8 mm + r4, l = 8 nl + 2 c4 + i), used at the end
+    int cY[D::MTM][D::NL][2];
+#pragma unroll
+    for (int mm = 0; mm < D::MTM; ++mm)
+#pragma unroll
+      for (int nl = 0; nl < D::NL; ++nl)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int m = mm * 8 + r4, l = nl * 8 + 2 * c4 + i;
+          cY[mm][nl][i] = (m < D::NT && l < D::N1) ? __ldg(ce + m + D::NT * l) : INT_MIN;
+        }
+    if (en < E) load_conn_a(en, cA);   // next element's gather positions (in flight during stage A)
     __syncwarp();
     if (en < E) issue_G(en, buf ^ 1);  // the other slot was released by the previous element
     // ---- stage A: Ut, Udt [m][q]
@@ -201,6 +225,9 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
           aw_dmma(Udt[mm][nq][0], Udt[mm][nq][1], ua[mm][kl], fDt[kl][nq]);
         }
       }
+    // ---- next element's u (in flight during stages B, G, B^T)
+    double un[D::MTM][D::KL];
+    if (en < E) gather_u(cA, un);
     // ---- B fragments of Ut, Udt for stage B: B[k=m][n=q]
     double bU[D::KM][D::NQ], bD[D::KM][D::NQ];
 #pragma unroll
@@ -305,20 +332,20 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
           aw_dmma(yc[nl][0], yc[nl][1], ad, gDt[kq][nl]);
         }
       }
-      const int m = mm * 8 + r4;
-      if (m < D::NT) {
 #pragma unroll
-        for (int nl = 0; nl < D::NL; ++nl)
+      for (int nl = 0; nl < D::NL; ++nl)
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int l = nl * 8 + 2 * c4 + i;
-            if (l < D::N1) {
-              const int g = __ldg(ce + m + D::NT * l);
-              if (g >= 0) atomicAdd(y + g, sgn * yc[nl][i]);
-              else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~g, sgn * yc[nl][i]);
-            }
-          }
-      }
+        for (int i = 0; i < 2; ++i) {
+          const int g = cY[mm][nl][i];
+          if (g >= 0) atomicAdd(y + g, sgn * yc[nl][i]);
+          else if (g != INT_MIN && (flags & AP_SCATTER_ALL)) atomicAdd(y + ~g, sgn * yc[nl][i]);
+        }
+    }
+    if (en < E) {
+#pragma unroll
+      for (int mm = 0; mm < D::MTM; ++mm)
+#pragma unroll
+        for (int kl = 0; kl < D::KL; ++kl) ua[mm][kl] = un[mm][kl];
     }
     buf ^= 1;
     e = en;
