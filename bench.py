@@ -32,7 +32,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="config3", choices=["config1", "config2", "config3"])
+    ap.add_argument("--config", default="config3", choices=["config1", "config2", "config3", "config5"])
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--smoother", default="dense", choices=["dense", "fdm"],
                     help="Schwarz local solves: exact dense inverses (eq 4.4) or FDM (reading O33)")
@@ -41,6 +41,8 @@ def parse():
                     help="1: FP32 storage of the exact Schwarz / coarse inverses, FP64 arithmetic (P:35)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the variant solves (FDM local solves, mixed-precision storage) reported beside the headline")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="validation only: run the partitioned solve with R emulated ranks on one GPU")
     return ap.parse_args()
@@ -48,13 +50,16 @@ def parse():
 
 def make_mesh(name):
     from workloads import config1, config2, config3
-    return {"config1": config1, "config2": config2, "config3": config3}[name]()
+    from workloads.config5 import config5
+    return {"config1": config1, "config2": config2, "config3": config3, "config5": config5}[name]()
 
 
 WORKLOAD = {
     "config1": "config1: box [0,2]x[0,1]x[-1,0], 64 straight prisms, p=3",
     "config2": "config2: wave channel [0,16]x[0,1], 2048 curved prisms, p=4",
     "config3": "config3: 3D wave basin [0,32]^2, 8192 jittered triangles x 8 layers = 65,536 curved prisms, p=5",
+    "config5": "config5: basin [0,64]x[0,32] with a box hull 8x2x0.6 (bilge r=0.2), graded jittered Delaunay "
+               "61,428 triangles x 5/8 layers = 477,600 curved prisms, p=6",
 }
 
 
@@ -162,6 +167,54 @@ def run_reference(args, rank, world):
     }))
 
 
+# ------------------------------------------------------------------ variants
+VARIANTS = [
+    ("fdm", "FDM local solves (reading O33) of the same Schwarz subdomains, overlap 1",
+     dict(local_solve=1, overlap=1)),
+    ("mixed", "exact dense local inverses and coarse inverse STORED in FP32, FP64 arithmetic (P:35)",
+     dict(local_solve=0, overlap=1, mixed_precision=1)),
+]
+
+
+def run_variants(args, lib, m, phiD_h, peak, base_kw):
+    """The same workload and stop test with the other smoother implementations
+    (not the headline: the headline is the paper's exact local inverses)."""
+    import torch
+    out = []
+    for name, desc, extra in VARIANTS:
+        kw = dict(base_kw)
+        kw.update(extra)
+        if kw == base_kw:
+            continue
+        t0 = time.perf_counter()
+        s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)), **kw)
+        setup_s = time.perf_counter() - t0
+        phiD = torch.from_numpy(phiD_h).cuda()
+        phi = s.empty(0)
+        for _ in range(args.warmup):
+            s.solve(phiD, args.tol, out=phi)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s.stream)
+        for _ in range(args.steps):
+            _, rep = s.solve(phiD, args.tol, out=phi)
+        e1.record(s.stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        us, b = s.bench_kernel("schwarz", 0, 20)
+        ach = b / (us * 1e-6) / 1e9
+        out.append({"name": name, "smoother": desc, "value": s.info["n_free"] / (ms * 1e-3) / 1e6,
+                    "unit": "MDOF/s", "ms_per_step": ms, "iters": rep["iters"], "vcycles": rep["vcycles"],
+                    "rel_res": rep["rel_res"], "setup_s": setup_s,
+                    "smoother_kernel": {"kernel": "k_fdm_warp" if extra.get("local_solve") else "k_schwarz<float>",
+                                        "us": us, "alg_bytes_per_launch": b, "achieved_GBs": ach,
+                                        "frac_hbm": ach / peak}})
+        s.close()
+        del s
+        torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     args = parse()
@@ -247,7 +300,8 @@ def main():
     if world == 1 and args.emulate_ranks <= 1 and args.config == "config3" and args.smoother == "dense" and not args.mixed:
         roof["traffic"] = 28.92e9
     ach_a = b_a / (us_a * 1e-6) / 1e9
-    apply = {"kernel": "k_apply_dmma<%d> (FP64 tensor cores)" % m.p, "us": us_a, "alg_bytes_per_launch": b_a,
+    apply = {"kernel": "k_apply_warp<%d> (FP64 tensor cores, warp per element)" % m.p, "us": us_a,
+             "alg_bytes_per_launch": b_a,
              "achieved_GBs": ach_a, "frac": ach_a / peak,
              "MDOF_s": info["n_dof"] / us_a if world == 1 else None}
     # ---- end to end through the public host API (pinned host buffers, H2D + D2H inside)
@@ -265,6 +319,9 @@ def main():
         e2e = {"value": n_free / t_e2e / 1e6, "unit": "MDOF/s",
                "h2d_bytes_per_step": info["n_dof"] * 8, "d2h_bytes_per_step": info["n_dof"] * 8,
                "ms_per_step": t_e2e * 1e3, "api": "laplace_solve_host (pinned host buffers)"}
+    variants = None
+    if world == 1 and args.emulate_ranks <= 1 and not args.no_variants:
+        variants = run_variants(args, lib, m, phiD_h, peak, kw)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = oracle_sample(args.tol)
@@ -289,7 +346,8 @@ def main():
                        else (f"{args.emulate_ranks} emulated ranks on 1 GPU (validation, not a scaling number)"
                              if args.emulate_ranks > 1 else "single GPU"), "setup_s": setup_s},
             "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "q_mean": rep["q_mean"],
-            "roofline": roof, "apply": apply, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "apply": apply, "variants": variants, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
             "clocks": clocks,
         }
         print(json.dumps(out), flush=True)

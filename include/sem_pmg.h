@@ -242,10 +242,12 @@ int sem_host_numbering(const sem_mesh *mesh, int p, int64_t *n_dof, int64_t *n_f
  * weights of eq 4.6 (0 on Dirichlet nodes).  Two-call pattern as above. */
 int sem_host_schwarz(const sem_mesh *mesh, int p, int overlap, int64_t *total, int64_t *off,
                      int32_t *idx, double *W);
-/* Subdomains of the FDM local solves (opts.local_solve = 1, reading O33) on
- * level order p with `overlap`: off [n_prism+1], idx [total] sorted free node
- * ids of each product subdomain H_k x V_k, W [n_dof] (eq 4.6).  Needs a layered
- * mesh (SEM_EUNSUPPORTED otherwise).  Two-call pattern as above. */
+/* Subdomains of the smoother with FDM local solves (opts.local_solve = 1,
+ * reading O33) on level order p with `overlap`: off [n_prism+1], idx [total]
+ * sorted free node ids of each subdomain -- the product box H_k x V_k where it
+ * is regular, the reading-O15 set where the exact local inverse is kept
+ * (reading O35) -- and W [n_dof] (eq 4.6).  Needs a layered mesh
+ * (SEM_EUNSUPPORTED otherwise).  Two-call pattern as above. */
 int sem_host_fdm(const sem_mesh *mesh, int p, int overlap, int64_t *total, int64_t *off, int32_t *idx,
                  double *W);
 /* Column partition used by the partitioned solve (opts.nranks > 1), level

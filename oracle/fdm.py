@@ -32,6 +32,12 @@ numpy.linalg.inv):
   are Dirichlet (the free surface);
 * local solve: (B~_k^{-1}) restricted to the box entries that exist and are
   free; W from the subdomain counts (eq 4.6).
+
+Reading O35 (hybrid): the separable form is only used where the box is a
+regular product -- every line of H_k has as many z-levels as element k's own
+column.  Next to a body (config 5) the patch mixes columns of different
+heights and the geometry is far from separable; those subdomains keep the
+paper's exact local inverse of eq 4.4 on their reading-O15 node set.
 """
 from __future__ import annotations
 
@@ -160,6 +166,21 @@ class Columns:
         for _ in range(overlap):
             cur = np.union1d(cur, self.adj[cur].indices)
         return cur
+
+
+def regular(cols: Columns, overlap: int):
+    """[E] bool: reading O35 -- every line of element k's patch has the length of
+    k's own column lines (Z_c + 1 z-levels)."""
+    linelen = (cols.node_at >= 0).sum(axis=1)
+    out = np.zeros(len(cols.col), dtype=bool)
+    cache = {}
+    for k in range(len(cols.col)):
+        c = int(cols.col[k])
+        if c not in cache:
+            H = cols.patch(c, overlap)
+            cache[c] = bool(np.all(linelen[H] == cols.p * len(cols.col_elems[c]) + 1))
+        out[k] = cache[c]
+    return out
 
 
 def fdm_blocks(mesh, level: sem.Level, overlap: int, cols: Columns | None = None):

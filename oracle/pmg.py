@@ -116,15 +116,34 @@ def build_smoother(level: sem.Level, AFF: sp.csr_matrix, overlap: int) -> Smooth
     return Smoother(sets=sets, inv=inv, W=1.0 / count)
 
 
-def build_fdm_smoother(mesh, level: sem.Level, overlap: int) -> Smoother:
-    """eq 4.4 with the FDM local inverses of reading O33 (oracle/fdm.py)."""
+def hybrid_sets(mesh, level: sem.Level, overlap: int):
+    """Node sets (global ids) of the FDM smoother's subdomains: the product box
+    where it is regular, the O15 set elsewhere (reading O35)."""
+    cols = fdm.Columns(mesh, level)
+    reg = fdm.regular(cols, overlap)
+    dense = schwarz_sets(level, overlap) if not reg.all() else None
+    return [np.sort(ids) if reg[k] else dense[k]
+            for k, (ids, _) in enumerate(fdm.fdm_blocks(mesh, level, overlap, cols))], reg
+
+
+def build_fdm_smoother(mesh, level: sem.Level, overlap: int, AFF: sp.csr_matrix | None = None) -> Smoother:
+    """eq 4.4 with the FDM local inverses of reading O33 (oracle/fdm.py) on the
+    regular subdomains and the exact (R_k A R_k^T)^{-1} on the others (O35)."""
     F = level.free
     fid = np.full(level.n, -1, dtype=np.int64)
     fid[F] = np.arange(len(F))
+    cols = fdm.Columns(mesh, level)
+    reg = fdm.regular(cols, overlap)
+    dense_sets = schwarz_sets(level, overlap) if not reg.all() else None
+    Ad = AFF.tocsr() if AFF is not None else None
     sets, inv = [], []
     count = np.zeros(len(F))
-    for ids, Binv in fdm.fdm_blocks(mesh, level, overlap):
-        I = fid[ids]
+    for k, (ids, Binv) in enumerate(fdm.fdm_blocks(mesh, level, overlap, cols)):
+        if not reg[k]:
+            I = fid[dense_sets[k]]
+            Binv = np.linalg.inv(Ad[I][:, I].toarray())
+        else:
+            I = fid[ids]
         sets.append(I)
         inv.append(Binv)
         count[I] += 1.0
@@ -164,7 +183,7 @@ class PMG:
             else:
                 ov = overlap if overlap >= 0 else (ml.level.p + 2) // 2   # refined: ceil((P+1)/2)
                 if local_solve == "fdm":
-                    ml.smoother = build_fdm_smoother(mesh, ml.level, ov)
+                    ml.smoother = build_fdm_smoother(mesh, ml.level, ov, ml.A)
                 else:
                     ml.smoother = build_smoother(ml.level, ml.A, ov)
 

@@ -62,7 +62,8 @@ double now_ms() {
 void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas, cusolverDnHandle_t sol,
                    const double* d_D, int verbose) {
   DeviceLevel& L = c->L[li];
-  const int E = c->E_own;  // one subdomain per owned element
+  const int E = (int)S.off.size() - 1;  // subdomains (one per owned element, or the dense subset of O35)
+  L.nsub = E;
   double t0 = now_ms();
   double t1 = now_ms();
   // padded index lists and tile offsets
@@ -454,6 +455,26 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
         const int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
         FdmTopo F = fdm_topology(gm.hm, gm.topo[lid], gm.X, p, ov);
         if (o.verbose) fprintf(stderr, "[sem] level p=%d FDM topology %.0f ms\n", c->L[li].p, now_ms() - t0);
+        int64_t nirr = 0;
+        for (uint8_t r : F.regular) nirr += !r;
+        if (nirr > 0) {  // reading O35: exact dense local inverses on the irregular subdomains
+          SchwarzTopo S = schwarz_topology(gm.topo[lid], E, ov, std::min(32, std::max(1, omp_get_max_threads())));
+          SchwarzTopo Sd = schwarz_subset(S, F.regular);
+          // W of the hybrid smoother: counts over the FDM boxes of the regular and the O15 sets of the others
+          std::vector<double> cnt(gm.topo[lid].n, 0.0);
+          for (int e = 0; e < E; ++e)
+            if (F.regular[e]) {
+              for (int64_t t = F.ioff[e]; t < F.ioff[e + 1]; ++t)
+                if (F.idx[t] >= 0) cnt[F.idx[t]] += 1.0;
+            } else {
+              for (int64_t t = S.off[e]; t < S.off[e + 1]; ++t) cnt[S.idx[t]] += 1.0;
+            }
+          for (int64_t i = 0; i < gm.topo[lid].n; ++i)
+            F.W[i] = gm.topo[lid].dir[i] ? 0.0 : 1.0 / cnt[i];
+          setup_schwarz(c, li, Sd, blas, sol, d_D, o.verbose);
+          if (o.verbose) fprintf(stderr, "[sem] level p=%d hybrid: %lld of %d subdomains dense (O35)\n", c->L[li].p,
+                                 (long long)nirr, E);
+        }
         setup_fdm(c, li, F, sol, blas, o.verbose);
       } else {
         const int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
@@ -952,7 +973,8 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
     if (mean_us) *mean_us = 1e3 * ms / reps;
     if (alg_bytes) {
       if (kernel == 0 && L.fdm)
-        *alg_bytes = (double)L.schwarz_bytes + 32.0 * L.n;
+        *alg_bytes = (double)L.f_bytes + (L.tiles32 ? 4.0 : 8.0) * L.packed + 32.0 * L.n +
+                     (L.nsub ? 4.0 * L.nk_sum : 0.0);
       else if (kernel == 0)
         *alg_bytes = (L.tiles32 ? 4.0 : 8.0) * L.packed + 4.0 * L.nk_sum + 32.0 * L.n;
       else
@@ -1105,16 +1127,27 @@ int sem_host_fdm(const sem_mesh* mesh, int p, int overlap, int64_t* total, int64
     prepare_global(mesh, p, o, gm);
     FdmTopo F = fdm_topology(gm.hm, gm.topo[0], gm.X, p, overlap);
     const int E = gm.hm.E;
+    SchwarzTopo S;
+    bool hybrid = false;
+    for (uint8_t r : F.regular) hybrid |= !r;
+    if (hybrid) S = schwarz_topology(gm.topo[0], E, overlap, std::min(32, std::max(1, omp_get_max_threads())));
     std::vector<int64_t> o2(E + 1, 0);
     std::vector<int32_t> all;
+    std::vector<double> cnt(gm.topo[0].n, 0.0);
     for (int e = 0; e < E; ++e) {
       std::vector<int32_t> s;
-      for (int64_t t = F.ioff[e]; t < F.ioff[e + 1]; ++t)
-        if (F.idx[t] >= 0) s.push_back(F.idx[t]);
+      if (F.regular[e]) {
+        for (int64_t t = F.ioff[e]; t < F.ioff[e + 1]; ++t)
+          if (F.idx[t] >= 0) s.push_back(F.idx[t]);
+      } else {  // reading O35: exact local inverse on the O15 set
+        s.assign(S.idx.begin() + S.off[e], S.idx.begin() + S.off[e + 1]);
+      }
       std::sort(s.begin(), s.end());
+      for (int32_t g : s) cnt[g] += 1.0;
       all.insert(all.end(), s.begin(), s.end());
       o2[e + 1] = (int64_t)all.size();
     }
+    for (int64_t i = 0; i < gm.topo[0].n; ++i) F.W[i] = gm.topo[0].dir[i] ? 0.0 : 1.0 / cnt[i];
     if (total) *total = (int64_t)all.size();
     if (off) std::copy(o2.begin(), o2.end(), off);
     if (idx) std::copy(all.begin(), all.end(), idx);

@@ -341,7 +341,16 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
       }
     }
   }
-  // ---- 9. weights (eq 4.6) over the FDM subdomains
+  // ---- 9. regular boxes (reading O35): every line of the patch as tall as the column's own lines
+  {
+    std::vector<uint8_t> creg(ncol, 1);
+    for (int c = 0; c < ncol; ++c)
+      for (int64_t a = F.hoff[c]; a < F.hoff[c + 1]; ++a)
+        if (linelen[F.hnode[a]] != nlay[c] * p + 1) creg[c] = 0;
+    F.regular.resize(E);
+    for (int e = 0; e < E; ++e) F.regular[e] = creg[F.col[e]];
+  }
+  // ---- 10. weights (eq 4.6) over the FDM subdomains
   std::vector<double> cnt(L.n, 0.0);
   for (int32_t g : F.idx)
     if (g >= 0) cnt[g] += 1.0;

@@ -253,15 +253,21 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
   L.fdm = 1;
   L.f_nh_max = F.nh_max;
   L.f_nv_max = F.nv_max;
-  L.nk_sum = 0;
-  for (int32_t g : F.idx) L.nk_sum += (g >= 0);
+  for (int e = 0; e < E; ++e)
+    if (F.regular[e])
+      for (int64_t t = F.ioff[e]; t < F.ioff[e + 1]; ++t) L.nk_sum += (F.idx[t] >= 0);
+  {
+    std::vector<uint8_t> skip(E);
+    for (int e = 0; e < E; ++e) skip[e] = F.regular[e] ? 0 : 1;
+    L.f_skip = upload(c, skip);
+  }
   // algorithmic bytes of one sweep (column-batched kernel): per column S_h, l_h and the patch
   // node ids [n_h][Z_c+1]; per element S_v, l_v
-  L.schwarz_bytes = 8 * (F.moff[ncol] + F.hoff[ncol] + F.voff[E] + acc) + 4 * F.cioff[ncol];
-  L.packed = 0;
+  L.f_bytes = 8 * (F.moff[ncol] + F.hoff[ncol] + F.voff[E] + acc) + 4 * F.cioff[ncol];
+  L.schwarz_bytes += L.f_bytes;  // plus the dense part of an O35 hybrid (setup_schwarz ran first)
   if (verbose)
     fprintf(stderr, "[sem] level p=%d FDM: %d columns, n_h max %d, n_v max %d, %.1f MiB, %.0f ms\n", L.p, ncol,
-            F.nh_max, F.nv_max, L.schwarz_bytes / 1048576.0, now_ms() - t0);
+            F.nh_max, F.nv_max, L.f_bytes / 1048576.0, now_ms() - t0);
 }
 
 // ---------------------------------------------------------------- apply
@@ -274,9 +280,11 @@ __global__ void __launch_bounds__(256) k_fdm(const int32_t* __restrict__ col, co
                                              const double* __restrict__ Sh, const double* __restrict__ lh,
                                              const double* __restrict__ Sv, const double* __restrict__ lv,
                                              const double* __restrict__ W, const double* __restrict__ r,
-                                             double* __restrict__ u, int transpose, int box_max) {
+                                             double* __restrict__ u, int transpose, int box_max,
+                                             const uint8_t* __restrict__ skip) {
   extern __shared__ double sm[];
   const int k = blockIdx.x;
+  if (skip[k]) return;
   const int c = col[k];
   const int nh = (int)(hoff[c + 1] - hoff[c]);
   const int nv = nvv[k];
@@ -372,7 +380,8 @@ __global__ void __launch_bounds__(256) k_fdm_col(const int4* __restrict__ units,
                                                  const int32_t* __restrict__ nvv, const double* __restrict__ Sh,
                                                  const double* __restrict__ lh, const double* __restrict__ Svp,
                                                  const double* __restrict__ lvp, const double* __restrict__ W,
-                                                 const double* __restrict__ r, double* __restrict__ u, int transpose) {
+                                                 const double* __restrict__ r, double* __restrict__ u, int transpose,
+                                                 const uint8_t* __restrict__ skip) {
   constexpr int ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, EMAX = FDM_NT / NVT, LD = FDM_LD;
   extern __shared__ __align__(16) double sm[];
   double* Bc = sm;              // [ROWS][LD]  boxes, later Y
@@ -386,11 +395,13 @@ __global__ void __launch_bounds__(256) k_fdm_col(const int4* __restrict__ units,
   const int32_t* ci = cidx + cioff[c];
   const double* S = Sh + moff[c];
   const double* Lh = lh + hoff[c];
+  __shared__ int eskip[EMAX];
   if (tid < cnt) {
     const int e = colel[first + tid];
     eid[tid] = e;
     ez0[tid] = z0[e];
     env[tid] = nvv[e];
+    eskip[tid] = skip[e];
   }
   __syncthreads();
   const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
@@ -410,7 +421,7 @@ __global__ void __launch_bounds__(256) k_fdm_col(const int4* __restrict__ units,
   for (int t = tid; t < ROWS * FDM_NC; t += blockDim.x) {
     const int h = t / FDM_NC, col = t - h * FDM_NC, j = col / NVP, b = col - j * NVP;
     double v = 0.0;
-    if (h < nh && j < cnt && b < env[j]) v = Tm[h * LD + ez0[j] - zlo + b];
+    if (h < nh && j < cnt && b < env[j] && !eskip[j]) v = Tm[h * LD + ez0[j] - zlo + b];
     Bc[h * LD + col] = v;
   }
   __syncthreads();
@@ -523,7 +534,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 1) k_fdm_warp(const int4* 
                                                   const double* __restrict__ lh, const double* __restrict__ Svp,
                                                   const double* __restrict__ lvp, const double* __restrict__ W,
                                                   const double* __restrict__ r, double* __restrict__ u, int transpose,
-                                                  int ldr) {
+                                                  int ldr, const uint8_t* __restrict__ skip) {
   constexpr int ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
   extern __shared__ __align__(16) double sm[];
   double* Ss = sm;                  // [ROWS][LDS]  S_h (row i node, col a mode), zero padded
@@ -581,8 +592,8 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 1) k_fdm_warp(const int4* 
     }
   }
   __syncthreads();
-  const bool active = warp < cnt;
-  const int j = active ? warp : 0;
+  const bool active = warp < cnt && !skip[eid[warp < cnt ? warp : 0]];
+  const int j = warp < cnt ? warp : 0;
   const int zb = ez0[j] - zlo, nvj = env[j];
   double b1[KT][NVT];
 #pragma unroll
@@ -723,7 +734,8 @@ static void fdm_warp_launch(sem_ctx* c, const DeviceLevel& L, const double* r, d
   }
   k_fdm_warp<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
                                                              L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
-                                                             L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_ldr);
+                                                             L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_ldr,
+                                                             L.f_skip);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -756,7 +768,7 @@ static void fdm_col_launch(sem_ctx* c, const DeviceLevel& L, const double* r, do
   }
   k_fdm_col<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
                                                             L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
-                                                            L.f_Svp, L.f_lvp, L.W, r, u, transpose);
+                                                            L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_skip);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -815,7 +827,8 @@ void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose
     attr = smem;
   }
   k_fdm<<<c->E_own, 256, smem, c->stream>>>(L.f_col, L.f_hoff, L.f_moff, L.f_nv, L.f_voff, L.f_lvoff, L.f_ioff,
-                                            L.f_idx, L.f_Sh, L.f_lh, L.f_Sv, L.f_lv, L.W, r, u, transpose, box);
+                                            L.f_idx, L.f_Sh, L.f_lh, L.f_Sv, L.f_lv, L.W, r, u, transpose, box,
+                                            L.f_skip);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }

@@ -66,6 +66,9 @@ struct DeviceLevel {
   int32_t *f_colel = nullptr, *f_nzc = nullptr, *f_cidx = nullptr, *f_z0 = nullptr;
   int64_t* f_cioff = nullptr;
   int64_t schwarz_bytes = 0;
+  int64_t f_bytes = 0;          // algorithmic bytes of one FDM sweep (fdm.cu)
+  int nsub = 0;                 // dense subdomains (all owned elements, or the O35 subset of an FDM level)
+  uint8_t* f_skip = nullptr;    // [E] 1 = subdomain solved densely (O35), skipped by the FDM kernels
   int64_t nk_sum = 0, packed = 0;
   int max_tiles_1d = 0;
   // transfer from the next coarser level (level+1 -> this)

@@ -355,25 +355,25 @@ void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int trans
   const DeviceLevel& L = c->L[level];
   if (L.fdm) {
     launch_fdm(c, level, r, u, transpose);
-    return;
+    if (L.nsub == 0) return;  // else: the dense subdomains of an O35 hybrid follow
   }
   const int npad = 16 * L.max_tiles_1d;
   const int smem = 9 * npad * (int)sizeof(double);
   static int attr_set = 0, attr_set32 = 0;
-  if (c->E_own == 0) return;
+  if (L.nsub == 0) return;
   if (L.tiles32) {  // mixed precision: FP32 storage of the exact inverses, FP64 arithmetic
     if (smem > 48 * 1024 && smem > attr_set32) {
       CUDA_CHECK(cudaFuncSetAttribute(k_schwarz<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr_set32 = smem;
     }
-    k_schwarz<float><<<c->E_own, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles32, L.W, r, u,
+    k_schwarz<float><<<L.nsub, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles32, L.W, r, u,
                                                          transpose, npad);
   } else {
     if (smem > 48 * 1024 && smem > attr_set) {
       CUDA_CHECK(cudaFuncSetAttribute(k_schwarz<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr_set = smem;
     }
-    k_schwarz<double><<<c->E_own, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u,
+    k_schwarz<double><<<L.nsub, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u,
                                                           transpose, npad);
   }
   CUDA_CHECK(cudaGetLastError());

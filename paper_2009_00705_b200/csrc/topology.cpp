@@ -303,4 +303,20 @@ SchwarzTopo schwarz_topology(const LevelTopo& L, int E, int overlap, int nthread
   return S;
 }
 
+SchwarzTopo schwarz_subset(const SchwarzTopo& S, const std::vector<uint8_t>& keep_if_zero) {
+  SchwarzTopo D;
+  D.off.push_back(0);
+  D.eoff.push_back(0);
+  for (size_t k = 0; k + 1 < S.off.size(); ++k) {
+    if (keep_if_zero[k]) continue;
+    D.idx.insert(D.idx.end(), S.idx.begin() + S.off[k], S.idx.begin() + S.off[k + 1]);
+    D.elist.insert(D.elist.end(), S.elist.begin() + S.eoff[k], S.elist.begin() + S.eoff[k + 1]);
+    D.off.push_back((int64_t)D.idx.size());
+    D.eoff.push_back((int64_t)D.elist.size());
+    D.max_nk = std::max<int>(D.max_nk, (int)(S.off[k + 1] - S.off[k]));
+  }
+  D.W = S.W;
+  return D;
+}
+
 }  // namespace sem

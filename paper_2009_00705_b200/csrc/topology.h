@@ -43,5 +43,7 @@ struct SchwarzTopo {
   int max_nk = 0;
 };
 SchwarzTopo schwarz_topology(const LevelTopo& L, int E, int overlap, int nthreads);
+// the subdomains k with keep[k] == 0 (W is left to the caller)
+SchwarzTopo schwarz_subset(const SchwarzTopo& S, const std::vector<uint8_t>& keep_if_zero);
 
 }  // namespace sem

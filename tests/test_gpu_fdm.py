@@ -27,7 +27,13 @@ CASES = {
     "c3s": lambda: (_c3_small(), 1),
     "c3s_refined": lambda: (_c3_small(), -1),       # overlap ceil((P+1)/2) per level
     "c2_o0": lambda: (config2(p=4, nx=32, ny=2, nz=3), 0),
+    "c5r": lambda: (_c5_replica(), 1),            # hull: FDM / exact-dense hybrid (reading O35)
 }
+
+
+def _c5_replica():
+    from workloads.config5 import config5
+    return config5(p=3, hf=0.5, Lx=16.0, Ly=10.0)
 
 
 @pytest.fixture(scope="module", params=list(CASES))
@@ -85,3 +91,18 @@ def test_fdm_equals_dense_on_straight_prisms():
         sf.schwarz(0, r, uf, transpose=tr)
         sd.schwarz(0, r, ud, transpose=tr)
         assert rel(uf.cpu().numpy(), ud.cpu().numpy()) <= 1e-12
+
+
+def test_config5_replica_dense_smoother_solve():
+    """The paper's exact smoother on the hull replica: solve parity vs sparse direct."""
+    from tests.test_gpu_parity import make_solver
+    from tests._mapping import lib_to_oracle
+    m = _c5_replica()
+    s = make_solver(m)
+    lev = sem.build_system(m, m.p)
+    perm = lib_to_oracle(s.node_xyz(0), lev.xyz)
+    phiD = m.phi(*lev.xyz.T)
+    phi, rep = s.solve(torch.from_numpy(np.ascontiguousarray(phiD[perm])).cuda(), tol=1e-13)
+    out = np.zeros(lev.n)
+    out[perm] = phi.cpu().numpy()
+    assert rep["converged"] and rel(out, sem.solve_direct(lev, phiD)) <= SOLVE_TOL

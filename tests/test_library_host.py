@@ -110,10 +110,11 @@ def test_fdm_sets_match_oracle(p, overlap):
     perm = lib_to_oracle(lib_node_xyz(m, conn, lib.reference_nodes(p)), lev.xyz)
     sets, W = lib.host_fdm(m.vertices, m.prisms, m.face_tag, p, overlap,
                            node_xyz=m.node_xyz(lib.reference_nodes(m.p)))
-    blocks = fdm.fdm_blocks(m, lev, overlap)
+    osets, reg = pmg.hybrid_sets(m, lev, overlap)
+    assert reg.all()
     cnt = np.zeros(lev.n)
-    for k, (ids, _) in enumerate(blocks):
-        np.testing.assert_array_equal(np.sort(perm[sets[k]]), np.sort(ids))
+    for k, ids in enumerate(osets):
+        np.testing.assert_array_equal(np.sort(perm[sets[k]]), ids)
         cnt[ids] += 1
     Wo = np.where(lev.dirichlet, 0.0, 1.0 / np.maximum(cnt, 1))
     np.testing.assert_allclose(W, Wo[perm], rtol=0, atol=0)
@@ -126,3 +127,23 @@ def test_fdm_rejects_unlayered_mesh():
     prisms[1, :3] = prisms[0, :3]
     with pytest.raises(lib.SemError):
         lib.host_fdm(m.vertices, prisms, m.face_tag, 2, 1)
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_hybrid_sets_match_oracle_on_hull_mesh(p):
+    """Config-5 construction (hull, graded jittered Delaunay, 5/8-layer columns):
+    the library's FDM/dense split (reading O35), node sets and W equal the oracle's."""
+    from workloads.config5 import config5
+    m = config5(p=p, hf=0.5, Lx=16.0, Ly=10.0)
+    conn, dirm, _ = lib.host_numbering(m.vertices, m.prisms, m.face_tag, p)
+    lev = sem.build_level(m, p)
+    perm = lib_to_oracle(lib_node_xyz(m, conn, lib.reference_nodes(p)), lev.xyz)
+    sets, W = lib.host_fdm(m.vertices, m.prisms, m.face_tag, p, 1, node_xyz=m.node_xyz(lib.reference_nodes(p)))
+    osets, reg = pmg.hybrid_sets(m, lev, 1)
+    assert 0 < (~reg).sum() < len(reg)
+    cnt = np.zeros(lev.n)
+    for k, ids in enumerate(osets):
+        np.testing.assert_array_equal(np.sort(perm[sets[k]]), ids)
+        cnt[ids] += 1
+    Wo = np.where(lev.dirichlet, 0.0, 1.0 / np.maximum(cnt, 1))
+    np.testing.assert_allclose(W, Wo[perm], rtol=0, atol=0)
