@@ -132,21 +132,35 @@ void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas
   }
   const double one = 1.0, zero = 0.0;
   std::vector<int> hinfo(nb);
+  // element matrices are formed per chunk of subdomains, only for the elements the
+  // chunk's subdomains touch (a compact list: subsets of O35 are scattered)
+  std::vector<int32_t> ulist, slots, stamp(c->E, -1);
+  int32_t* d_ulist = sc.get<int32_t>((size_t)cap);
+  int32_t* d_slots = sc.get<int32_t>((size_t)std::max<int64_t>(1, S.eoff[E]));
   for (int k0 = 0; k0 < E;) {
     int cnt = 0;
-    int64_t emin = INT64_MAX, emax = -1;
+    ulist.clear();
     while (k0 + cnt < E && cnt < nb) {
       const int k = k0 + cnt;
-      const int64_t lo = std::min<int64_t>(emin, S.elist[S.eoff[k]]);
-      const int64_t hi = std::max<int64_t>(emax, S.elist[S.eoff[k + 1] - 1]);
-      if (cnt > 0 && hi - lo + 1 > cap) break;
-      emin = lo;
-      emax = hi;
+      int64_t add = 0;
+      for (int64_t t = S.eoff[k]; t < S.eoff[k + 1]; ++t) add += (stamp[S.elist[t]] != k0);
+      if (cnt > 0 && (int64_t)ulist.size() + add > cap) break;
+      for (int64_t t = S.eoff[k]; t < S.eoff[k + 1]; ++t)
+        if (stamp[S.elist[t]] != k0) {
+          stamp[S.elist[t]] = k0;
+          ulist.push_back(S.elist[t]);
+        }
       ++cnt;
     }
-    launch_elem_matrices(c, li, d_D, Ae, (int)emin, (int)(emax - emin + 1));
+    std::sort(ulist.begin(), ulist.end());
+    slots.resize(S.eoff[k0 + cnt] - S.eoff[k0]);
+    for (int64_t t = S.eoff[k0]; t < S.eoff[k0 + cnt]; ++t)
+      slots[t - S.eoff[k0]] = (int32_t)(std::lower_bound(ulist.begin(), ulist.end(), S.elist[t]) - ulist.begin());
+    CUDA_CHECK(cudaMemcpyAsync(d_ulist, ulist.data(), ulist.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d_slots, slots.data(), slots.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    launch_elem_matrices_list(c, li, d_D, Ae, d_ulist, (int)ulist.size());
     CUDA_CHECK(cudaMemsetAsync(B, 0, (size_t)cnt * npad * npad * 8, c->stream));
-    launch_assemble_blocks(c, li, d_idx, d_off, d_el, d_eoff, Ae, (int)emin, k0, cnt, npad, B);
+    launch_assemble_blocks(c, li, d_idx, d_off, d_el, d_eoff, Ae, 0, k0, cnt, npad, B, d_slots);
     launch_set_identity(c, X, cnt, npad);  // X <- I for every block
     CUSOLVER_CHECK(cusolverDnDpotrfBatched(sol, CUBLAS_FILL_MODE_LOWER, npad, dA, npad, dinfo, cnt));
     CUDA_CHECK(cudaMemcpyAsync(hinfo.data(), dinfo, cnt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));

@@ -170,7 +170,9 @@ void launch_to_float(sem_ctx* c, int64_t n, const double* a, float* b);
 int launch_geometry(sem_ctx* c, int level, const double* d_xfine, const double* d_gmat, int Nf, const double* d_w);
 void launch_elem_matrices(sem_ctx* c, int level, const double* d_D, double* Ae, int e0, int ne);
 void launch_assemble_blocks(sem_ctx* c, int level, const int32_t* d_idx, const int64_t* d_off, const int32_t* d_elist,
-                            const int64_t* d_eoff, const double* Ae, int ebase, int k0, int nb, int npad, double* B);
+                            const int64_t* d_eoff, const double* Ae, int ebase, int k0, int nb, int npad, double* B,
+                            const int32_t* eslot = nullptr);
+void launch_elem_matrices_list(sem_ctx* c, int level, const double* d_D, double* Ae, const int32_t* elist, int ne);
 void launch_pack_tiles(sem_ctx* c, int level, const double* Binv, int k0, int nb, int npad, const int64_t* d_off);
 void launch_assemble_coarse(sem_ctx* c, const double* Ae, const int32_t* d_cmap, double* A, int64_t nc);
 void launch_symmetrize(sem_ctx* c, double* A, int64_t n);

@@ -738,13 +738,15 @@ int launch_geometry(sem_ctx* c, int level, const double* X, const double* gm, in
 
 // Ae[e][i][j] = sum_q sum_cd D_c[q][i] G_cd[e][q] D_d[q][j]   (setup only)
 __global__ void k_elem_matrices(int e0, int ne, int N, int Q, const double* __restrict__ D,
-                                const double* __restrict__ G, double* __restrict__ Ae) {
+                                const double* __restrict__ G, double* __restrict__ Ae,
+                                const int32_t* __restrict__ elist) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t NN = (int64_t)N * N;
   if (idx >= (int64_t)ne * NN) return;
   const int64_t le = idx / NN;
   const int i = (int)((idx % NN) / N), j = (int)(idx % N);
-  const double* g = G + (e0 + le) * 6 * Q;
+  const int64_t e = elist ? (int64_t)elist[le] : e0 + le;
+  const double* g = G + e * 6 * Q;
   double s = 0.0;
   for (int q = 0; q < Q; ++q) {
     const double ri = D[(0 * Q + q) * N + i], si = D[(1 * Q + q) * N + i], ti = D[(2 * Q + q) * N + i];
@@ -760,7 +762,14 @@ __global__ void k_elem_matrices(int e0, int ne, int N, int Q, const double* __re
 void launch_elem_matrices(sem_ctx* c, int level, const double* D, double* Ae, int e0, int ne) {
   const DeviceLevel& L = c->L[level];
   const int64_t tot = (int64_t)ne * L.N * L.N;
-  k_elem_matrices<<<(int)((tot + 255) / 256), 256, 0, c->stream>>>(e0, ne, L.N, L.Q, D, L.G, Ae);
+  k_elem_matrices<<<(int)((tot + 255) / 256), 256, 0, c->stream>>>(e0, ne, L.N, L.Q, D, L.G, Ae, nullptr);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_elem_matrices_list(sem_ctx* c, int level, const double* D, double* Ae, const int32_t* elist, int ne) {
+  const DeviceLevel& L = c->L[level];
+  const int64_t tot = (int64_t)ne * L.N * L.N;
+  k_elem_matrices<<<(int)((tot + 255) / 256), 256, 0, c->stream>>>(0, ne, L.N, L.Q, D, L.G, Ae, elist);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -769,7 +778,7 @@ void launch_elem_matrices(sem_ctx* c, int level, const double* D, double* Ae, in
 __global__ void k_assemble_blocks(int N, const int32_t* __restrict__ conn, const int32_t* __restrict__ idx,
                                   const int64_t* __restrict__ off, const int32_t* __restrict__ elist,
                                   const int64_t* __restrict__ eoff, const double* __restrict__ Ae, int ebase,
-                                  int k0, int npad, double* __restrict__ B) {
+                                  int k0, int npad, double* __restrict__ B, const int32_t* __restrict__ eslot) {
   extern __shared__ int ism[];
   int* sidx = ism;              // [npad]
   int* pos = ism + npad;        // [N]
@@ -803,7 +812,7 @@ __global__ void k_assemble_blocks(int N, const int32_t* __restrict__ conn, const
     }
     __syncthreads();
     const int nl = nloc;
-    const double* A = Ae + (size_t)(e - ebase) * N * N;
+    const double* A = Ae + (size_t)(eslot ? eslot[t - eoff[k0]] : e - ebase) * N * N;
     for (int pr = threadIdx.x; pr < nl * nl; pr += blockDim.x) {
       const int i = loc[pr / nl], j = loc[pr % nl];
       Bk[(size_t)pos[i] * npad + pos[j]] += A[(size_t)i * N + j];
@@ -813,10 +822,11 @@ __global__ void k_assemble_blocks(int N, const int32_t* __restrict__ conn, const
 }
 
 void launch_assemble_blocks(sem_ctx* c, int level, const int32_t* idx, const int64_t* off, const int32_t* elist,
-                            const int64_t* eoff, const double* Ae, int ebase, int k0, int nb, int npad, double* B) {
+                            const int64_t* eoff, const double* Ae, int ebase, int k0, int nb, int npad, double* B,
+                            const int32_t* eslot) {
   const DeviceLevel& L = c->L[level];
   const int smem = (npad + 2 * L.N) * (int)sizeof(int);
-  k_assemble_blocks<<<nb, 256, smem, c->stream>>>(L.N, L.conn, idx, off, elist, eoff, Ae, ebase, k0, npad, B);
+  k_assemble_blocks<<<nb, 256, smem, c->stream>>>(L.N, L.conn, idx, off, elist, eoff, Ae, ebase, k0, npad, B, eslot);
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -24,3 +24,19 @@ def lib_node_xyz(mesh, conn: np.ndarray, rst: np.ndarray) -> np.ndarray:
     xyz = np.zeros((n, 3))
     xyz[conn.ravel()] = pts.reshape(-1, 3)
     return xyz
+
+
+def fine_map_xyz(mesh, level, p_fine: int) -> np.ndarray:
+    """Positions of a (coarse) level's oracle nodes on the FINEST-order nodal map
+    (the library's convention) instead of the exact workload map: the
+    order-p_fine interpolant of each element's nodes, evaluated at the level's
+    reference nodes (oracle basis; test-side helper)."""
+    from oracle import refelem as R
+    rst_c, _ = R.prism_nodes(level.p)
+    rst_f, _ = R.prism_nodes(p_fine)
+    X = mesh.node_xyz(rst_f)                               # [E][Nf][3]
+    V, _ = R.prism_basis(p_fine, rst_c)                    # [Nc][Nf]
+    pts = np.einsum("cf,efi->eci", V, X)
+    out = np.zeros((level.n, 3))
+    out[level.conn.ravel()] = pts.reshape(-1, 3)
+    return out

@@ -28,6 +28,7 @@ CASES = {
     "c3s_refined": lambda: (_c3_small(), -1),       # overlap ceil((P+1)/2) per level
     "c2_o0": lambda: (config2(p=4, nx=32, ny=2, nz=3), 0),
     "c5r": lambda: (_c5_replica(), 1),            # hull: FDM / exact-dense hybrid (reading O35)
+    "c2p6": lambda: (config2(p=6, nx=24, ny=2, nz=2), 1),   # n_v = 9: two n-tiles per box
 }
 
 

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 import paper_2009_00705_b200 as lib  # noqa: E402
 from oracle import pmg, sem  # noqa: E402
-from tests._mapping import lib_to_oracle  # noqa: E402
+from tests._mapping import fine_map_xyz, lib_to_oracle  # noqa: E402
 from workloads import config1, config2, config3, config4, random_vector  # noqa: E402
 
 if not torch.cuda.is_available():
@@ -44,7 +44,8 @@ class Case:
         self.levels = []
         for li, pl in enumerate(self.s.info["level_p"]):
             lev = sem.build_system(m, pl, p_geo=m.p)
-            perm = lib_to_oracle(self.s.node_xyz(li), lev.xyz)
+            ref_xyz = lev.xyz if li == 0 else fine_map_xyz(m, lev, m.p)
+            perm = lib_to_oracle(self.s.node_xyz(li), ref_xyz)
             self.levels.append((lev, perm))
         self.mg = pmg.PMG(m, schedule=self.s.info["level_p"], nu1=kw.get("nu1", 3), nu2=kw.get("nu2", 3),
                           overlap=kw.get("overlap", 1), literal=bool(kw.get("literal_smoother", 0)),
