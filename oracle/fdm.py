@@ -34,10 +34,12 @@ numpy.linalg.inv):
   free; W from the subdomain counts (eq 4.6).
 
 Reading O35 (hybrid): the separable form is only used where the box is a
-regular product -- every line of H_k has as many z-levels as element k's own
-column.  Next to a body (config 5) the patch mixes columns of different
-heights and the geometry is far from separable; those subdomains keep the
-paper's exact local inverse of eq 4.4 on their reading-O15 node set.
+regular product -- every footprint triangle with a node in H_k carries a
+column with as many layers as element k's own (so K_h, M_h are the true
+horizontal operators at every height of the box).  Next to a body (config 5)
+the patch mixes columns of different heights and the geometry is far from
+separable; those subdomains keep the paper's exact local inverse of eq 4.4 on
+their reading-O15 node set.
 """
 from __future__ import annotations
 
@@ -169,16 +171,20 @@ class Columns:
 
 
 def regular(cols: Columns, overlap: int):
-    """[E] bool: reading O35 -- every line of element k's patch has the length of
-    k's own column lines (Z_c + 1 z-levels)."""
-    linelen = (cols.node_at >= 0).sum(axis=1)
+    """[E] bool: reading O35 -- every column whose footprint triangle has a node
+    in element k's patch has as many layers as k's column."""
+    nh = cols.xy.shape[0]
+    touch = [[] for _ in range(nh)]                     # 2D node -> columns holding it
+    for c in range(cols.tri_h.shape[0]):
+        for h in cols.tri_h[c]:
+            touch[h].append(c)
     out = np.zeros(len(cols.col), dtype=bool)
     cache = {}
     for k in range(len(cols.col)):
         c = int(cols.col[k])
         if c not in cache:
             H = cols.patch(c, overlap)
-            cache[c] = bool(np.all(linelen[H] == cols.p * len(cols.col_elems[c]) + 1))
+            cache[c] = all(cols.nlayer[t] == cols.nlayer[c] for h in H for t in touch[h])
         out[k] = cache[c]
     return out
 

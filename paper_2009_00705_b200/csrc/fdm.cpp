@@ -341,12 +341,18 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
       }
     }
   }
-  // ---- 9. regular boxes (reading O35): every line of the patch as tall as the column's own lines
+  // ---- 9. regular boxes (reading O35): every column touching the patch as tall as the element's own
   {
     std::vector<uint8_t> creg(ncol, 1);
     for (int c = 0; c < ncol; ++c)
-      for (int64_t a = F.hoff[c]; a < F.hoff[c + 1]; ++a)
-        if (linelen[F.hnode[a]] != nlay[c] * p + 1) creg[c] = 0;
+      for (int64_t a = F.hoff[c]; a < F.hoff[c + 1] && creg[c]; ++a) {
+        const int32_t h = F.hnode[a];
+        for (int64_t s2 = coff[h]; s2 < coff[h + 1]; ++s2)
+          if (nlay[cinc[s2]] != nlay[c]) {
+            creg[c] = 0;
+            break;
+          }
+      }
     F.regular.resize(E);
     for (int e = 0; e < E; ++e) F.regular[e] = creg[F.col[e]];
   }

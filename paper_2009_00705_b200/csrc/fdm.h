@@ -34,7 +34,7 @@ struct FdmTopo {
   std::vector<int64_t> ioff;            // [E+1]
   std::vector<int32_t> idx;
   std::vector<double> W;                // [n] eq 4.6 from the FDM subdomains (0 on Dirichlet)
-  std::vector<uint8_t> regular;         // [E] reading O35: every patch line as tall as the element's column
+  std::vector<uint8_t> regular;         // [E] reading O35: every column touching the patch as tall as the element's
   // column view for the column-batched kernel: elements of every column in layer order,
   // and the node ids of the whole column patch [nh][Z_c+1] (-1 = absent or Dirichlet)
   std::vector<int64_t> cfirst;          // [ncol+1] into colel

@@ -203,7 +203,7 @@ def _points(Lx, Ly, foot, hf, rng, jitter):
 
 
 def config5(p: int = 6, hf: float = 1.0 / 12.0, Lx: float = 64.0, Ly: float = 32.0, seed: int = 5,
-            jitter: float = 0.15, n_comp: int = 32) -> HullMesh:
+            jitter: float = 0.15, n_comp: int = 32, hull: bool = True, amp: float = 0.03) -> HullMesh:
     """Unstructured basin with a body (BASELINE.json config 5).  Scaled replicas:
     a smaller domain around the same hull and/or a larger hf."""
     rng = np.random.default_rng(seed)
@@ -220,15 +220,19 @@ def config5(p: int = 6, hf: float = 1.0 / 12.0, Lx: float = 64.0, Ly: float = 32
     cen = a2.mean(axis=1)
     x0, y0, x1, y1 = foot
     tin = (cen[:, 0] > x0) & (cen[:, 0] < x1) & (cen[:, 1] > y0) & (cen[:, 1] < y1)
+    if not hull:  # study variant: the same graded mesh without the body
+        tin[:] = False
     eps = 1e-9
     vin = (P[:, 0] >= x0 - eps) & (P[:, 0] <= x1 + eps) & (P[:, 1] >= y0 - eps) & (P[:, 1] <= y1 + eps)
     vout = ~((P[:, 0] > x0 + eps) & (P[:, 0] < x1 - eps) & (P[:, 1] > y0 + eps) & (P[:, 1] < y1 - eps))
-    assert np.all(vin[tri[tin]]) and np.all(vout[tri[~tin]]), "triangulation does not conform to the hull"
+    assert np.all(vin[tri[tin]]) and (not hull or np.all(vout[tri[~tin]])), "triangulation does not conform"
+    if not hull:
+        vout[:] = True
     # wave group (deterministic)
     kp = 5.6
     k = np.linspace(0.5, 2.0, n_comp) * kp
     a = np.exp(-0.5 * ((k - kp) / (0.25 * kp)) ** 2)
-    a = 0.03 * a / a.sum()
+    a = amp * a / a.sum()
     meta = dict(a=a.tolist(), k=k.tolist(), theta=0.1745, focus=(xc, yc), foot=foot, hf=hf, seed=seed,
                 Lx=Lx, Ly=Ly)
     zh, z_edge = _bilge_profile()
