@@ -12,7 +12,8 @@ for r in rows[rows.index(hdr) + 1:]:
         continue
     name = re.sub(r"\(.*", "", r[iname]).replace("void ", "").replace("sem::", "")
     v = float(r[ival].replace(",", ""))
-    unit = 1e-3 if "nsecond" in r[hdr.index("Metric Unit")] else 1.0
+    u = r[hdr.index("Metric Unit")]
+    unit = 1e-3 if u in ("ns", "nsecond") else (1e3 if u in ("ms", "msecond") else 1.0)
     n, t = agg.get(name, (0, 0.0))
     agg[name] = (n + 1, t + v * unit)
 tot = sum(t for _, t in agg.values())
