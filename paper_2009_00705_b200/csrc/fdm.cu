@@ -131,20 +131,27 @@ static void batched_geneig(sem_ctx* c, cusolverDnHandle_t sol, cublasHandle_t bl
                                    np, np, &one, (const double* const*)pM, np, pK, np, nb));
       CUBLAS_OK(cublasDtrsmBatched(blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
                                    np, np, &one, (const double* const*)pM, np, pK, np, nb));
-      // C = Q L Q^T
+      // C = Q L Q^T: batched XsyevBatched, or one cusolverDnDsyevd per problem where the
+      // batched routine rejects the size (it does for some n)
       size_t wdev = 0, whost = 0;
-      CUSOLVER_OK(cusolverDnXsyevBatched_bufferSize(sol, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np,
-                                                    CUDA_R_64F, Kp, np, CUDA_R_64F, Wp, CUDA_R_64F, &wdev, &whost, nb));
-      void* bdev = s2.get<char>(wdev);
-      std::vector<char> bhost(std::max<size_t>(whost, 1));
-      CUSOLVER_OK(cusolverDnXsyevBatched(sol, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np, CUDA_R_64F,
-                                         Kp, np, CUDA_R_64F, Wp, CUDA_R_64F, bdev, wdev, bhost.data(), whost, info,
-                                         nb));
-      CUDA_CHECK(cudaMemcpyAsync(hinfo.data(), info, nb * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_CHECK(cudaStreamSynchronize(c->stream));
-      for (int i = 0; i < nb; ++i)
-        if (hinfo[i] != 0)
-          throw SemError(SEM_ESINGULAR, "FDM eigensolver failed (info " + std::to_string(hinfo[i]) + ")");
+      const cusolverStatus_t bs = cusolverDnXsyevBatched_bufferSize(
+          sol, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np, CUDA_R_64F, Kp, np, CUDA_R_64F, Wp,
+          CUDA_R_64F, &wdev, &whost, nb);
+      if (bs == CUSOLVER_STATUS_SUCCESS) {
+        void* bdev = s2.get<char>(wdev);
+        std::vector<char> bhost(std::max<size_t>(whost, 1));
+        CUSOLVER_OK(cusolverDnXsyevBatched(sol, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np,
+                                           CUDA_R_64F, Kp, np, CUDA_R_64F, Wp, CUDA_R_64F, bdev, wdev, bhost.data(),
+                                           whost, info, nb));
+      } else {
+        int lw = 0;
+        CUSOLVER_OK(cusolverDnDsyevd_bufferSize(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np, Kp, np, Wp,
+                                                &lw));
+        double* work = s2.get<double>((size_t)std::max(lw, 1));
+        for (int i = 0; i < nb; ++i)
+          CUSOLVER_OK(cusolverDnDsyevd(sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, np,
+                                       Kp + (size_t)i * np * np, np, Wp + (size_t)i * np, work, lw, info + i));
+      }
       // S = L^-T Q
       CUBLAS_OK(cublasDtrsmBatched(blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
                                    np, np, &one, (const double* const*)pM, np, pK, np, nb));
