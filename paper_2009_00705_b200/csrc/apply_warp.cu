@@ -18,9 +18,9 @@
 // re-laid out as A or B fragments of the next stage with two shuffles.
 //
 // Data movement: the element's geometric factors (6 Q doubles, contiguous) are
-// brought into the warp's shared-memory slot by one TMA bulk copy
-// (cp.async.bulk + mbarrier), double-buffered so the next element's copy flies
-// during the current element's stages; u is gathered into registers through
+// stored a-tile-major (k_g_tiles) and streamed through a 3-slot ring per warp,
+// one TMA bulk copy (cp.async.bulk + mbarrier) per a-tile issued two tiles
+// ahead (across element boundaries); u is gathered into registers through
 // the connectivity, y scattered with FP64 atomics.  Persistent CTAs, no CTA
 // barrier after the prologue.
 #include <cuda_runtime.h>
@@ -49,9 +49,15 @@ struct AW {
   static constexpr int LDM = 8 * MTM + 4;       // row stride of Bm (= 4 mod 8: conflict-free both ways)
   static constexpr int ROWSA = 8 * MTA;
   static constexpr int BM = 3 * ROWSA * LDM;    // doubles of Bm [3][ROWSA][LDM] (Br, Bs, B0)
-  static constexpr int W = (P <= 3) ? 16 : ((P <= 5) ? 8 : 4);   // warps per CTA
+  static constexpr int W = (P <= 5) ? 16 : 8;   // warps per CTA
   static constexpr int GSZ = 6 * Q;             // doubles of one element's G
-  static constexpr int SMEM = (BM + 2 * W * GSZ) * 8 + 2 * W * 8;
+  static constexpr bool WHOLE = (P <= 3);       // small elements: one TMA copy per element, else per a-tile
+  static constexpr int R = WHOLE ? 2 : 3;       // slots per warp (TMA ring)
+  static constexpr int TS = WHOLE ? 6 * Q : 6 * QV * 8;   // doubles of one slot
+  static constexpr int TPE = WHOLE ? 1 : MTA;   // TMA copies per element
+  static constexpr int NALAST = QT - 8 * (MTA - 1);
+  static constexpr int QE = (QV + 1) / 2;       // even vertical points first in a tile (bank spread)
+  static constexpr int SMEM = (BM + W * R * TS) * 8 + W * R * 8;
   static_assert(SMEM <= 227 * 1024, "apply_warp shared memory");
 };
 
@@ -115,14 +121,14 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
   using D = AW<P>;
   extern __shared__ __align__(128) double sm[];
   double* Bm = sm;                          // [3][ROWSA][LDM]
-  double* Gs = sm + D::BM;                  // [W][2][6 Q]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(Gs + 2 * D::W * D::GSZ);  // [W][2]
+  double* Gs = sm + D::BM;                  // [W][R][TS]  a-tile ring of every warp
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(Gs + D::W * D::R * D::TS);  // [W][R]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r4 = lane >> 2, c4 = lane & 3;
   for (int i = tid; i < D::BM; i += 32 * D::W) Bm[i] = __ldg(mats + i);
   if (lane == 0) {
-    for (int b = 0; b < 2; ++b)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(aw_smem(mbar + 2 * warp + b)));
+    for (int b = 0; b < D::R; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(aw_smem(mbar + D::R * warp + b)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -152,20 +158,23 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
   const double sgn = (flags & AP_NEGATE) ? -1.0 : 1.0;
   const int stride = gridDim.x * D::W;
   int e = blockIdx.x * D::W + warp;
-  double* gslot = Gs + (2 * warp) * D::GSZ;   // two slots of GSZ doubles
-  uint32_t phase = 0u;                          // bit b: parity of slot b's next completion
-  auto issue_G = [&](int el, int b) {
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
-      const uint32_t bytes = (uint32_t)D::GSZ * 8u;
-      const uint32_t mb = aw_smem(mbar + 2 * warp + b);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              aw_smem(gslot + b * D::GSZ)),
-          "l"(G + (size_t)el * D::GSZ), "r"(bytes), "r"(mb)
-          : "memory");
-    }
+  const int e0 = e;
+  double* ring = Gs + warp * D::R * D::TS;
+  // copy t of this warp's stream: element e0 + (t / TPE) stride, a-tile ma = t % TPE (or the whole
+  // element), slot t % R
+  auto issue_tile = [&](int t) {
+    const int el = e0 + (t / D::TPE) * stride, ma = t % D::TPE;
+    if (el >= E || lane != 0) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+    const uint32_t bytes =
+        D::WHOLE ? (uint32_t)D::GSZ * 8u : (uint32_t)(6 * D::QV * (ma < D::MTA - 1 ? 8 : D::NALAST)) * 8u;
+    const uint32_t mb = aw_smem(mbar + D::R * warp + t % D::R);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            aw_smem(ring + (t % D::R) * D::TS)),
+        "l"(G + (size_t)el * D::GSZ + (size_t)ma * D::TS), "r"(bytes), "r"(mb)
+        : "memory");
   };
   // connectivity of the A-fragment positions (m = 8 mm + r4, l = 4 kl + c4) and gather of u
   auto load_conn_a = [&](int el, int (&cA)[D::MTM][D::KL]) {
@@ -187,14 +196,14 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
         ua[mm][kl] = (g >= 0 || (g != INT_MIN && (flags & AP_GATHER_ALL))) ? __ldg(u + (g >= 0 ? g : ~g)) : 0.0;
       }
   };
-  int buf = 0;
   int cA[D::MTM][D::KL];
   double ua[D::MTM][D::KL];
   if (e < E) {
-    issue_G(e, 0);
+    for (int t = 0; t < D::R; ++t) issue_tile(t);
     load_conn_a(e, cA);
     gather_u(cA, ua);
   }
+  int tk = 0;  // first copy index of the current element
   while (e < E) {
     const int en = e + stride;
     const int32_t* ce = conn + (size_t)e * D::N;
@@ -210,8 +219,6 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
           cY[mm][nl][i] = (m < D::NT && l < D::N1) ? __ldg(ce + m + D::NT * l) : INT_MIN;
         }
     if (en < E) load_conn_a(en, cA);   // next element's gather positions (in flight during stage A)
-    __syncwarp();
-    if (en < E) issue_G(en, buf ^ 1);  // the other slot was released by the previous element
     // ---- stage A: Ut, Udt [m][q]
     double Ut[D::MTM][D::NQ][2], Udt[D::MTM][D::NQ][2];
 #pragma unroll
@@ -237,19 +244,6 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
         bU[km][nq] = aw_c_to_b(Ut[km >> 1][nq][0], Ut[km >> 1][nq][1], km, lane);
         bD[km][nq] = aw_c_to_b(Udt[km >> 1][nq][0], Udt[km >> 1][nq][1], km, lane);
       }
-    // ---- wait for this element's geometric factors
-    {
-      const uint32_t mb = aw_smem(mbar + 2 * warp + buf);
-      uint32_t done = 0;
-      while (!done)
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(mb), "r"((phase >> buf) & 1u)
-            : "memory");
-      phase ^= 1u << buf;
-    }
-    const double* Ge = gslot + buf * D::GSZ;
     double Vt[D::MTM][D::NQ][2], Vdt[D::MTM][D::NQ][2];
 #pragma unroll
     for (int mm = 0; mm < D::MTM; ++mm)
@@ -257,6 +251,20 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
       for (int nq = 0; nq < D::NQ; ++nq) Vt[mm][nq][0] = Vt[mm][nq][1] = Vdt[mm][nq][0] = Vdt[mm][nq][1] = 0.0;
 #pragma unroll 1
     for (int ma = 0; ma < D::MTA; ++ma) {
+      const int t = D::WHOLE ? tk : tk + ma;
+      if (!D::WHOLE || ma == 0) {  // wait for copy t of G
+        const uint32_t mb = aw_smem(mbar + D::R * warp + t % D::R);
+        const uint32_t par = (uint32_t)(t / D::R) & 1u;
+        uint32_t done = 0;
+        while (!done)
+          asm volatile(
+              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+              : "=r"(done)
+              : "r"(mb), "r"(par)
+              : "memory");
+      }
+      const double* Gt = ring + (t % D::R) * D::TS + (D::WHOLE ? ma * 48 * D::QV : 0);
+      const int na = (ma < D::MTA - 1) ? 8 : D::NALAST;
       // ---- stage B for a-tile ma
       double g[3][D::NQ][2];
 #pragma unroll
@@ -282,9 +290,11 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
           const int a = ma * 8 + r4, q = nq * 8 + 2 * c4 + i;
           double w0 = 0.0, w1 = 0.0, w2 = 0.0;
           if (a < D::QT && q < D::QV) {
-            const double* gp = Ge + a + D::QT * q;
-            const double gxx = gp[0], gxy = gp[D::Q], gxz = gp[2 * D::Q], gyy = gp[3 * D::Q], gyz = gp[4 * D::Q],
-                         gzz = gp[5 * D::Q];
+            const int qp = (q & 1) ? D::QE + (q >> 1) : (q >> 1);   // tile row of q
+            const double* gp = Gt + qp * na + r4;
+            const int cs = D::QV * na;                               // component stride in the tile
+            const double gxx = gp[0], gxy = gp[cs], gxz = gp[2 * cs], gyy = gp[3 * cs], gyz = gp[4 * cs],
+                         gzz = gp[5 * cs];
             const double x0 = g[0][nq][i], x1 = g[1][nq][i], x2 = g[2][nq][i];
             w0 = gxx * x0 + gxy * x1 + gxz * x2;
             w1 = gxy * x0 + gyy * x1 + gyz * x2;
@@ -314,8 +324,11 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
           }
         }
       }
+      if (!D::WHOLE || ma == D::MTA - 1) {
+        __syncwarp();  // every lane is done with this slot before it is refilled
+        issue_tile(t + D::R);
+      }
     }
-    __syncwarp();  // every lane is done with this G slot before it is refilled
     // ---- stage A^T: y[m][l] = Vt Bt + Vdt Dt (k = q), scatter
 #pragma unroll
     for (int mm = 0; mm < D::MTM; ++mm) {
@@ -347,9 +360,36 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
 #pragma unroll
         for (int kl = 0; kl < D::KL; ++kl) ua[mm][kl] = un[mm][kl];
     }
-    buf ^= 1;
+    tk += D::TPE;
     e = en;
   }
+}
+
+// G [E][6][Q] (point a + QT q) -> a-tile-major copy for k_apply_warp: per element, tile ma
+// (8 points a, the last one QT - 8(MTA-1)) at offset 48 QV ma, inside [comp][qpos][a_local]
+// with the even vertical points first (qpos spreads a fragment's 4 q-rows over both bank halves)
+__global__ void k_g_tiles(int64_t E, int QT, int QV, const double* __restrict__ G, double* __restrict__ Gw) {
+  const int Q = QT * QV, MTA = (QT + 7) / 8, QE = (QV + 1) / 2;
+  const int64_t tot = E * 6 * Q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / (6 * Q);
+    const int r = (int)(i % (6 * Q)), c = r / Q, pt = r % Q, a = pt % QT, q = pt / QT;
+    const int ma = a / 8, na = (ma < MTA - 1) ? 8 : QT - 8 * (MTA - 1);
+    const int qp = (q & 1) ? QE + (q >> 1) : (q >> 1);
+    Gw[e * 6 * Q + (int64_t)48 * QV * ma + (c * QV + qp) * na + (a - 8 * ma)] = G[i];
+  }
+}
+
+void build_g_tiles(sem_ctx* c, int level) {
+  DeviceLevel& L = c->L[level];
+  const int QT = L.ref.qt, QV = L.ref.qv;
+  L.Gw = nullptr;
+  if (L.p > 6 || c->opts.apply_kernel != 0) return;
+  CUDA_CHECK(cudaMalloc(&L.Gw, (size_t)c->E * 6 * L.Q * sizeof(double)));
+  c->allocs.push_back(L.Gw);
+  c->device_bytes += (int64_t)c->E * 6 * L.Q * 8;
+  k_g_tiles<<<148 * 16, 256, 0, c->stream>>>(c->E, QT, QV, L.G, L.Gw);
+  CUDA_CHECK(cudaGetLastError());
 }
 
 template <int P>
@@ -367,13 +407,13 @@ static void apply_warp_P(sem_ctx* c, const DeviceLevel& L, const double* u, doub
   if (c->E_own == 0) return;
   const int need = (c->E_own + D::W - 1) / D::W;
   const int grid = need < grid_max ? need : grid_max;
-  k_apply_warp<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(c->E_own, L.conn, L.G, L.wmats, u, y, flags);
+  k_apply_warp<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(c->E_own, L.conn, L.Gw, L.wmats, u, y, flags);
   CUDA_CHECK(cudaGetLastError());
 }
 
 bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags) {
   const DeviceLevel& L = c->L[level];
-  if (!L.wmats) return false;
+  if (!L.wmats || !L.Gw) return false;
   switch (L.p) {
     case 1: apply_warp_P<1>(c, L, u, y, flags); break;
     case 2: apply_warp_P<2>(c, L, u, y, flags); break;

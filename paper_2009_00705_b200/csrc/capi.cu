@@ -412,6 +412,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
       double* d_gm = s2.put(geometry_matrix(p, L.p));
       double* d_w = s2.put(R.wq);
       if (launch_geometry(c, li, d_X, d_gm, Nf, d_w)) throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
+      build_g_tiles(c, li);
     }
     // node coordinates of this level (fine map evaluated at the level's nodes)
     L.xyz.assign((size_t)L.n * 3, 0.0);
