@@ -346,6 +346,7 @@ def main():
                        else (f"{args.emulate_ranks} emulated ranks on 1 GPU (validation, not a scaling number)"
                              if args.emulate_ranks > 1 else "single GPU"), "setup_s": setup_s},
             "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "q_mean": rep["q_mean"],
+            "work_units": ms_step * 1e3 / us_a,    # solve time / one finest operator apply (O25)
             "roofline": roof, "apply": apply, "variants": variants, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,

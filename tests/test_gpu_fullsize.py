@@ -173,3 +173,25 @@ def test_full_config5_apply_and_properties():
     # the P=1 problem (243,654 free DOF) is solved iteratively to 1e-10 (reading O9): symmetric to that level
     assert abs((x @ vz).item() - (vx @ z).item()) <= 1e-9 * x.norm().item() * vz.norm().item()
     s.close()
+
+
+@pytest.mark.parametrize("p", [8])
+def test_full_config4_apply_rows(p):
+    """Config 4 at full size (~11.5 M DOF, p = 8: the CTA-batched DMMA kernel) with
+    the FDM smoother of the sweep: sampled interior rows and A 1 = 0."""
+    from workloads import config4
+    F = Full(config4(p), local_solve=1)
+    s = F.s
+    n = s.n_dof(0)
+    u = random_vector(n, seed=31)
+    y = s.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    rng = np.random.default_rng(2)
+    el = np.sort(rng.choice(F.m.n_elem, 60, replace=False))
+    ids = F.elem_ids(el)
+    Ae = F.elem_mats(el)
+    inner = _interior_locals(F.p)
+    yo = np.einsum("eij,ej->ei", Ae, u[ids])[:, inner].ravel()
+    assert np.linalg.norm(y[ids[:, inner]].ravel() - yo) <= 1e-12 * np.linalg.norm(yo)
+    one = torch.ones(n, dtype=torch.float64, device="cuda")
+    assert s.apply(one).abs().max().item() <= 1e-11 * np.abs(y).max()
+    s.close()
