@@ -460,6 +460,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
     Scratch s2;
     double* d_D = s2.put(c->L[li].ref.Dfull);
     const int lid = lids[li];
+    if (o.apply_kernel == 0) build_p1_matrices(c, li, d_D);
     if (li + 1 < nl) {
       double t0 = now_ms();
       if (part) {

@@ -45,6 +45,7 @@ struct DeviceLevel {
   double* frag = nullptr;       // DMMA fragment-ordered reference operands (apply_dmma.cu)
   double* wmats = nullptr;      // reference operands of the warp-per-element apply (apply_warp.cu), p <= 6
   double* Gw = nullptr;         // a-tile-major copy of G for k_apply_warp (apply_warp.cu)
+  double* Ae1 = nullptr;        // P = 1 levels: packed element matrices [21][E] (k_apply_p1)
   // Schwarz (not on the coarsest level)
   int32_t* sidx = nullptr;      // padded to 16 per subdomain, -1 = padding
   int64_t* sidx_off = nullptr;  // [E+1] (padded offsets)
@@ -154,6 +155,7 @@ std::vector<double> dmma_fragments(const LevelRef& R);
 std::vector<double> warp_apply_mats(const LevelRef& R);
 bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags);
 void build_g_tiles(sem_ctx* c, int level);
+void build_p1_matrices(sem_ctx* c, int level, const double* d_D);
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);
 void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose);
 void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose);
