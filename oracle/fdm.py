@@ -34,9 +34,10 @@ numpy.linalg.inv):
   free; W from the subdomain counts (eq 4.6).
 
 Reading O35 (hybrid): the separable form is only used where the box is a
-regular product -- every footprint triangle with a node in H_k carries a
-column with as many layers as element k's own (so K_h, M_h are the true
-horizontal operators at every height of the box).  Next to a body (config 5)
+regular product -- every footprint triangle with a node in H_k widened by one
+element ring carries a column with as many layers as element k's own (so K_h,
+M_h are the true horizontal operators at every height of the box, and the
+sloped bilge rows next to a body keep the exact inverse).  Next to a body (config 5)
 the patch mixes columns of different heights and the geometry is far from
 separable; those subdomains keep the paper's exact local inverse of eq 4.4 on
 their reading-O15 node set.
@@ -172,7 +173,8 @@ class Columns:
 
 def regular(cols: Columns, overlap: int):
     """[E] bool: reading O35 -- every column whose footprint triangle has a node
-    in element k's patch has as many layers as k's column."""
+    within lattice distance overlap + p of element k's triangle (its patch widened
+    by one element ring) has as many layers as k's column."""
     nh = cols.xy.shape[0]
     touch = [[] for _ in range(nh)]                     # 2D node -> columns holding it
     for c in range(cols.tri_h.shape[0]):
@@ -183,7 +185,7 @@ def regular(cols: Columns, overlap: int):
     for k in range(len(cols.col)):
         c = int(cols.col[k])
         if c not in cache:
-            H = cols.patch(c, overlap)
+            H = cols.patch(c, overlap + cols.p)
             cache[c] = all(cols.nlayer[t] == cols.nlayer[c] for h in H for t in touch[h])
         out[k] = cache[c]
     return out

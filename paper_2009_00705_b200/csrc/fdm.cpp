@@ -341,18 +341,35 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
       }
     }
   }
-  // ---- 9. regular boxes (reading O35): every column touching the patch as tall as the element's own
+  // ---- 9. regular boxes (reading O35): every column touching the patch widened by one element
+  //         ring (lattice radius overlap + p) as tall as the element's own column
   {
     std::vector<uint8_t> creg(ncol, 1);
-    for (int c = 0; c < ncol; ++c)
-      for (int64_t a = F.hoff[c]; a < F.hoff[c + 1] && creg[c]; ++a) {
-        const int32_t h = F.hnode[a];
-        for (int64_t s2 = coff[h]; s2 < coff[h + 1]; ++s2)
-          if (nlay[cinc[s2]] != nlay[c]) {
-            creg[c] = 0;
-            break;
-          }
+    const int radius = overlap + p;
+#pragma omp parallel
+    {
+      std::vector<int32_t> stamp(nh2, -1), cur, nxt, ball;
+#pragma omp for schedule(dynamic, 64)
+      for (int c = 0; c < ncol; ++c) {
+        cur.clear();
+        ball.clear();
+        const int32_t* t = &eh[(size_t)colbot[c] * Nt];
+        for (int mm = 0; mm < Nt; ++mm)
+          if (stamp[t[mm]] != c) { stamp[t[mm]] = c; cur.push_back(t[mm]); ball.push_back(t[mm]); }
+        for (int d = 0; d < radius; ++d) {
+          nxt.clear();
+          for (int32_t h : cur)
+            for (int64_t s2 = aoff[h]; s2 < aoff[h + 1]; ++s2)
+              if (stamp[adj[s2]] != c) { stamp[adj[s2]] = c; nxt.push_back(adj[s2]); ball.push_back(adj[s2]); }
+          cur.swap(nxt);
+        }
+        for (int32_t h : ball) {
+          for (int64_t s2 = coff[h]; s2 < coff[h + 1]; ++s2)
+            if (nlay[cinc[s2]] != nlay[c]) { creg[c] = 0; break; }
+          if (!creg[c]) break;
+        }
       }
+    }
     F.regular.resize(E);
     for (int e = 0; e < E; ++e) F.regular[e] = creg[F.col[e]];
   }
