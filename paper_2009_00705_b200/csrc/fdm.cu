@@ -228,6 +228,7 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
     L.f_mt = (F.nh_max + 7) / 8;
     std::vector<int4> units;
     L.f_warp = (L.f_mt <= 8 && nvt <= 2) ? 1 : 0;
+    L.f_nph = 2 + (2 * F.overlap) / F.p;  // boxes j, j + k of a column overlap iff k p <= p + 2 o
     const int per = L.f_warp ? 8 : FDM_NT / nvt;
     for (int q = 0; q < ncol; ++q)
       for (int64_t j = F.cfirst[q]; j < F.cfirst[q + 1]; j += per)
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 2) k_fdm_warp(const int4* 
                                                   const double* __restrict__ lh, const double* __restrict__ Svp,
                                                   const double* __restrict__ lvp, const double* __restrict__ W,
                                                   const double* __restrict__ r, double* __restrict__ u, int transpose,
-                                                  int ldr, const uint8_t* __restrict__ skip) {
+                                                  int ldr, const uint8_t* __restrict__ skip, int nph) {
   constexpr int ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
   extern __shared__ __align__(16) double sm[];
   double* Ss = sm;                  // [ROWS][LDS]  S_h (row i node, col a mode), zero padded
@@ -613,6 +614,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 2) k_fdm_warp(const int4* 
   __syncthreads();
   for (int t = tid; t < ROWS * ldr; t += 256) Rc[t] = 0.0;  // Rc becomes the accumulator
   __syncthreads();
+  double yk[MT][NVT][2];
   if (active) {
     const int e = eid[j];
     // T = S_h^T B1
@@ -660,7 +662,13 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 2) k_fdm_warp(const int4* 
 #pragma unroll
       for (int n = 0; n < NVT; ++n)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) v[n][i] /= (la + lvv[n][i]);
+        for (int i = 0; i < 2; ++i) {  // v /= (l_h + l_v): float reciprocal + two Newton steps (FP64 accurate)
+          const double d = la + lvv[n][i];
+          double rc = (double)__frcp_rn((float)d);
+          rc = fma(rc, fma(-d, rc, 1.0), rc);
+          rc = fma(rc, fma(-d, rc, 1.0), rc);
+          v[n][i] *= rc;
+        }
 #pragma unroll
       for (int n = 0; n < NVT; ++n) T[mt][n][0] = T[mt][n][1] = 0.0;
 #pragma unroll
@@ -685,29 +693,38 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 2) k_fdm_warp(const int4* 
         }
       }
     }
-    // Y = S_h T, accumulated into the column block
+    // Y = S_h T (kept in registers, added to the column block by phases below)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
-      double y[NVT][2];
 #pragma unroll
-      for (int n = 0; n < NVT; ++n) y[n][0] = y[n][1] = 0.0;
+      for (int n = 0; n < NVT; ++n) yk[mt][n][0] = yk[mt][n][1] = 0.0;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
         const double af = Ss[(mt * 8 + (lane >> 2)) * LDS + kt * 4 + (lane & 3)];
 #pragma unroll
-        for (int n = 0; n < NVT; ++n) fdm_dmma(y[n][0], y[n][1], af, b2[kt][n]);
-      }
-      const int i = mt * 8 + (lane >> 2);
-      if (i < nh) {
-#pragma unroll
-        for (int n = 0; n < NVT; ++n)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int col = n * 8 + 2 * (lane & 3) + q;
-            if (col < nvj) atomicAdd(Rc + i * ldr + zb + col, y[n][q]);
-          }
+        for (int n = 0; n < NVT; ++n) fdm_dmma(yk[mt][n][0], yk[mt][n][1], af, b2[kt][n]);
       }
     }
+  }
+  // boxes j and j + k overlap only for k < nph: in phase ph the warps j = ph mod nph add
+  // their (mutually disjoint) boxes with plain shared-memory adds
+  for (int ph = 0; ph < nph; ++ph) {
+    if (active && j % nph == ph) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int i = mt * 8 + (lane >> 2);
+        if (i < nh) {
+#pragma unroll
+          for (int n = 0; n < NVT; ++n)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int col = n * 8 + 2 * (lane & 3) + q;
+              if (col < nvj) Rc[i * ldr + zb + col] += yk[mt][n][q];
+            }
+        }
+      }
+    }
+    __syncthreads();
   }
   __syncthreads();
   for (int base = 0; base < nh * ldr; base += 256 * 8) {  // scatter every column node of the unit once
@@ -742,7 +759,7 @@ static void fdm_warp_launch(sem_ctx* c, const DeviceLevel& L, const double* r, d
   k_fdm_warp<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
                                                              L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
                                                              L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_ldr,
-                                                             L.f_skip);
+                                                             L.f_skip, L.f_nph);
   CUDA_CHECK(cudaGetLastError());
 }
 
