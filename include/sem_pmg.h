@@ -109,8 +109,10 @@ typedef struct {
                                  (eq 4.4); 1 fast diagonalisation of the separable operator
                                  K_h (x) M_v + M_h (x) K_v on the product subdomain (reading O33,
                                  Lottes & Fischer [FL05]): exact on straight prisms with flat
-                                 layers, needs a layered mesh (SEM_EUNSUPPORTED otherwise) and
-                                 nranks = 1.  Same subdomains (O15) and weights (eq 4.6).            */
+                                 layers, needs a layered mesh (SEM_EUNSUPPORTED otherwise).
+                                 Subdomains next to columns of a different height keep the exact
+                                 inverse (reading O35).  Same subdomains (O15) and weights (eq 4.6);
+                                 partitioned solves (nranks > 1) supported.                          */
   int mixed_precision;        /* 0 (default): everything stored and computed in FP64.  1: the exact
                                  dense Schwarz inverses and the dense coarse inverse are STORED in FP32
                                  (rounded once at setup) and applied with FP64 arithmetic -- the

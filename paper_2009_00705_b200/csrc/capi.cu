@@ -263,8 +263,6 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
 void check_opts(const sem_opts& o) {
   if (o.local_solve < 0 || o.local_solve > 1) throw SemError(SEM_EINVAL, "bad options: local_solve");
   if (o.mixed_precision < 0 || o.mixed_precision > 1) throw SemError(SEM_EINVAL, "bad options: mixed_precision");
-  if (o.local_solve == 1 && o.nranks > 1)
-    throw SemError(SEM_EUNSUPPORTED, "FDM local solves are single-domain only (nranks = 1)");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
       o.apply_kernel > 2 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
       o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
@@ -463,7 +461,13 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
     if (o.apply_kernel == 0) build_p1_matrices(c, li, d_D);
     if (li + 1 < nl) {
       double t0 = now_ms();
-      if (part) {
+      if (part && o.local_solve == 1) {  // partitioned FDM / exact-dense hybrid (O33, O35)
+        const FdmTopo& F = part->F[lid];
+        bool any = false;
+        for (uint8_t r : F.regular) any |= !r;
+        if (any) setup_schwarz(c, li, schwarz_subset(part->L[lid].S, F.regular), blas, sol, d_D, o.verbose);
+        setup_fdm(c, li, F, sol, blas, o.verbose);
+      } else if (part) {
         setup_schwarz(c, li, part->L[lid].S, blas, sol, d_D, o.verbose);
       } else if (gsch) {
         setup_schwarz(c, li, (*gsch)[lid], blas, sol, d_D, o.verbose);

@@ -500,8 +500,32 @@ void setup_distributed(sem_ctx* c, GlobalModel& gm) {
   } else {
     ranks.push_back(o.rank);
   }
+  // FDM local solves (reading O33/O35): global topologies and hybrid weights, restricted per rank
+  std::vector<FdmTopo> Fg;
+  std::vector<std::vector<double>> Wh;
+  if (o.local_solve == 1) {
+    for (int l = 0; l + 1 < nl; ++l) {
+      const int ov = o.overlap >= 0 ? o.overlap : (gm.sched[l] + 2) / 2;
+      Fg.push_back(fdm_topology(gm.hm, gm.topo[l], gm.X, gm.P, ov));
+      const FdmTopo& F = Fg.back();
+      std::vector<double> cnt(gm.topo[l].n, 0.0);
+      for (int e = 0; e < E; ++e)
+        if (F.regular[e]) {
+          for (int64_t t = F.ioff[e]; t < F.ioff[e + 1]; ++t)
+            if (F.idx[t] >= 0) cnt[F.idx[t]] += 1.0;
+        } else {
+          for (int64_t t = sch[l].off[e]; t < sch[l].off[e + 1]; ++t) cnt[sch[l].idx[t]] += 1.0;
+        }
+      std::vector<double> W(gm.topo[l].n, 0.0);
+      for (int64_t i = 0; i < gm.topo[l].n; ++i) W[i] = gm.topo[l].dir[i] ? 0.0 : 1.0 / cnt[i];
+      Wh.push_back(std::move(W));
+    }
+  }
   for (int r : ranks) {
     LocalPart P = extract_part(gm.topo, sch, epart, r, o.nranks);
+    if (o.local_solve == 1)
+      for (int l = 0; l + 1 < nl; ++l)
+        P.F.push_back(fdm_local(Fg[l], P.elems, P.E_own, P.L[l].gid, gm.topo[l].n, Wh[l]));
     sem_ctx* pc = new sem_ctx();
     D->parts.push_back(pc);
     D->part_rank.push_back(r);

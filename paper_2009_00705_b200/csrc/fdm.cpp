@@ -386,4 +386,79 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
   return F;
 }
 
+FdmTopo fdm_local(const FdmTopo& G, const std::vector<int32_t>& elems, int E_own, const std::vector<int32_t>& gid,
+                  int64_t n_global, const std::vector<double>& Wg) {
+  FdmTopo F;
+  F.p = G.p;
+  F.overlap = G.overlap;
+  std::vector<int32_t> gloc(n_global, -1);
+  for (size_t i = 0; i < gid.size(); ++i) gloc[gid[i]] = (int32_t)i;
+  auto lid = [&](int32_t g) {
+    if (g < 0) return -1;
+    const int32_t l = gloc[g];
+    if (l < 0) throw SemError(SEM_EINVAL, "FDM partition: a box node is not held by the rank");
+    return (int)l;
+  };
+  const int Eg = (int)G.col.size();
+  std::vector<int32_t> eloc(Eg, -1);
+  for (int k = 0; k < E_own; ++k) eloc[elems[k]] = k;
+  // local columns: the owned elements' columns in ascending global column id
+  std::vector<int32_t> gcols;
+  for (int k = 0; k < E_own; ++k) gcols.push_back(G.col[elems[k]]);
+  std::sort(gcols.begin(), gcols.end());
+  gcols.erase(std::unique(gcols.begin(), gcols.end()), gcols.end());
+  const int ncol = (int)gcols.size();
+  F.ncol = ncol;
+  std::vector<int32_t> cloc(G.ncol, -1);
+  for (int q = 0; q < ncol; ++q) cloc[gcols[q]] = q;
+  F.hoff.assign(ncol + 1, 0);
+  F.moff.assign(ncol + 1, 0);
+  F.cfirst.assign(ncol + 1, 0);
+  F.cioff.assign(ncol + 1, 0);
+  F.nzc.resize(ncol);
+  for (int q = 0; q < ncol; ++q) {
+    const int gc = gcols[q];
+    const int64_t nh = G.hoff[gc + 1] - G.hoff[gc];
+    F.hoff[q + 1] = F.hoff[q] + nh;
+    F.moff[q + 1] = F.moff[q] + nh * nh;
+    F.nh_max = std::max<int>(F.nh_max, (int)nh);
+    F.hnode.insert(F.hnode.end(), G.hnode.begin() + G.hoff[gc], G.hnode.begin() + G.hoff[gc + 1]);
+    F.Kh.insert(F.Kh.end(), G.Kh.begin() + G.moff[gc], G.Kh.begin() + G.moff[gc + 1]);
+    F.Mh.insert(F.Mh.end(), G.Mh.begin() + G.moff[gc], G.Mh.begin() + G.moff[gc + 1]);
+    for (int64_t j = G.cfirst[gc]; j < G.cfirst[gc + 1]; ++j) {
+      const int k = eloc[G.colel[j]];
+      if (k < 0) throw SemError(SEM_EINVAL, "FDM partition: a column split between ranks");
+      F.colel.push_back(k);
+    }
+    F.cfirst[q + 1] = (int64_t)F.colel.size();
+    F.nzc[q] = G.nzc[gc];
+    for (int64_t t = G.cioff[gc]; t < G.cioff[gc + 1]; ++t) F.cidx.push_back(lid(G.cidx[t]));
+    F.cioff[q + 1] = (int64_t)F.cidx.size();
+  }
+  F.col.resize(E_own);
+  F.layer.resize(E_own);
+  F.z0.resize(E_own);
+  F.nv.resize(E_own);
+  F.regular.resize(E_own);
+  F.voff.assign(E_own + 1, 0);
+  F.ioff.assign(E_own + 1, 0);
+  for (int k = 0; k < E_own; ++k) {
+    const int e = elems[k];
+    F.col[k] = cloc[G.col[e]];
+    F.layer[k] = G.layer[e];
+    F.z0[k] = G.z0[e];
+    F.nv[k] = G.nv[e];
+    F.regular[k] = G.regular[e];
+    F.nv_max = std::max(F.nv_max, F.nv[k]);
+    F.Kv.insert(F.Kv.end(), G.Kv.begin() + G.voff[e], G.Kv.begin() + G.voff[e + 1]);
+    F.Mv.insert(F.Mv.end(), G.Mv.begin() + G.voff[e], G.Mv.begin() + G.voff[e + 1]);
+    F.voff[k + 1] = (int64_t)F.Kv.size();
+    for (int64_t t = G.ioff[e]; t < G.ioff[e + 1]; ++t) F.idx.push_back(lid(G.idx[t]));
+    F.ioff[k + 1] = (int64_t)F.idx.size();
+  }
+  F.W.resize(gid.size());
+  for (size_t i = 0; i < gid.size(); ++i) F.W[i] = Wg[gid[i]];
+  return F;
+}
+
 }  // namespace sem

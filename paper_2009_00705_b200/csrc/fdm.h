@@ -44,6 +44,13 @@ struct FdmTopo {
   std::vector<int32_t> cidx;
 };
 
+// The FDM topology of one rank's partition: the owned elements elems[0, E_own)
+// (whole columns), node ids mapped to the rank's local numbering (gid: local ->
+// global), W taken from the global hybrid weights Wg.  Throws if a box node is
+// not held by the rank.
+FdmTopo fdm_local(const FdmTopo& G, const std::vector<int32_t>& elems, int E_own, const std::vector<int32_t>& gid,
+                  int64_t n_global, const std::vector<double>& Wg);
+
 // X: [E][N(pg)][3] nodal map of order pg (the finest order; x, y are taken as
 // affine per triangle from its corner nodes, z-thicknesses from the corners).
 // Throws SemError(SEM_EUNSUPPORTED) if the mesh is not a stack of prism layers.

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <vector>
 
+#include "fdm.h"
 #include "topology.h"
 
 namespace sem {
@@ -32,6 +33,7 @@ struct LocalPart {
   std::vector<int32_t> elems;    // local -> global element id: owned (ascending) then halo (ascending)
   int E_own = 0;
   std::vector<LocalLevel> L;
+  std::vector<FdmTopo> F;         // opts.local_solve = 1: per level < coarsest, the rank's FDM topology
 };
 
 // topo[l]: global numbering per level; sch[l]: global Schwarz topology for
