@@ -12,6 +12,7 @@ import torch  # noqa: E402
 
 import paper_2009_00705_b200 as lib  # noqa: E402
 from workloads import config1, config2, config3  # noqa: E402
+from workloads.config5 import config5  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="config3")
@@ -20,7 +21,7 @@ ap.add_argument("--tol", type=float, default=1e-8)
 ap.add_argument("--smoother", default="dense", choices=["dense", "fdm"])
 ap.add_argument("--overlap", type=int, default=1)
 a = ap.parse_args()
-m = {"config1": config1, "config2": config2, "config3": config3}[a.config]()
+m = {"config1": config1, "config2": config2, "config3": config3, "config5": config5}[a.config]()
 s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
                local_solve=1 if a.smoother == "fdm" else 0, overlap=a.overlap)
 xyz = s.node_xyz(0)
