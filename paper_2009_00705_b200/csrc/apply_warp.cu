@@ -49,7 +49,7 @@ struct AW {
   static constexpr int LDM = 8 * MTM + 4;       // row stride of Bm (= 4 mod 8: conflict-free both ways)
   static constexpr int ROWSA = 8 * MTA;
   static constexpr int BM = 3 * ROWSA * LDM;    // doubles of Bm [3][ROWSA][LDM] (Br, Bs, B0)
-  static constexpr int W = (P <= 5) ? 16 : 8;   // warps per CTA
+  static constexpr int W = (P <= 5) ? 16 : 12;  // warps per CTA
   static constexpr int GSZ = 6 * Q;             // doubles of one element's G
   static constexpr bool WHOLE = (P <= 3);       // small elements: one TMA copy per element, else per a-tile
   static constexpr int R = WHOLE ? 2 : 3;       // slots per warp (TMA ring)
