@@ -107,10 +107,9 @@ void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas
   // element matrices are formed per chunk of subdomains, only for the element
   // range the chunk's subdomains touch (keeps setup memory bounded)
   const size_t ae_elem = (size_t)L.N * L.N * 8;
-  int64_t max_range = 1;
-  for (int k = 0; k < E; ++k)
-    max_range = std::max<int64_t>(max_range, S.elist[S.eoff[k + 1] - 1] - S.elist[S.eoff[k]] + 1);
-  int64_t cap = std::min<int64_t>(c->E, std::max<int64_t>((int64_t)(freeb * 0.25 / ae_elem), max_range));
+  int64_t max_el = 1;  // elements touched by one subdomain (the chunks below use compact element lists)
+  for (int k = 0; k < E; ++k) max_el = std::max<int64_t>(max_el, S.eoff[k + 1] - S.eoff[k]);
+  int64_t cap = std::min<int64_t>(c->E, std::max<int64_t>((int64_t)(freeb * 0.25 / ae_elem), max_el));
   double* Ae = sc.get<double>((size_t)cap * L.N * L.N);
   CUDA_CHECK(cudaMemGetInfo(&freeb, &totb));
   size_t per = (size_t)npad * npad * 8 * 2 + 64;

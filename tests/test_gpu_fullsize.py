@@ -54,7 +54,10 @@ def _interior_locals(p):
 
 @pytest.fixture(scope="module")
 def c3full():
-    return Full(config3())           # bench.py's headline configuration (exact dense Schwarz)
+    F = Full(config3())              # bench.py's headline configuration (exact dense Schwarz)
+    yield F
+    F.s.close()
+    torch.cuda.empty_cache()
 
 
 def test_full_config3_apply_sampled_rows(c3full):
