@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -629,6 +630,49 @@ void vcycle(sem_ctx* c, int li, const double* f, double* u) {
   }
 }
 
+// z = V(r) for PCG on the ctx's own buffers, replayed from a CUDA graph: the V-cycle is a
+// fixed sequence of ~100 small launches (launch-bound on small configs).  Captured on a
+// private stream after one eager run (function attributes set), replayed on the solve's
+// stream.  Not used with the iterative coarse solve (host syncs) or partitioned ctxs;
+// SEM_NO_GRAPHS=1 disables it.
+void vcycle_pcg(sem_ctx* c, const double* r, double* z) {
+  static const int off = [] {
+    const char* e = getenv("SEM_NO_GRAPHS");
+    return (e && atoi(e)) ? 1 : 0;
+  }();
+  const int slot = (z == c->pw) ? 0 : ((z == c->zw) ? 1 : -1);
+  if (off || c->C.iterative || slot < 0 || r != c->bw || c->vc_eager < 1) {
+    vcycle(c, 0, r, z);
+    c->vc_eager++;
+    return;
+  }
+  if (!c->vc_graph[slot]) {
+    if (!c->cap_stream) CUDA_CHECK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    cudaStream_t keep = c->stream;
+    c->stream = c->cap_stream;
+    const int64_t l0 = c->launches;
+    cudaGraph_t g = nullptr;
+    CUDA_CHECK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      vcycle(c, 0, r, z);
+    } catch (...) {
+      cudaStreamEndCapture(c->cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c->stream = keep;
+      throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(c->cap_stream, &g));
+    c->stream = keep;
+    c->vc_graph_launches[slot] = c->launches - l0;
+    c->launches = l0;
+    CUDA_CHECK(cudaGraphInstantiate(&c->vc_graph[slot], g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+  }
+  CUDA_CHECK(cudaGraphLaunch(c->vc_graph[slot], c->stream));
+  c->launches += c->vc_graph_launches[slot];
+}
+
 void read_scalars(sem_ctx* c, int n) {
   CUDA_CHECK(cudaMemcpyAsync(c->hscal, c->scal, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -670,7 +714,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
     // Alg 4.3: p = V(r); delta = p^T r.  With an iterative coarse solve the
     // preconditioner is not exactly linear: flexible CG (Polak-Ribiere beta)
     const bool flex = c->C.iterative != 0;
-    vcycle(c, 0, r, p);
+    vcycle_pcg(c, r, p);
     R.vcycles++;
     int dcur = 8, dnew = 10;  // [d] = z^T r, [d+1] = z^T r_old
     launch_dot2(c, n, p, r, nullptr, nullptr, nullptr, sc + dcur);
@@ -695,7 +739,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
         break;
       }
       // z = V(r); beta = z^T r / delta (flexible: z^T (r - r_old) / delta); p = z + beta p
-      vcycle(c, 0, r, z);
+      vcycle_pcg(c, r, z);
       R.vcycles++;
       if (flex) {
         launch_dot2(c, n, z, r, z, c->rw_old, nullptr, sc + dnew);
@@ -1027,6 +1071,9 @@ void sem_destroy(sem_ctx* c) {
   if (!c) return;
   cudaDeviceSynchronize();
   dist_destroy(c);
+  for (int i = 0; i < 2; ++i)
+    if (c->vc_graph[i]) cudaGraphExecDestroy(c->vc_graph[i]);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hscal) cudaFreeHost(c->hscal);
   if (c->ev0) cudaEventDestroy(c->ev0);

@@ -145,6 +145,11 @@ struct sem_ctx {
   double setup_ms = 0.0;
   std::vector<void*> allocs;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // CUDA graphs of the V-cycle (PCG's z = V(r) with the ctx's own buffers; single domain, dense coarse)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t vc_graph[2] = {nullptr, nullptr};   // output pw / zw, input bw
+  int64_t vc_graph_launches[2] = {0, 0};
+  int vc_eager = 0;                                    // eager V-cycles run before capturing
 };
 
 namespace sem {
