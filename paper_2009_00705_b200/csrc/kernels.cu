@@ -330,6 +330,20 @@ void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, i
 // 256-byte loads; row sums are reduced with a value-halving shuffle butterfly,
 // column sums (the symmetric half) accumulated per lane; per-warp private
 // accumulators in shared memory avoid atomics.
+// the lane's 8 entries of a packed tile (layouts in k_pack_tiles)
+__device__ __forceinline__ void load8(const double* tile, int lane, double (&a)[8]) {
+#pragma unroll
+  for (int m = 0; m < 8; ++m) a[m] = __ldg(tile + 32 * m + lane);
+}
+__device__ __forceinline__ void load8(const float* tile, int lane, double (&a)[8]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 v = __ldg(reinterpret_cast<const float2*>(tile + 64 * q) + lane);
+    a[2 * q] = v.x;
+    a[2 * q + 1] = v.y;
+  }
+}
+
 template <class TT>
 __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sidx, const int64_t* __restrict__ sidx_off,
                                                  const int64_t* __restrict__ tile_off,
@@ -359,12 +373,6 @@ __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sid
   const TT* tk = tiles + tile_off[k];
   const int ntiles = T * (T + 1) / 2;
   const int r0 = lane >> 4, cc = lane & 15;
-  auto tile_ij = [](int t, int& I, int& J) {
-    I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-    while ((I + 1) * (I + 2) / 2 <= t) ++I;
-    while (I * (I + 1) / 2 > t) --I;
-    J = t - I * (I + 1) / 2;
-  };
   auto tile_apply = [&](const double (&a)[8], int I, int J) {
     const double xc = x[16 * J + cc];
     double v[8];
@@ -405,14 +413,15 @@ __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sid
       y[16 * I + 2 * m + r0] += k1;
     }
   };
+  // tiles t = warp, warp + 8, ...: (I, J) advanced incrementally along the packed lower triangle
+  int I = 0, J = warp;
+  while (J > I) { J -= I + 1; ++I; }
   for (int t = warp; t < ntiles; t += 8) {
-    const TT* A = tk + (size_t)t * 256;
     double a[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) a[m] = (double)__ldg(A + 32 * m + lane);
-    int I, J;
-    tile_ij(t, I, J);
+    load8(tk + (size_t)t * 256, lane, a);
     tile_apply(a, I, J);
+    J += 8;
+    while (J > I) { J -= I + 1; ++I; }
   }
   __syncthreads();
   for (int i = tid; i < np; i += 256) {
@@ -922,7 +931,11 @@ __global__ void k_pack_tiles(const double* __restrict__ Binv, int k0, int npad, 
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     const int J = t - I * (I + 1) / 2;
     const int gi = 16 * I + r, gj = 16 * J + cc;
-    out[x] = (TT)((gi < nk && gj < nk) ? B[(size_t)gi * npad + gj] : 0.0);
+    // entry (r, c) is value m = r / 2 of lane (r % 2) * 16 + c; every warp-wide load instruction
+    // reads 256 contiguous bytes: FP64 m * 32 + lane, FP32 pairs (m / 2) * 64 + 2 lane + m % 2
+    const int ln = (r & 1) * 16 + cc, mm = r >> 1;
+    const int64_t dst = (int64_t)t * 256 + (sizeof(TT) == 8 ? mm * 32 + ln : (mm >> 1) * 64 + 2 * ln + (mm & 1));
+    out[dst] = (TT)((gi < nk && gj < nk) ? B[(size_t)gi * npad + gj] : 0.0);
   }
 }
 
