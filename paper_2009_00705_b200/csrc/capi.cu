@@ -1040,6 +1040,8 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
                      (L.nsub ? 4.0 * L.nk_sum : 0.0);
       else if (kernel == 0)
         *alg_bytes = (L.tiles32 ? 4.0 : 8.0) * L.packed + 4.0 * L.nk_sum + 32.0 * L.n;
+      else if (L.Ae1 && t->opts.apply_kernel == 0)  // element-matrix path (p <= 2)
+        *alg_bytes = (double)t->E_own * (8.0 * L.N * (L.N + 1) / 2 + 4.0 * L.N) + 16.0 * L.n;
       else
         *alg_bytes = (double)t->E_own * (48.0 * L.Q + 4.0 * L.N) + 16.0 * L.n;
     }

@@ -45,7 +45,7 @@ struct DeviceLevel {
   double* frag = nullptr;       // DMMA fragment-ordered reference operands (apply_dmma.cu)
   double* wmats = nullptr;      // reference operands of the warp-per-element apply (apply_warp.cu), p <= 6
   double* Gw = nullptr;         // a-tile-major copy of G for k_apply_warp (apply_warp.cu)
-  double* Ae1 = nullptr;        // P = 1 levels: packed element matrices [21][E] (k_apply_p1)
+  double* Ae1 = nullptr;        // P <= 2 levels: packed element matrices [N(N+1)/2][E] (k_apply_em)
   // Schwarz (not on the coarsest level)
   int32_t* sidx = nullptr;      // padded to 16 per subdomain, -1 = padding
   int64_t* sidx_off = nullptr;  // [E+1] (padded offsets)

@@ -198,61 +198,67 @@ static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y
   CUDA_CHECK(cudaGetLastError());
 }
 
-// P = 1 operator: one thread per element, y_e = A_e u_e with the element matrix
-// precomputed at setup (21 packed entries, structure-of-arrays for coalescing):
-// 192 B per element instead of the 384 B of G, and no padded tensor-core tiles.
-__global__ void __launch_bounds__(256) k_apply_p1(int E, int64_t ld, const int32_t* __restrict__ conn,
-                                                  const double* __restrict__ Ae1, const double* __restrict__ u,
+// P <= 2 operators: one thread per element, y_e = A_e u_e with the element matrix
+// precomputed at setup (N(N+1)/2 packed entries, structure-of-arrays for coalescing).
+// P = 1: 168 B per element instead of G's 384 B; P = 2: 1368 B vs 1296 B, but no
+// padded tensor-core tiles (N = 18 fills 8x8 fragments poorly).
+template <int N>
+__global__ void __launch_bounds__(128) k_apply_em(int E, int64_t ld, const int32_t* __restrict__ conn,
+                                                  const double* __restrict__ Aem, const double* __restrict__ u,
                                                   double* __restrict__ y, int flags) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
-  int g[6];
-  double x[6];
+  int g[N];
+  double x[N], acc[N];
 #pragma unroll
-  for (int i = 0; i < 6; ++i) g[i] = __ldg(conn + (size_t)e * 6 + i);
+  for (int i = 0; i < N; ++i) g[i] = __ldg(conn + (size_t)e * N + i);
 #pragma unroll
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < N; ++i) {
     x[i] = (g[i] >= 0 || (flags & AP_GATHER_ALL)) ? __ldg(u + (g[i] >= 0 ? g[i] : ~g[i])) : 0.0;
-  double a[21];
+    acc[i] = 0.0;
+  }
+  // packed lower triangle, row r: entries (r, 0..r); A symmetric
+  int k = 0;
 #pragma unroll
-  for (int k = 0; k < 21; ++k) a[k] = __ldg(Ae1 + (size_t)k * ld + e);
+  for (int r = 0; r < N; ++r) {
+#pragma unroll
+    for (int q = 0; q <= r; ++q) {
+      const double a = __ldg(Aem + (size_t)(k++) * ld + e);
+      acc[r] = fma(a, x[q], acc[r]);
+      if (q != r) acc[q] = fma(a, x[r], acc[q]);
+    }
+  }
   const double sgn = (flags & AP_NEGATE) ? -1.0 : 1.0;
 #pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {
-      const int r = i > j ? i : j, q = i > j ? j : i;
-      s = fma(a[r * (r + 1) / 2 + q], x[j], s);
-    }
-    if (g[i] >= 0) atomicAdd(y + g[i], sgn * s);
-    else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~g[i], sgn * s);
+  for (int i = 0; i < N; ++i) {
+    if (g[i] >= 0) atomicAdd(y + g[i], sgn * acc[i]);
+    else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~g[i], sgn * acc[i]);
   }
 }
 
-__global__ void k_pack_p1(int ne, int e0, int E, const double* __restrict__ Ae, double* __restrict__ Ae1) {
+__global__ void k_pack_em(int N, int ne, int e0, int64_t ld, const double* __restrict__ Ae, double* __restrict__ Aem) {
   const int le = blockIdx.x * blockDim.x + threadIdx.x;
   if (le >= ne) return;
   int k = 0;
-  for (int r = 0; r < 6; ++r)
-    for (int q = 0; q <= r; ++q) Ae1[(size_t)(k++) * E + e0 + le] = Ae[(size_t)le * 36 + r * 6 + q];
+  for (int r = 0; r < N; ++r)
+    for (int q = 0; q <= r; ++q) Aem[(size_t)(k++) * ld + e0 + le] = Ae[(size_t)le * N * N + r * N + q];
 }
 
 void build_p1_matrices(sem_ctx* c, int level, const double* d_D) {
   DeviceLevel& L = c->L[level];
-  if (L.p != 1) return;
-  const int E = c->E;
+  if (L.p > 2) return;
+  const int E = c->E, N = L.N, NP = N * (N + 1) / 2;
   L.Ae1 = nullptr;
-  CUDA_CHECK(cudaMalloc(&L.Ae1, (size_t)21 * E * sizeof(double)));
+  CUDA_CHECK(cudaMalloc(&L.Ae1, (size_t)NP * E * sizeof(double)));
   c->allocs.push_back(L.Ae1);
-  c->device_bytes += (int64_t)21 * E * 8;
-  const int chunk = 1 << 20;
+  c->device_bytes += (int64_t)NP * E * 8;
+  const int chunk = 1 << 18;
   double* Ae = nullptr;
-  CUDA_CHECK(cudaMalloc(&Ae, (size_t)std::min(chunk, E) * 36 * sizeof(double)));
+  CUDA_CHECK(cudaMalloc(&Ae, (size_t)std::min(chunk, E) * N * N * sizeof(double)));
   for (int e0 = 0; e0 < E; e0 += chunk) {
     const int ne = std::min(chunk, E - e0);
     launch_elem_matrices(c, level, d_D, Ae, e0, ne);
-    k_pack_p1<<<(ne + 255) / 256, 256, 0, c->stream>>>(ne, e0, E, Ae, L.Ae1);
+    k_pack_em<<<(ne + 255) / 256, 256, 0, c->stream>>>(N, ne, e0, (int64_t)E, Ae, L.Ae1);
     CUDA_CHECK(cudaGetLastError());
   }
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -262,10 +268,14 @@ void build_p1_matrices(sem_ctx* c, int level, const double* d_D) {
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
   {
     const DeviceLevel& L = c->L[level];
-    if (L.p == 1 && L.Ae1 && c->opts.apply_kernel == 0) {
+    if (L.p <= 2 && L.Ae1 && c->opts.apply_kernel == 0) {
       if (c->E_own > 0) {
-        k_apply_p1<<<(c->E_own + 255) / 256, 256, 0, c->stream>>>(c->E_own, (int64_t)c->E, L.conn, L.Ae1, u, y,
-                                                                   flags);
+        if (L.p == 1)
+          k_apply_em<6><<<(c->E_own + 127) / 128, 128, 0, c->stream>>>(c->E_own, (int64_t)c->E, L.conn, L.Ae1, u,
+                                                                        y, flags);
+        else
+          k_apply_em<18><<<(c->E_own + 127) / 128, 128, 0, c->stream>>>(c->E_own, (int64_t)c->E, L.conn, L.Ae1,
+                                                                         u, y, flags);
         CUDA_CHECK(cudaGetLastError());
       }
       c->launches++;
