@@ -198,6 +198,24 @@ int pmg_vcycle(sem_ctx *ctx, const double *r, double *z);
 int laplace_solve(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
                   double tol, double *phi, sem_report *rep);
 
+/* laplace_solve warm-started (the paper's per-stage solves,
+ * P:350-356): phi is read on free nodes as the initial guess u_F and overwritten
+ * with the solution; the stop test stays relative to ||b_F - A_FD phi_D||.
+ * Single-domain ctx only (SEM_EUNSUPPORTED otherwise). */
+int laplace_solve_guess(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
+                        double tol, double *phi, sem_report *rep);
+
+/* New element geometry for the next time stage:
+ * node_xyz is the nodal map in sem_mesh.node_xyz's layout (host, copied), with
+ * the same mesh topology.  strategy 1 (the paper's strategy I): only the finest
+ * operator follows the new geometry; the Schwarz inverses / FDM factors, the
+ * coarse-level operators and the coarse inverse stay those of sem_setup (t = 0).
+ * strategy 2: the operators of every level follow it (G, the P <= 2 element
+ * matrices), the smoothers and the coarse inverse stay.  Node coordinates
+ * (sem_node_xyz) are updated on the refreshed levels.  Single-domain ctx only.
+ * Errors: SEM_EINVAL, SEM_EBADELEM (detJ <= 0), SEM_EUNSUPPORTED. */
+int sem_update_geometry(sem_ctx *ctx, const double *node_xyz, int strategy);
+
 /* laplace_solve with HOST buffers (pinned recommended): copies rhs (if not
  * NULL) and dirichlet_phi host->device, solves, copies phi device->host, all
  * on opts.stream, and synchronises.  The end-to-end entry point. */

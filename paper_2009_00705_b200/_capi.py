@@ -63,6 +63,8 @@ _lib.sem_apply_laplace.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int]
 _lib.pmg_vcycle.argtypes = [_vp, _vp, _vp]
 _lib.laplace_solve.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
 _lib.laplace_solve_host.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
+_lib.laplace_solve_guess.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
+_lib.sem_update_geometry.argtypes = [_vp, _dp, C.c_int]
 _lib.sem_prolong.argtypes = [_vp, C.c_int, _vp, _vp]
 _lib.sem_restrict.argtypes = [_vp, C.c_int, _vp, _vp]
 _lib.sem_schwarz.argtypes = [_vp, C.c_int, _vp, _vp, C.c_int]
@@ -84,7 +86,7 @@ _lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.sem_host_partition.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp]
 
-EXPORTS = ["sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+EXPORTS = ["laplace_solve_guess", "sem_update_geometry", "sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
            "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
            "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
            "sem_destroy", "sem_strerror", "sem_last_error"]
@@ -310,6 +312,20 @@ class Solver:
         if check and code not in (0,):
             raise SemError(code, "laplace_solve")
         return phi, rep.as_dict()
+
+    def solve_guess(self, dirichlet_phi, tol, phi, rhs=None, check=True):
+        """laplace_solve_guess: phi (CUDA tensor) is the initial guess and the output."""
+        rep = SemReport()
+        code = _lib.laplace_solve_guess(self._ctx, None if rhs is None else _ptr(rhs), _ptr(dirichlet_phi), tol,
+                                        _ptr(phi), C.byref(rep))
+        if check and code != 0:
+            raise SemError(code, "laplace_solve_guess")
+        return phi, rep.as_dict()
+
+    def update_geometry(self, node_xyz, strategy=1):
+        """sem_update_geometry: new nodal map [n_prism][N(p)][3] (same topology)."""
+        nx = np.ascontiguousarray(node_xyz, dtype=np.float64)
+        _check(_lib.sem_update_geometry(self._ctx, nx.ctypes.data_as(_dp), int(strategy)), "sem_update_geometry")
 
     def solve_host(self, dirichlet_phi_host, tol, out_host, rhs_host=None):
         """Host buffers (numpy arrays or pinned CPU tensors), copies inside the call."""

@@ -315,6 +315,39 @@ void prepare_global(const sem_mesh* mesh, int p, const sem_opts& o, GlobalModel&
   if (o.verbose) fprintf(stderr, "[sem] numbering %.0f ms\n", now_ms() - tm);
 }
 
+// host coordinates of a level's nodes: the finest nodal map X (order pf) evaluated at the
+// level's reference nodes; in the global build the owner element's value is kept
+void level_xyz(DeviceLevel& L, int pf, const std::vector<double>& X, const std::vector<int32_t>& conn,
+               const std::vector<uint8_t>& own, int E, bool all_elements) {
+  const LevelRef& R = L.ref;
+  const int Nf = n_prism(pf);
+  L.xyz.assign((size_t)L.n * 3, 0.0);
+  std::vector<double> It, I1;
+  transfer_matrices(L.p, pf, It, I1);  // order-pf basis at this level's nodes
+  const int ntl = R.nt, n1l = R.n1, ntf = n_tri(pf), n1f = pf + 1;
+#pragma omp parallel for
+  for (int e = 0; e < E; ++e)
+    for (int l = 0; l < n1l; ++l)
+      for (int m = 0; m < ntl; ++m) {
+        const int n = m + ntl * l;
+        if (!all_elements && !own[(size_t)e * L.N + n]) continue;
+        double x[3] = {0, 0, 0};
+        for (int lf = 0; lf < n1f; ++lf)
+          for (int mf = 0; mf < ntf; ++mf) {
+            const double w = It[(size_t)m * ntf + mf] * I1[(size_t)l * n1f + lf];
+            if (w == 0.0) continue;
+            const double* Xn = &X[((size_t)e * Nf + mf + ntf * lf) * 3];
+            x[0] += w * Xn[0];
+            x[1] += w * Xn[1];
+            x[2] += w * Xn[2];
+          }
+        const int32_t g = conn[(size_t)e * L.N + n];
+        L.xyz[3 * (size_t)g] = x[0];
+        L.xyz[3 * (size_t)g + 1] = x[1];
+        L.xyz[3 * (size_t)g + 2] = x[2];
+      }
+}
+
 // Device data of the levels lids (indices into gm.topo, finest first) for the
 // whole mesh (part == nullptr; gsch = global Schwarz topologies, computed here
 // when null) or for one rank's partition.
@@ -413,33 +446,10 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
       build_g_tiles(c, li);
     }
     // node coordinates of this level (fine map evaluated at the level's nodes)
-    L.xyz.assign((size_t)L.n * 3, 0.0);
-    {
-      std::vector<double> It, I1;
-      transfer_matrices(L.p, p, It, I1);  // order-p basis at this level's nodes
-      const int ntl = R.nt, n1l = R.n1, ntf = n_tri(p), n1f = p + 1;
-#pragma omp parallel for
-      for (int e = 0; e < E; ++e)
-        for (int l = 0; l < n1l; ++l)
-          for (int m = 0; m < ntl; ++m) {
-            const int n = m + ntl * l;
-            // every (e, n) writes the same position (up to rounding); the owner's wins in the global build
-            if (!part && !own[(size_t)e * L.N + n]) continue;
-            double x[3] = {0, 0, 0};
-            for (int lf = 0; lf < n1f; ++lf)
-              for (int mf = 0; mf < ntf; ++mf) {
-                const double w = It[(size_t)m * ntf + mf] * I1[(size_t)l * n1f + lf];
-                if (w == 0.0) continue;
-                const double* Xn = &X[((size_t)e * Nf + mf + ntf * lf) * 3];
-                x[0] += w * Xn[0];
-                x[1] += w * Xn[1];
-                x[2] += w * Xn[2];
-              }
-            const int32_t g = conn[(size_t)e * L.N + n];
-            L.xyz[3 * (size_t)g] = x[0];
-            L.xyz[3 * (size_t)g + 1] = x[1];
-            L.xyz[3 * (size_t)g + 2] = x[2];
-          }
+    level_xyz(L, p, X, conn, own, E, part != nullptr);
+    if (!part) {  // kept for sem_update_geometry (single domain)
+      L.conn_host = conn;
+      L.owner_host = own;
     }
     if (li + 1 < nl) {
       std::vector<double> It, I1;
@@ -679,7 +689,8 @@ void read_scalars(sem_ctx* c, int n) {
 }
 
 // ------------------------------------------------------------------ solve
-int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
+int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep,
+             int guess = 0) {
   if (!phiD || !phi) throw SemError(SEM_EINVAL, "dirichlet_phi and phi are required");
   if (!(tol >= 0.0)) throw SemError(SEM_EINVAL, "tol must be >= 0");
   DeviceLevel& L = c->L[0];
@@ -706,6 +717,13 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   R.norm_f = nf;
   const double thresh = tol * nf + o.atol;
   double rn = nf;
+  if (guess) {  // warm start (NEXT-1, the paper's per-stage solves): u_F = phi_F, r = b_F - A_FF u_F
+    launch_init_masked(c, 0, phi, u, 1);
+    launch_apply(c, 0, u, r, AP_NEGATE);
+    launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 6);
+    read_scalars(c, 7);
+    rn = std::sqrt(c->hscal[6]);
+  }
   R.res_hist[R.n_hist++] = rn;
   int status = SEM_OK;
   if (rn <= thresh) {
@@ -939,6 +957,45 @@ int laplace_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol,
       return dist_solve(c, rhs, phiD, tol, phi, rep);
     }
     return do_solve(c, rhs, phiD, tol, phi, rep);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+}
+
+int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
+  if (!c || !node_xyz || (strategy != 1 && strategy != 2)) return SEM_EINVAL;
+  if (c->dist) return SEM_EUNSUPPORTED;
+  try {
+    const int p = c->P, Nf = n_prism(p), E = c->E;
+    std::vector<double> X(node_xyz, node_xyz + (size_t)E * Nf * 3);
+    Scratch sc;
+    const double* d_X = sc.put(X);
+    const int nlev = (strategy == 1) ? 1 : (int)c->L.size();
+    for (int li = 0; li < nlev; ++li) {
+      DeviceLevel& L = c->L[li];
+      Scratch s2;
+      const double* d_gm = s2.put(geometry_matrix(p, L.p));
+      const double* d_w = s2.put(L.ref.wq);
+      if (launch_geometry(c, li, d_X, d_gm, Nf, d_w)) throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
+      if (L.Gw) build_g_tiles(c, li);
+      if (L.Ae1) {
+        const double* d_D = s2.put(L.ref.Dfull);
+        build_p1_matrices(c, li, d_D);
+      }
+      level_xyz(L, p, X, L.conn_host, L.owner_host, E, false);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int laplace_solve_guess(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
+  if (!c) return SEM_EINVAL;
+  if (c->dist) return SEM_EUNSUPPORTED;
+  try {
+    return do_solve(c, rhs, phiD, tol, phi, rep, 1);
   } catch (const SemError& e) {
     return fail(e);
   }

@@ -79,6 +79,8 @@ struct DeviceLevel {
   // work vectors
   double *u = nullptr, *f = nullptr, *r = nullptr;
   std::vector<double> xyz;      // host [n][3]
+  std::vector<int32_t> conn_host;    // single domain: host connectivity / owner flags (geometry updates)
+  std::vector<uint8_t> owner_host;
   std::vector<uint8_t> dir_host;
   // partitioned solve (dist.cu)
   std::vector<int32_t> gid_host;     // local -> global node id

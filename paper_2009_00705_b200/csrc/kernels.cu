@@ -248,10 +248,11 @@ void build_p1_matrices(sem_ctx* c, int level, const double* d_D) {
   DeviceLevel& L = c->L[level];
   if (L.p > 2) return;
   const int E = c->E, N = L.N, NP = N * (N + 1) / 2;
-  L.Ae1 = nullptr;
-  CUDA_CHECK(cudaMalloc(&L.Ae1, (size_t)NP * E * sizeof(double)));
-  c->allocs.push_back(L.Ae1);
-  c->device_bytes += (int64_t)NP * E * 8;
+  if (!L.Ae1) {  // refreshed in place by sem_update_geometry
+    CUDA_CHECK(cudaMalloc(&L.Ae1, (size_t)NP * E * sizeof(double)));
+    c->allocs.push_back(L.Ae1);
+    c->device_bytes += (int64_t)NP * E * 8;
+  }
   const int chunk = 1 << 18;
   double* Ae = nullptr;
   CUDA_CHECK(cudaMalloc(&Ae, (size_t)std::min(chunk, E) * N * N * sizeof(double)));
