@@ -164,7 +164,8 @@ static void batched_geneig(sem_ctx* c, cusolverDnHandle_t sol, cublasHandle_t bl
 
 constexpr int FDM_NT = 8;     // n-tiles (of 8 box columns) per work unit
 constexpr int FDM_NC = 8 * FDM_NT;
-constexpr int FDM_LDR_MAX = 76;  // column-block row stride bound of the warp kernel (= 4 mod 8)
+constexpr int FDM_LDR_MAX = 76;
+constexpr int FDM_UD = 34;       // ints per unit descriptor of k_fdm_warp  // column-block row stride bound of the warp kernel (= 4 mod 8)
 constexpr int FDM_LD = 72;    // shared-memory row stride in doubles (= 8 mod 16: conflict-free B-fragment reads)
 
 // S_v, l_v of every element zero-padded to [nvp][nvp] / [nvp] (pad eigenvalue 1)
@@ -257,6 +258,32 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
                                                           L.f_Svp, L.f_lvp);
     CUDA_CHECK(cudaGetLastError());
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  }
+  {  // unit descriptors of the warp kernel (see k_fdm_warp)
+    std::vector<int4> hu(L.f_nunits);
+    CUDA_CHECK(cudaMemcpy(hu.data(), L.f_units, hu.size() * sizeof(int4), cudaMemcpyDeviceToHost));
+    std::vector<int> ud((size_t)L.f_nunits * FDM_UD, 0);
+    for (int i = 0; i < L.f_nunits; ++i) {
+      int* d = &ud[(size_t)i * FDM_UD];
+      const int q = hu[i].x, first = hu[i].y, cnt = hu[i].z;
+      d[0] = q;
+      d[1] = cnt;
+      d[2] = (int)(F.hoff[q + 1] - F.hoff[q]);
+      d[3] = F.nzc[q];
+      d[4] = (int)(uint32_t)(F.moff[q] & 0xffffffffu);
+      d[5] = (int)(F.moff[q] >> 32);
+      d[6] = (int)(uint32_t)(F.cioff[q] & 0xffffffffu);
+      d[7] = (int)(F.cioff[q] >> 32);
+      d[8] = (int)(uint32_t)(F.hoff[q] & 0xffffffffu);
+      d[9] = (int)(F.hoff[q] >> 32);
+      for (int j = 0; j < cnt && j < 8; ++j) {
+        const int e = F.colel[first + j];
+        d[10 + j] = e;
+        d[18 + j] = F.z0[e];
+        d[26 + j] = F.nv[e];
+      }
+    }
+    L.f_udesc = upload(c, ud);
   }
   L.fdm = 1;
   L.f_nh_max = F.nh_max;
@@ -542,25 +569,37 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 2) k_fdm_warp(const int4* 
                                                   const double* __restrict__ lh, const double* __restrict__ Svp,
                                                   const double* __restrict__ lvp, const double* __restrict__ W,
                                                   const double* __restrict__ r, double* __restrict__ u, int transpose,
-                                                  int ldr, const uint8_t* __restrict__ skip, int nph) {
+                                                  int ldr, const uint8_t* __restrict__ skip, int nph,
+                                                  const int* __restrict__ udesc) {
   constexpr int ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
   extern __shared__ __align__(16) double sm[];
   double* Ss = sm;                  // [ROWS][LDS]  S_h (row i node, col a mode), zero padded
   double* Rc = Ss + ROWS * LDS;     // [ROWS][ldr]  column block, later the accumulator
-  __shared__ int ez0[8], env[8], eid[8];
-  const int4 U = units[blockIdx.x];
-  const int c = U.x, first = U.y, cnt = U.z;
+  // unit descriptor (precomputed at setup, one coalesced load): [0] column, [1] elements,
+  // [2] n_h, [3] Z_c + 1, [4..5] S_h offset, [6..7] node-id offset, [8..9] l_h offset,
+  // [10..17] element ids, [18..25] z0, [26..33] n_v
+  __shared__ int ud[FDM_UD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nh = (int)(hoff[c + 1] - hoff[c]);
-  const int nz = nzc[c];
-  const int32_t* ci = cidx + cioff[c];
-  const double* S = Sh + moff[c];
-  if (tid < cnt) {
-    const int e = colel[first + tid];
-    eid[tid] = e;
-    ez0[tid] = z0[e];
-    env[tid] = nvv[e];
-  }
+  if (tid < FDM_UD) ud[tid] = __ldg(udesc + (size_t)blockIdx.x * FDM_UD + tid);
+  __syncthreads();
+  const int c = ud[0], cnt = ud[1], nh = ud[2], nz = ud[3];
+  const int64_t mo = (int64_t)(uint32_t)ud[4] | ((int64_t)ud[5] << 32);
+  const int64_t co = (int64_t)(uint32_t)ud[6] | ((int64_t)ud[7] << 32);
+  const int64_t ho = (int64_t)(uint32_t)ud[8] | ((int64_t)ud[9] << 32);
+  const int* eid = ud + 10;
+  const int* ez0 = ud + 18;
+  const int* env = ud + 26;
+  const int32_t* ci = cidx + co;
+  const double* S = Sh + mo;
+  (void)c;
+  (void)units;
+  (void)colel;
+  (void)hoff;
+  (void)moff;
+  (void)cioff;
+  (void)nzc;
+  (void)z0;
+  (void)nvv;
   {  // S_h -> shared (all loads in flight before the stores)
     constexpr int IS = (ROWS * ROWS + 255) / 256;
     double tmp[IS];
@@ -645,7 +684,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? 3 : 2) k_fdm_warp(const int4* 
     for (int n = 0; n < NVT; ++n)
 #pragma unroll
       for (int i = 0; i < 2; ++i) lvv[n][i] = __ldg(lv + n * 8 + 2 * (lane & 3) + i);
-    const double* Lh = lh + hoff[c];
+    const double* Lh = lh + ho;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       double v[NVT][2];
@@ -759,7 +798,7 @@ static void fdm_warp_launch(sem_ctx* c, const DeviceLevel& L, const double* r, d
   k_fdm_warp<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
                                                              L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
                                                              L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_ldr,
-                                                             L.f_skip, L.f_nph);
+                                                             L.f_skip, L.f_nph, L.f_udesc);
   CUDA_CHECK(cudaGetLastError());
 }
 

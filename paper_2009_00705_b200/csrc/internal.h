@@ -64,6 +64,7 @@ struct DeviceLevel {
   // column-batched kernel: work units (column, first element slot, elements, box columns)
   int4* f_units = nullptr;
   int f_nunits = 0, f_mt = 0, f_nvt = 0, f_warp = 0, f_ldr = 0, f_nph = 2;
+  int* f_udesc = nullptr;       // [units][34] descriptors of k_fdm_warp
   double *f_Svp = nullptr, *f_lvp = nullptr;   // [E][8 nvt][8 nvt] / [E][8 nvt] zero-padded S_v, l_v
   int32_t *f_colel = nullptr, *f_nzc = nullptr, *f_cidx = nullptr, *f_z0 = nullptr;
   int64_t* f_cioff = nullptr;
