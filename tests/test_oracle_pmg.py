@@ -141,3 +141,24 @@ def test_solvers_reach_direct_solution(mg_c1, method):
     res = np.array(info["res"])
     q = res[1:] / res[:-1]
     assert np.all(q[:-1] < 0.15), q
+
+
+def test_overlap_improves_contraction():
+    """P:320 / S:332-335: one overlapping node improves on block Jacobi (overlap 0)
+    and the refined overlap ceil((P+1)/2) improves further: the spectral
+    radius of the V-cycle error propagator I - V A decreases with the overlap."""
+    m = config2(p=4, nx=6, ny=2, nz=2)
+    rho = []
+    for ov in (0, 1, -1):
+        mg = pmg.PMG(m, overlap=ov)
+        A = mg.levels[0].A
+        n = A.shape[0]
+        rng = np.random.default_rng(0)
+        x = rng.standard_normal(n)
+        for _ in range(60):          # power iteration on e <- e - V(A e)
+            x = x - mg.vcycle(A @ x)
+            nx_ = np.linalg.norm(x)
+            x /= nx_
+        rho.append(nx_)
+    assert rho[0] > rho[1] > rho[2], rho
+    assert rho[1] < 0.2
