@@ -238,7 +238,9 @@ int sem_coarse_solve(sem_ctx *ctx, const double *r, double *z);
 /* Time `reps` back-to-back launches of one hot kernel on the ctx's stream with
  * CUDA events (after 3 warm-ups), on this rank's partition in a partitioned
  * ctx: kernel 0 = one Schwarz sweep (k_schwarz) on `level` (not the coarsest),
- * 1 = one operator apply (k_apply) on `level`.  mean_us: mean duration;
+ * 1 = one operator apply (k_apply) on `level`, 2 = one exact coarse solve
+ * (k_coarse_symv or the FP32 GEMV; `level` ignored; SEM_EINVAL with the
+ * iterative coarse solver).  mean_us: mean duration;
  * alg_bytes: algorithmic bytes per launch. */
 int sem_bench_kernel(sem_ctx *ctx, int kernel, int level, int reps, double *mean_us, double *alg_bytes);
 

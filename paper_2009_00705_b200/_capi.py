@@ -361,9 +361,9 @@ class Solver:
         return z
 
     def bench_kernel(self, kernel: str, level=0, reps=20):
-        """sem_bench_kernel: (mean microseconds, algorithmic bytes) of 'schwarz' or 'apply'."""
+        """sem_bench_kernel: (mean microseconds, algorithmic bytes) of 'schwarz', 'apply' or 'coarse'."""
         us, b = C.c_double(), C.c_double()
-        _check(_lib.sem_bench_kernel(self._ctx, {"schwarz": 0, "apply": 1}[kernel], level, reps, C.byref(us),
+        _check(_lib.sem_bench_kernel(self._ctx, {"schwarz": 0, "apply": 1, "coarse": 2}[kernel], level, reps, C.byref(us),
                                      C.byref(b)), "sem_bench_kernel")
         return us.value, b.value
 

@@ -226,7 +226,7 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
   c->C.fidx = upload(c, fidx);
   c->C.x = dalloc<double>(c, nc);
   Scratch sc;
-  c->C.Ainv = c->opts.mixed_precision ? sc.get<double>((size_t)nc * nc) : dalloc<double>(c, (size_t)nc * nc);
+  c->C.Ainv = sc.get<double>((size_t)nc * nc);  // full inverse in scratch; stored packed (FP64) or FP32
   if (nc == 0) return;
   double* Ae = sc.get<double>((size_t)E * L.N * L.N);
   launch_elem_matrices(c, (int)c->L.size() - 1, d_D, Ae, 0, E);
@@ -249,12 +249,15 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
   if (hinfo != 0) throw SemError(SEM_ESINGULAR, "coarse inverse failed (info " + std::to_string(hinfo) + ")");
   launch_symmetrize(c, c->C.Ainv, nc);
-  if (c->opts.mixed_precision) {  // FP32 storage of the exact inverse, FP64 arithmetic
-    c->C.Ainv32 = dalloc<float>(c, (size_t)nc * nc);
-    launch_to_float(c, nc * nc, c->C.Ainv, c->C.Ainv32);
-    CUDA_CHECK(cudaStreamSynchronize(c->stream));
-    c->C.Ainv = nullptr;  // scratch, freed on return
+  {  // packed lower-triangular tiles (FP64, or FP32 storage under mixed precision, O36):
+     // the GEMV reads half of the symmetric inverse
+    const int64_t T = (nc + 63) / 64, len = T * (T + 1) / 2 * 4096;
+    if (c->opts.mixed_precision) c->C.Apack32 = dalloc<float>(c, (size_t)len);
+    else c->C.Apack = dalloc<double>(c, (size_t)len);
+    launch_coarse_pack(c, nc, c->C.Ainv, c->C.Apack, c->C.Apack32);
   }
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->C.Ainv = nullptr;  // scratch, freed on return
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }
 
@@ -1071,9 +1074,11 @@ int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
 }
 
 int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_us, double* alg_bytes) {
-  if (!c || reps < 1 || kernel < 0 || kernel > 1) return SEM_EINVAL;
+  if (!c || reps < 1 || kernel < 0 || kernel > 2) return SEM_EINVAL;
   try {
     sem_ctx* t = c->dist ? dist_part0(c) : c;
+    if (kernel == 2) level = (int)t->L.size() - 1;
+    if (kernel == 2 && !t->C.Apack && !t->C.Apack32) return SEM_EINVAL;
     if (level < 0 || level >= (int)t->L.size()) return SEM_EINVAL;
     if (kernel == 0 && level + 1 >= (int)t->L.size()) return SEM_EINVAL;
     DeviceLevel& L = t->L[level];
@@ -1081,6 +1086,7 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
     CUDA_CHECK(cudaMemsetAsync(L.u, 0, sizeof(double) * L.n, t->stream));
     auto run = [&]() {
       if (kernel == 0) launch_schwarz(t, level, L.f, L.u, 0);
+      else if (kernel == 2) launch_coarse(t, L.f, L.u);
       else launch_apply(t, level, L.f, L.u, 0);
     };
     for (int i = 0; i < 3; ++i) run();
@@ -1092,7 +1098,10 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
     CUDA_CHECK(cudaEventElapsedTime(&ms, t->ev0, t->ev1));
     if (mean_us) *mean_us = 1e3 * ms / reps;
     if (alg_bytes) {
-      if (kernel == 0 && L.fdm)
+      const int64_t nc = t->C.nc, T = (nc + 63) / 64;
+      if (kernel == 2)  // packed lower tiles of the inverse + x, index, z
+        *alg_bytes = (t->C.Apack ? 8.0 : 4.0) * 4096.0 * (double)(T * (T + 1) / 2) + 28.0 * nc;
+      else if (kernel == 0 && L.fdm)
         *alg_bytes = (double)L.f_bytes + (L.tiles32 ? 4.0 : 8.0) * L.packed + 32.0 * L.n +
                      (L.nsub ? 4.0 * L.nk_sum : 0.0);
       else if (kernel == 0)

@@ -104,7 +104,8 @@ struct Coarse {
   int64_t nc = 0;               // free coarse nodes
   int32_t* fidx = nullptr;      // [nc] compact -> level gid
   double* Ainv = nullptr;       // [nc][nc] row-major, symmetric (dense path)
-  float* Ainv32 = nullptr;      // opts.mixed_precision: FP32 storage of Ainv (Ainv freed)
+  double* Apack = nullptr;      // lower-triangular 64x64 tiles of Ainv (Ainv freed), k_coarse_symv
+  float* Apack32 = nullptr;     // the same in FP32 storage (opts.mixed_precision, reading O36)
   double* x = nullptr;          // [nc] work
   // iterative path (reading O9): Jacobi-preconditioned CG on the P=1 operator
   int iterative = 0;
@@ -178,6 +179,7 @@ void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double
 void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi);
 void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);
 void launch_to_float(sem_ctx* c, int64_t n, const double* a, float* b);
+void launch_coarse_pack(sem_ctx* c, int64_t n, const double* A, double* P, float* P32);
 // setup kernels
 int launch_geometry(sem_ctx* c, int level, const double* d_xfine, const double* d_gmat, int Nf, const double* d_w);
 void launch_elem_matrices(sem_ctx* c, int level, const double* d_D, double* Ae, int e0, int ne);

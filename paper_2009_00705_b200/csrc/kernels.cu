@@ -7,7 +7,7 @@
 //                  packed-symmetric 16x16-tile GEMV per subdomain, HBM streaming.
 //  k_restrict      a7: r_c = P^T r_f (eq 4.3), sum-factorised.
 //  k_prolong       a9: u_f += P u_c, sum-factorised.
-//  k_coarse_gemv   a8: z = A_1^-1 r, dense symmetric inverse.
+//  k_coarse_symv   a8: z = A_1^-1 r, packed lower tiles of the symmetric inverse.
 //  vector kernels  a11: fused PCG updates and dot products (Alg 4.3).
 #include <cuda_runtime.h>
 
@@ -572,41 +572,154 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ idx, const doubl
     dst[i] = src[idx[i]];
 }
 
-// one warp per row of the dense symmetric inverse; z[fidx[i]] = sum_j Ainv[i][j] x[j]
+// ---- packed symmetric coarse inverse: lower-triangular 64x64 tiles, tile rows I = 0..T-1
+// each holding tiles J = 0..I (zero beyond n_c); tile t = I (I + 1) / 2 + J starts at t * 4096.
+// Inside a tile, lane l = 4 a + b of a warp owns the 8 x 16 sub-block rows 8a.., columns 16b..;
+// its k-th value (row 8a + k/16, column 16b + k%16) is stored at k * 32 + l, so every load
+// instruction of the GEMV reads 256 contiguous bytes.  z = A x reads each stored entry once
+// (half of the dense inverse; FP64, or FP32 storage with FP64 arithmetic under
+// opts.mixed_precision, reading O36): warps stream contiguous tile ranges, row partials stay in
+// registers along a tile row, column partials of off-diagonal tiles (the symmetric half) are
+// reduce-scattered over the 8 row-lanes and added atomically.
+__device__ __forceinline__ void tile_of(int64_t t, int64_t& I, int64_t& J) {
+  I = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  J = t - I * (I + 1) / 2;
+}
+
 template <class TA>
-__global__ void __launch_bounds__(256) k_coarse_gemv(int64_t n, const TA* __restrict__ A,
+__global__ void k_coarse_pack(int64_t n, int T, const double* __restrict__ A, TA* __restrict__ P) {
+  const int64_t ntile = (int64_t)T * (T + 1) / 2;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < ntile * 4096;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int64_t I, J;
+    tile_of(x >> 12, I, J);
+    const int w = (int)(x & 4095), k = w >> 5, l = w & 31;
+    const int64_t gi = 64 * I + 8 * (l >> 2) + (k >> 4), gj = 64 * J + 16 * (l & 3) + (k & 15);
+    P[x] = (TA)((gi < n && gj < n) ? A[gi * n + gj] : 0.0);
+  }
+}
+
+__device__ __forceinline__ void symv_flush_rows(double (&acc)[8], int64_t I, int lane, int64_t n,
+                                                const int32_t* __restrict__ fidx, double* __restrict__ z) {
+  // reduce-scatter the 8 row partials over the 4 column-lanes (lane bits 0, 1)
+  const bool b1 = lane & 2, b0 = lane & 1;
+  double v4[4], v2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double snd = b1 ? acc[i] : acc[i + 4];
+    v4[i] = (b1 ? acc[i + 4] : acc[i]) + __shfl_xor_sync(0xffffffffu, snd, 2);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double snd = b0 ? v4[i] : v4[i + 2];
+    v2[i] = (b0 ? v4[i + 2] : v4[i]) + __shfl_xor_sync(0xffffffffu, snd, 1);
+  }
+  const int64_t r0 = 64 * I + 8 * (lane >> 2) + 4 * (b1 ? 1 : 0) + 2 * (b0 ? 1 : 0);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    if (r0 + i < n) atomicAdd(z + fidx[r0 + i], v2[i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+}
+
+template <class TA>
+__global__ void __launch_bounds__(256, 3) k_coarse_symv(int64_t n, int T, const TA* __restrict__ P,
                                                      const double* __restrict__ x, const int32_t* __restrict__ fidx,
                                                      double* __restrict__ z) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = blockIdx.x * 8ll + (threadIdx.x >> 5);
-  if (row >= n) return;
-  const TA* a = A + row * n;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int64_t j = lane;
-  for (; j + 96 < n; j += 128) {
-    s0 = fma((double)__ldg(a + j), __ldg(x + j), s0);
-    s1 = fma((double)__ldg(a + j + 32), __ldg(x + j + 32), s1);
-    s2 = fma((double)__ldg(a + j + 64), __ldg(x + j + 64), s2);
-    s3 = fma((double)__ldg(a + j + 96), __ldg(x + j + 96), s3);
-  }
-  for (; j < n; j += 32) s0 = fma((double)__ldg(a + j), __ldg(x + j), s0);
-  double s = (s0 + s1) + (s2 + s3);
+  const int lane = threadIdx.x & 31, a = lane >> 2, b = lane & 3;
+  const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t ntile = (int64_t)T * (T + 1) / 2;
+  const int64_t t0 = wid * ntile / nwarp, t1 = (wid + 1) * ntile / nwarp;
+  if (t0 >= t1) return;
+  int64_t I, J;
+  tile_of(t0, I, J);
+  double acc[8], xi[8];
+  auto load_xi = [&]() {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) z[fidx[row]] = s;
+    for (int i = 0; i < 8; ++i) {
+      const int64_t g = 64 * I + 8 * a + i;
+      xi[i] = g < n ? x[g] : 0.0;
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  load_xi();
+  for (int64_t t = t0; t < t1; ++t) {
+    const TA* tile = P + t * 4096 + lane;
+    double xj[16], col[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int64_t g = 64 * J + 16 * b + j;
+      xj[j] = g < n ? x[g] : 0.0;
+      col[j] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {  // row 8a + c
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = (double)__ldcs(tile + (16 * c + k) * 32);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int rr = c, cc = k;
+        acc[rr] = fma(v[k], xj[cc], acc[rr]);
+        col[cc] = fma(v[k], xi[rr], col[cc]);
+      }
+    }
+    if (J != I) {  // z_J += A_IJ^T x_I: reduce-scatter the 16 column partials over lane bits 4, 3, 2
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+      double v8[8], v4[4], v2[2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double snd = b4 ? col[i] : col[i + 8];
+        v8[i] = (b4 ? col[i + 8] : col[i]) + __shfl_xor_sync(0xffffffffu, snd, 16);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double snd = b3 ? v8[i] : v8[i + 4];
+        v4[i] = (b3 ? v8[i + 4] : v8[i]) + __shfl_xor_sync(0xffffffffu, snd, 8);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double snd = b2 ? v4[i] : v4[i + 2];
+        v2[i] = (b2 ? v4[i + 2] : v4[i]) + __shfl_xor_sync(0xffffffffu, snd, 4);
+      }
+      const int64_t c0 = 64 * J + 16 * b + 8 * (b4 ? 1 : 0) + 4 * (b3 ? 1 : 0) + 2 * (b2 ? 1 : 0);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        if (c0 + i < n) atomicAdd(z + fidx[c0 + i], v2[i]);
+    }
+    if (++J > I || t + 1 == t1) {  // tile row done (or range end): z_I += its row partials
+      symv_flush_rows(acc, I, lane, n, fidx, z);
+      if (J > I) {
+        ++I;
+        J = 0;
+        load_xi();
+      }
+    }
+  }
 }
 
 void launch_coarse(sem_ctx* c, const double* r, double* z) {
   const DeviceLevel& L = c->L.back();
-  CUDA_CHECK(cudaMemsetAsync(z, 0, sizeof(double) * L.n, c->stream));
-  k_gather<<<grid_for(c->C.nc, 256), 256, 0, c->stream>>>(c->C.nc, c->C.fidx, r, c->C.x);
-  CUDA_CHECK(cudaGetLastError());
-  if (c->C.Ainv32)
-    k_coarse_gemv<float><<<(int)((c->C.nc + 7) / 8), 256, 0, c->stream>>>(c->C.nc, c->C.Ainv32, c->C.x, c->C.fidx, z);
-  else
-    k_coarse_gemv<double><<<(int)((c->C.nc + 7) / 8), 256, 0, c->stream>>>(c->C.nc, c->C.Ainv, c->C.x, c->C.fidx, z);
-  CUDA_CHECK(cudaGetLastError());
-  c->launches += 2;
+  if (c->C.Apack || c->C.Apack32) {
+    CUDA_CHECK(cudaMemsetAsync(z, 0, sizeof(double) * L.n, c->stream));
+    k_gather<<<grid_for(c->C.nc, 256), 256, 0, c->stream>>>(c->C.nc, c->C.fidx, r, c->C.x);
+    CUDA_CHECK(cudaGetLastError());
+    const int T = (int)((c->C.nc + 63) / 64);
+    const int64_t ntile = (int64_t)T * (T + 1) / 2;
+    const int grid = (int)std::min<int64_t>(148 * 3, (ntile + 7) / 8);  // 3 resident CTAs per SM
+    if (c->C.Apack)
+      k_coarse_symv<double><<<grid, 256, 0, c->stream>>>(c->C.nc, T, c->C.Apack, c->C.x, c->C.fidx, z);
+    else
+      k_coarse_symv<float><<<grid, 256, 0, c->stream>>>(c->C.nc, T, c->C.Apack32, c->C.x, c->C.fidx, z);
+    CUDA_CHECK(cudaGetLastError());
+    c->launches += 2;
+    return;
+  }
+  throw SemError(SEM_EINVAL, "exact coarse solve without a stored inverse");
 }
 
 // ============================================================== vector kernels
@@ -960,6 +1073,13 @@ void launch_pack_tiles(sem_ctx* c, int level, const double* Binv, int k0, int nb
 __global__ void k_to_float(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (float)a[i];
+}
+
+void launch_coarse_pack(sem_ctx* c, int64_t n, const double* A, double* P, float* P32) {
+  const int T = (int)((n + 63) / 64);
+  if (P) k_coarse_pack<double><<<148 * 32, 256, 0, c->stream>>>(n, T, A, P);
+  else k_coarse_pack<float><<<148 * 32, 256, 0, c->stream>>>(n, T, A, P32);
+  CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_to_float(sem_ctx* c, int64_t n, const double* a, float* b) {

@@ -148,7 +148,9 @@ def test_schwarz_parity(case, request):
 
 @pytest.mark.parametrize("case", ALL)
 def test_coarse_solve_parity(case, request):
-    """a8: exact P=1 solve."""
+    """a8: exact P=1 solve: k_coarse_symv on packed 64x64 tiles of the
+    symmetric inverse -- c1's 50 free P=1 nodes fill one ragged diagonal tile, c2's
+    1300 span 21 tile rows (ragged tail of 20) with off-diagonal tiles."""
     C = request.getfixturevalue(case)
     last = C.mg.levels[-1]
     r = random_vector(last.A.shape[0], seed=5)
