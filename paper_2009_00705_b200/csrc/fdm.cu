@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(256) k_fdm_col(const int4* __restrict__ units,
 // then every column node is scattered once.  Row strides = 4 mod 8 doubles:
 // conflict-free for both fragment patterns (4 rows x 8 and 8 rows x 4).
 template <int MT, int NVT>
-__global__ void __launch_bounds__(256, NVT == 1 ? 3 : 2) k_fdm_warp(const int4* __restrict__ units, const int32_t* __restrict__ colel,
+__global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_warp(const int4* __restrict__ units, const int32_t* __restrict__ colel,
                                                   const int64_t* __restrict__ hoff, const int64_t* __restrict__ moff,
                                                   const int64_t* __restrict__ cioff, const int32_t* __restrict__ nzc,
                                                   const int32_t* __restrict__ cidx, const int32_t* __restrict__ z0,

@@ -595,7 +595,9 @@ __global__ void k_coarse_pack(int64_t n, int T, const double* __restrict__ A, TA
        x += (int64_t)gridDim.x * blockDim.x) {
     int64_t I, J;
     tile_of(x >> 12, I, J);
-    const int w = (int)(x & 4095), k = w >> 5, l = w & 31;
+    // FP64: value k of lane l at k * 32 + l; FP32: pairs (k, k + 1) at (k / 2) * 64 + 2 l + k % 2 (8-byte loads)
+    const int w = (int)(x & 4095);
+    const int k = sizeof(TA) == 8 ? w >> 5 : 2 * (w >> 6) + (w & 1), l = sizeof(TA) == 8 ? w & 31 : (w >> 1) & 31;
     const int64_t gi = 64 * I + 8 * (l >> 2) + (k >> 4), gj = 64 * J + 16 * (l & 3) + (k & 15);
     P[x] = (TA)((gi < n && gj < n) ? A[gi * n + gj] : 0.0);
   }
@@ -659,8 +661,18 @@ __global__ void __launch_bounds__(256, 3) k_coarse_symv(int64_t n, int T, const 
 #pragma unroll
     for (int c = 0; c < 8; ++c) {  // row 8a + c
       double v[16];
+      if constexpr (sizeof(TA) == 8) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = (double)__ldcs(tile + (16 * c + k) * 32);
+        for (int k = 0; k < 16; ++k) v[k] = (double)__ldcs(tile + (16 * c + k) * 32);
+      } else {
+        const float2* t2 = reinterpret_cast<const float2*>(tile - lane) + lane;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 f = __ldcs(t2 + (8 * c + k) * 32);
+          v[2 * k] = f.x;
+          v[2 * k + 1] = f.y;
+        }
+      }
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int rr = c, cc = k;
