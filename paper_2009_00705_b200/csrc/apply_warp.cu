@@ -32,6 +32,15 @@
 
 namespace sem {
 
+#ifndef AW_W_SMALL
+#define AW_W_SMALL 16   // warps per CTA for p <= 5
+#endif
+#ifndef AW_MA_UNROLL
+#define AW_MA_UNROLL 1  // unroll of the a-tile loop
+#endif
+#define AW_PRAGMA_(x) _Pragma(#x)
+#define AW_PRAGMA(x) AW_PRAGMA_(x)
+
 namespace aw {
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 }  // namespace aw
@@ -49,7 +58,7 @@ struct AW {
   static constexpr int LDM = 8 * MTM + 4;       // row stride of Bm (= 4 mod 8: conflict-free both ways)
   static constexpr int ROWSA = 8 * MTA;
   static constexpr int BM = 3 * ROWSA * LDM;    // doubles of Bm [3][ROWSA][LDM] (Br, Bs, B0)
-  static constexpr int W = (P <= 5) ? 16 : 12;  // warps per CTA
+  static constexpr int W = (P <= 5) ? AW_W_SMALL : 12;  // warps per CTA
   static constexpr int GSZ = 6 * Q;             // doubles of one element's G
   static constexpr bool WHOLE = (P <= 3);       // small elements: one TMA copy per element, else per a-tile
   static constexpr int R = WHOLE ? 2 : 3;       // slots per warp (TMA ring)
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
     for (int mm = 0; mm < D::MTM; ++mm)
 #pragma unroll
       for (int nq = 0; nq < D::NQ; ++nq) Vt[mm][nq][0] = Vt[mm][nq][1] = Vdt[mm][nq][0] = Vdt[mm][nq][1] = 0.0;
-#pragma unroll 1
+    AW_PRAGMA(unroll AW_MA_UNROLL)
     for (int ma = 0; ma < D::MTA; ++ma) {
       const int t = D::WHOLE ? tk : tk + ma;
       if (!D::WHOLE || ma == 0) {  // wait for copy t of G

@@ -1,0 +1,31 @@
+"""Summarise one ncu --set full report (first kernel) into a text file for profiles/:
+key raw metrics and the SOL / memory / scheduler / occupancy sections."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum"]
+SECTIONS = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Scheduler Statistics", "Occupancy",
+            "Warp State Statistics", "Compute Workload Analysis")
+
+
+def main(rep, title, out):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, u, v = r[0], r[1], r[2]
+    lines = [f"# ncu --set full capture: {title}", ""]
+    lines += [f"{k} = {v[h.index(k)]} {u[h.index(k)]}" for k in KEYS if k in h]
+    lines.append("")
+    det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.DictReader(io.StringIO(det)))
+    for row in rows:
+        if row["ID"] == rows[0]["ID"] and row["Section Name"] in SECTIONS:
+            lines.append(f"{row['Section Name']} | {row['Metric Name']} = {row['Metric Value']} {row['Metric Unit']}")
+    open(out, "w").write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], sys.argv[3])
