@@ -1,4 +1,5 @@
-"""Time one FDM sweep (k_fdm_col) and one operator apply on a config, finest level."""
+"""Time one FDM sweep per level (config 3, or config 5 with CONFIG=config5) with
+sem_bench_kernel: mean us, algorithmic bytes, GB/s."""
 import os
 import sys
 
@@ -9,7 +10,11 @@ import paper_2009_00705_b200 as lib
 from workloads import config3
 
 ov = int(os.environ.get("OV", "1"))
-m = config3()
+if os.environ.get("CONFIG") == "config5":
+    from workloads.config5 import config5
+    m = config5()
+else:
+    m = config3()
 s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
                local_solve=1, overlap=ov, verbose=1)
 for li in range(s.info["n_levels"] - 1):
