@@ -9,7 +9,7 @@ import paper_2009_00705_b200 as lib
 from workloads.config5 import config5
 
 m = config5()
-for crt in (1e-10, 1e-13, 1e-6):
+for crt in [float(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1e-10,1e-6,1e-4,1e-2").split(",")]:
     s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
                    local_solve=1, coarse_rtol=crt)
     xyz = s.node_xyz(0)
