@@ -904,14 +904,19 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     for (int mt = 0; mt < MT; ++mt) lav[mt] = mt * 8 + r4 < nh ? __ldg(lh + ho + mt * 8 + r4) : 1.0;
   }
   const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
-  for (int base = 0; base < ROWS * ldb; base += 256 * 8) {  // column block (x W for S^-T)
-    int gid[8];
-    double val[8];
+  // column block (x W for S^-T): the n_h x n_zu valid entries; rows >= n_h zeroed (they meet the
+  // zero columns of S_h^T: stale shared memory there could hold non-finite values), columns
+  // >= n_zu only reach output columns no later step reads
+  const int nval = nh * nzu;
+  for (int base = 0; base < nval; base += 256 * 8) {
+    int gid[8], pos[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int t = base + tid + 256 * k, h = t / ldb, zz = t - h * ldb;
-      gid[k] = (t < ROWS * ldb && h < nh && zz < nzu) ? __ldg(ci + h * nz + zlo + zz) : -1;
+      const int t = base + tid + 256 * k, h = t / nzu, zz = t - h * nzu;
+      pos[k] = t < nval ? h * ldb + zz : -1;
+      gid[k] = t < nval ? __ldg(ci + h * nz + zlo + zz) : -1;
     }
+    double val[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) val[k] = gid[k] >= 0 ? r[gid[k]] : 0.0;
     if (transpose) {
@@ -920,11 +925,10 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
         if (gid[k] >= 0) val[k] *= __ldg(W + gid[k]);
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = base + tid + 256 * k;
-      if (t < ROWS * ldb) B1[t] = val[k];
-    }
+    for (int k = 0; k < 8; ++k)
+      if (pos[k] >= 0) B1[pos[k]] = val[k];
   }
+  for (int t = nh * ldb + tid; t < ROWS * ldb; t += 256) B1[t] = 0.0;
   __syncthreads();
   // 1. Tall = S_h^T Rc -> B2
   fdm_cta_gemm<MT, true>(Ss, B1, B2, ldb, nzu, warp, lane);
