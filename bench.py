@@ -248,7 +248,7 @@ def run_config5(args, lib, peak):
            "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "n_dof": i["n_dof"],
            "n_free": i["n_free"], "coarse": f"P=1, {i['coarse_n']} free DOF (Jacobi-PCG)", "setup_s": setup_s,
            "device_GB": i["device_bytes"] / 1e9,
-           "smoother_kernel": {"kernel": "k_fdm_warp<8,2> + k_schwarz<double> (O35 subset)", "us": us,
+           "smoother_kernel": {"kernel": "k_fdm_cta<8> + k_schwarz<double> (O35 subset)", "us": us,
                                "alg_bytes_per_launch": b, "achieved_GBs": b / us / 1e3, "frac_hbm": b / us / 1e3 / peak},
            "apply": {"kernel": "k_apply_warp<6>", "us": ua, "achieved_GBs": ba / ua / 1e3, "frac": ba / ua / 1e3 / peak}}
     s.close()

@@ -122,12 +122,15 @@ typedef struct {
 
 typedef struct {
   int iters;                  /* outer iterations                                                   */
-  int vcycles;                /* V-cycles applied (iterations + 1 for PCG)           */
+  int vcycles;                /* V-cycles applied: = iters for PCG (the V-cycle after the converged
+                                 iteration is skipped) and for PDC / MG                 */
   int converged;              /* 1 if ||r|| <= rtol ||f|| + atol (O21)                        */
   double rel_res;             /* final ||r||_2 / ||f||_2 over free nodes                            */
   double q_mean;              /* geometric mean of q = ||r^m||/||r^m-1|| (eq 4.7; O22)        */
   double t_ms;                /* device time of the solve (CUDA events)                             */
   double norm_f;              /* ||b_F||_2                                                           */
+  double wu;                  /* work units of this solve: t_ms / (device time of one finest-level
+                                 operator apply, timed at setup) (reading O25)                 */
   int coarse_iters;           /* inner coarse-solve iterations in this solve (iterative coarse path)  */
   int n_hist;                 /* entries of res_hist used                                            */
   double res_hist[256];       /* ||r^m||_2, m = 0..iters                                            */
@@ -147,7 +150,19 @@ typedef struct {
   int64_t coarse_n;           /* free nodes of the P=1 level (size of the dense coarse inverse)     */
   int64_t device_bytes;       /* total device memory held by the ctx                                */
   double setup_ms;            /* wall time of sem_setup                                             */
+  int smoother_kernel[16];    /* sweep kernel of each level's smoother (SEM_SMOOTHER_*; 0 on the
+                                 coarsest level)                                                     */
+  int smoother_mt[16];        /* FDM levels: 8-row tiles of the largest horizontal patch, ceil(n_h/8) */
 } sem_info;
+
+/* sem_info.smoother_kernel */
+#define SEM_SMOOTHER_NONE        0   /* coarsest level: exact coarse solve                             */
+#define SEM_SMOOTHER_DENSE       1   /* k_schwarz: packed exact inverses (eq 4.4)                      */
+#define SEM_SMOOTHER_FDM_WARP1   2   /* k_fdm_warp<MT,1>: FDM, one warp per element, n_v <= 8          */
+#define SEM_SMOOTHER_FDM_WARP2   3   /* k_fdm_warp<MT,2>: FDM, one warp per element, n_v <= 16         */
+#define SEM_SMOOTHER_FDM_CTA     4   /* k_fdm_cta<MT>: FDM, CTA-shared horizontal transforms (p >= 6)   */
+#define SEM_SMOOTHER_FDM_COL     5   /* k_fdm_col<MT,NVT>: FDM, large patches (refined overlap)         */
+#define SEM_SMOOTHER_FDM_GENERIC 6   /* k_fdm: FDM, any size (fallback)                                 */
 
 /* Default options (values above). */
 void sem_default_opts(sem_opts *opts);

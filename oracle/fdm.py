@@ -191,14 +191,16 @@ def regular(cols: Columns, overlap: int):
     return out
 
 
-def fdm_blocks(mesh, level: sem.Level, overlap: int, cols: Columns | None = None):
-    """Per element k: (global 3D ids of the subdomain's free nodes, dense local
-    inverse (B~_k^{-1}) restricted to them)."""
+def fdm_blocks(mesh, level: sem.Level, overlap: int, cols: Columns | None = None, elems=None,
+               inverses: bool = True):
+    """Per element k (all, or those in `elems`): (global 3D ids of the subdomain's
+    free nodes, dense local inverse (B~_k^{-1}) restricted to them, or None when
+    inverses=False)."""
     cols = cols or Columns(mesh, level)
     p = level.p
     out = []
     cache = {}
-    for k in range(level.conn.shape[0]):
+    for k in (range(level.conn.shape[0]) if elems is None else elems):
         c = int(cols.col[k])
         if c not in cache:
             H = cols.patch(c, overlap)
@@ -211,10 +213,13 @@ def fdm_blocks(mesh, level: sem.Level, overlap: int, cols: Columns | None = None
         j = int(cols.layer[k])
         V = [z for z in range(max(0, j * p - overlap), min(Zc, j * p + p + overlap) + 1) if z not in dz]
         V = np.array(V)
-        B = np.kron(Kh, Mv[np.ix_(V, V)]) + np.kron(Mh, Kv[np.ix_(V, V)])
-        Binv = np.linalg.inv(B)
         ids = cols.node_at[np.repeat(H, len(V)), np.tile(V, len(H))]    # box order (h outer, z inner)
         keep = ids >= 0
         keep[keep] = ~level.dirichlet[ids[keep]]
+        if not inverses:
+            out.append((ids[keep], None))
+            continue
+        B = np.kron(Kh, Mv[np.ix_(V, V)]) + np.kron(Mh, Kv[np.ix_(V, V)])
+        Binv = np.linalg.inv(B)
         out.append((ids[keep], Binv[np.ix_(keep, keep)]))
     return out

@@ -123,7 +123,7 @@ def hybrid_sets(mesh, level: sem.Level, overlap: int):
     reg = fdm.regular(cols, overlap)
     dense = schwarz_sets(level, overlap) if not reg.all() else None
     return [np.sort(ids) if reg[k] else dense[k]
-            for k, (ids, _) in enumerate(fdm.fdm_blocks(mesh, level, overlap, cols))], reg
+            for k, (ids, _) in enumerate(fdm.fdm_blocks(mesh, level, overlap, cols, inverses=False))], reg
 
 
 def build_fdm_smoother(mesh, level: sem.Level, overlap: int, AFF: sp.csr_matrix | None = None) -> Smoother:

@@ -85,12 +85,13 @@ def geometry(mesh, p_geo: int, p: int, elems=None):
     pts, w = R.prism_cubature(p)
     _, dgeo = R.prism_basis(p_geo, pts)                 # [3][Q][Ng]
     # J[e][q][i][c] = sum_n X[e][n][i] * dgeo[c][q][n]
-    J = np.einsum("eni,cqn->eqic", X, dgeo)
+    # (optimize=True only lets numpy contract through BLAS: same formula, summation order only)
+    J = np.einsum("eni,cqn->eqic", X, dgeo, optimize=True)
     det = np.linalg.det(J)
     if np.any(det <= 0):
         raise ValueError("invalid element: detJ <= 0")
     Ji = np.linalg.inv(J)
-    G = np.einsum("q,eq,eqij,eqkj->eqik", w, det, Ji, Ji)
+    G = np.einsum("q,eq,eqij,eqkj->eqik", w, det, Ji, Ji, optimize=True)
     return G
 
 
@@ -117,23 +118,27 @@ def build_system(mesh, p: int, p_geo: int | None = None) -> Level:
     return lev
 
 
-def apply_streamed(mesh, level: Level, u: np.ndarray, p_geo: int | None = None, chunk: int = 4096):
+def apply_streamed(mesh, level: Level, u: np.ndarray, p_geo: int | None = None, chunk: int = 4096,
+                   elems: np.ndarray | None = None):
     """y = sum_e Q_e^T D^T (G (.) D Q_e u) without forming element matrices
-    (SURVEY §8(c) tier (a) for configs too large to assemble)."""
+    (SURVEY §8(c) tier (a) for configs too large to assemble).  u: [n] or [n][k]
+    (k vectors at once); elems: the elements summed (default all; level.conn is
+    indexed by position in elems when given)."""
     p = level.p
     pts, _ = R.prism_cubature(p)
     _, D = R.prism_basis(p, pts)                        # [3][Q][N]
-    y = np.zeros(level.n)
-    E = level.conn.shape[0]
-    for e0 in range(0, E, chunk):
-        el = np.arange(e0, min(E, e0 + chunk))
-        G = geometry(mesh, p_geo or mesh.p, p, el)      # [e][Q][3][3]
-        ue = u[level.conn[el]]                          # [e][N]
-        g = np.einsum("cqn,en->eqc", D, ue)
-        f = np.einsum("eqcd,eqd->eqc", G, g)
-        ye = np.einsum("cqn,eqc->en", D, f)
-        np.add.at(y, level.conn[el].ravel(), ye.ravel())
-    return y
+    u2 = u.reshape(u.shape[0], -1)
+    y = np.zeros((level.n, u2.shape[1]))
+    all_el = np.arange(level.conn.shape[0]) if elems is None else np.asarray(elems)
+    for c0 in range(0, len(all_el), chunk):
+        pos = np.arange(c0, min(len(all_el), c0 + chunk))
+        G = geometry(mesh, p_geo or mesh.p, p, all_el[pos])   # [e][Q][3][3]
+        ue = u2[level.conn[pos]]                        # [e][N][k]
+        g = np.einsum("cqn,enk->eqck", D, ue, optimize=True)
+        f = np.einsum("eqcd,eqdk->eqck", G, g, optimize=True)
+        ye = np.einsum("cqn,eqck->enk", D, f, optimize=True)
+        np.add.at(y, level.conn[pos].ravel(), ye.reshape(-1, u2.shape[1]))
+    return y.reshape(u.shape)
 
 
 def apply_sampled(mesh, level: Level, u: np.ndarray, rows: np.ndarray, p_geo: int | None = None):

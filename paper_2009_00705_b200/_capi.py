@@ -33,13 +33,14 @@ class SemOpts(C.Structure):
 
 class SemReport(C.Structure):
     _fields_ = [("iters", C.c_int), ("vcycles", C.c_int), ("converged", C.c_int), ("rel_res", C.c_double),
-                ("q_mean", C.c_double), ("t_ms", C.c_double), ("norm_f", C.c_double), ("coarse_iters", C.c_int),
+                ("q_mean", C.c_double), ("t_ms", C.c_double), ("norm_f", C.c_double), ("wu", C.c_double),
+                ("coarse_iters", C.c_int),
                 ("n_hist", C.c_int),
                 ("res_hist", C.c_double * 256)]
 
     def as_dict(self):
         return dict(iters=self.iters, vcycles=self.vcycles, converged=bool(self.converged),
-                    rel_res=self.rel_res, q_mean=self.q_mean, t_ms=self.t_ms, norm_f=self.norm_f,
+                    rel_res=self.rel_res, q_mean=self.q_mean, t_ms=self.t_ms, norm_f=self.norm_f, wu=self.wu,
                     coarse_iters=self.coarse_iters,
                     res_hist=list(self.res_hist[: self.n_hist]))
 
@@ -49,7 +50,11 @@ class SemInfo(C.Structure):
                 ("level_p", C.c_int * 16), ("level_n_dof", C.c_int64 * 16), ("level_n_free", C.c_int64 * 16),
                 ("schwarz_bytes", C.c_int64 * 16), ("schwarz_nk_sum", C.c_int64 * 16),
                 ("schwarz_packed", C.c_int64 * 16), ("coarse_n", C.c_int64), ("device_bytes", C.c_int64),
-                ("setup_ms", C.c_double)]
+                ("setup_ms", C.c_double), ("smoother_kernel", C.c_int * 16), ("smoother_mt", C.c_int * 16)]
+
+
+SMOOTHER_KERNELS = {0: "coarse", 1: "k_schwarz", 2: "k_fdm_warp<MT,1>", 3: "k_fdm_warp<MT,2>", 4: "k_fdm_cta<MT>",
+                    5: "k_fdm_col", 6: "k_fdm"}
 
 
 _vp = C.c_void_p
@@ -274,7 +279,9 @@ class Solver:
                          schwarz_bytes=list(inf.schwarz_bytes[: inf.n_levels]),
                          schwarz_nk_sum=list(inf.schwarz_nk_sum[: inf.n_levels]),
                          schwarz_packed=list(inf.schwarz_packed[: inf.n_levels]),
-                         coarse_n=inf.coarse_n, device_bytes=inf.device_bytes, setup_ms=inf.setup_ms)
+                         coarse_n=inf.coarse_n, device_bytes=inf.device_bytes, setup_ms=inf.setup_ms,
+                         smoother_kernel=[SMOOTHER_KERNELS[k] for k in inf.smoother_kernel[: inf.n_levels]],
+                         smoother_mt=list(inf.smoother_mt[: inf.n_levels]))
 
     # ---------------------------------------------------------------- helpers
     def n_dof(self, level=0):

@@ -22,16 +22,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for s in srcs:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(s):
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        cmd = [NVCC, "-c", s, "-o", o] + FLAGS
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if verbose or r.returncode:
-            sys.stderr.write(r.stdout + r.stderr)
-        if r.returncode:
-            raise RuntimeError("nvcc failed on " + s)
-        objs.append(o)
+        r = subprocess.run([NVCC, "-c", s, "-o", o] + FLAGS, capture_output=True, text=True)
+        return s, o, r
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        for s, o, r in ex.map(compile_one, srcs):
+            if verbose or r.returncode:
+                sys.stderr.write(r.stdout + r.stderr)
+            if r.returncode:
+                raise RuntimeError("nvcc failed on " + s)
+            objs.append(o)
     cmd = [NVCC, "-shared", "-o", LIB] + objs + ["-gencode", "arch=compute_100a,code=sm_100a",
                                                  "-Xcompiler", "-fopenmp", "-lcublas", "-lcusolver", "-lgomp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)

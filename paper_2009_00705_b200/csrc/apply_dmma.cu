@@ -356,11 +356,12 @@ static void apply_dmma_P(sem_ctx* c, const DeviceLevel& L, const double* u, doub
   using D = MD<P, NE_, W_, FS_>;
   constexpr int ne = D::NE, w = D::WARPS, fs = D::FS ? 1 : 0;
   auto kern = k_apply_dmma<P, ne, w, fs>;
-  static int grid_max = 0;
+  static int grid_maxes[kMaxDev] = {0};
+  const int dev = cur_device();
+  int& grid_max = grid_maxes[dev];
   if (!grid_max) {
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
-    int per_sm = 0, sms = 0, dev = 0;
-    CUDA_CHECK(cudaGetDevice(&dev));
+    int per_sm = 0, sms = 0;
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, D::T, D::SMEM));
     grid_max = sms * (per_sm > 0 ? per_sm : 1);

@@ -405,11 +405,12 @@ void build_g_tiles(sem_ctx* c, int level) {
 template <int P>
 static void apply_warp_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags) {
   using D = AW<P>;
-  static int grid_max = 0;
+  static int grid_maxes[kMaxDev] = {0};
+  const int dev = cur_device();
+  int& grid_max = grid_maxes[dev];
   if (!grid_max) {
     CUDA_CHECK(cudaFuncSetAttribute(k_apply_warp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
-    int per_sm = 0, sms = 0, dev = 0;
-    CUDA_CHECK(cudaGetDevice(&dev));
+    int per_sm = 0, sms = 0;
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_warp<P>, 32 * D::W, D::SMEM));
     grid_max = sms * (per_sm > 0 ? per_sm : 1);

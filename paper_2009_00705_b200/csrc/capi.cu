@@ -554,6 +554,17 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
     std::vector<int> lids(gm.sched.size());
     for (size_t i = 0; i < lids.size(); ++i) lids[i] = (int)i;
     build_levels(c, gm, lids, nullptr, nullptr);
+    // one finest-level apply, timed for the work-unit count of every solve (O25)
+    const int64_t n0 = c->L[0].n;
+    CUDA_CHECK(cudaMemsetAsync(c->pw, 0, sizeof(double) * n0, c->stream));
+    for (int i = 0; i < 2; ++i) launch_apply(c, 0, c->pw, c->qw, 0);
+    CUDA_CHECK(cudaEventRecord(c->ev0, c->stream));
+    for (int i = 0; i < 5; ++i) launch_apply(c, 0, c->pw, c->qw, 0);
+    CUDA_CHECK(cudaEventRecord(c->ev1, c->stream));
+    CUDA_CHECK(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->t_apply_ms = ms / 5.0;
   }
   CUDA_CHECK(cudaDeviceSynchronize());
   c->launches = 0;
@@ -714,6 +725,8 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   launch_init_masked(c, 0, rhs, r, 1);
   launch_apply(c, 0, q, r, AP_GATHER_ALL | AP_NEGATE);
   CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * n, c->stream));
+  if (o.outer != 0)  // PDC / MG recompute r = b_F - A_FF u from the kept b_F
+    CUDA_CHECK(cudaMemcpyAsync(c->rw_old, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 4);
   read_scalars(c, 5);
   const double nf = std::sqrt(c->hscal[4]);
@@ -773,13 +786,13 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
     }
   } else {
     // Alg 4.2 (PDC; reading O13) and stand-alone MG: u <- u - MG(-r) = u + V(r)
+    const double* bF = c->rw_old;  // b_F of the lift (kept below)
     while (R.iters < o.imax) {
       vcycle(c, 0, r, z);
       R.vcycles++;
       launch_axpy(c, n, 1.0, z, u);
-      // r = b - A u
-      launch_init_masked(c, 0, rhs, r, 1);
-      launch_apply(c, 0, q, r, AP_GATHER_ALL | AP_NEGATE);  // q still holds the lift v
+      // r = b_F - A_FF u (one operator apply per iteration)
+      CUDA_CHECK(cudaMemcpyAsync(r, bF, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
       launch_apply(c, 0, u, r, AP_NEGATE);
       R.iters++;
       launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 3);
@@ -798,6 +811,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   float ms = 0.f;
   CUDA_CHECK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   R.t_ms = ms;
+  R.wu = c->t_apply_ms > 0 ? ms / c->t_apply_ms : 0.0;
   R.coarse_iters = (int)c->C.iters;
   R.rel_res = nf > 0 ? rn / nf : 0.0;
   if (R.n_hist > 1) {
@@ -853,6 +867,14 @@ int sem_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx** out) 
   if (!out) return SEM_EINVAL;
   *out = nullptr;
   sem_ctx* c = new sem_ctx();
+  int caller_dev = -1;
+  cudaGetDevice(&caller_dev);
+  struct Restore {
+    int d;
+    ~Restore() {
+      if (d >= 0) cudaSetDevice(d);
+    }
+  } restore{caller_dev};
   try {
     do_setup(mesh, p, opts, c);
   } catch (const SemError& e) {
@@ -886,6 +908,8 @@ int sem_get_info(const sem_ctx* c, sem_info* info) {
     info->schwarz_bytes[i] = c->L[i].schwarz_bytes;
     info->schwarz_nk_sum[i] = c->L[i].nk_sum;
     info->schwarz_packed[i] = c->L[i].packed;
+    info->smoother_kernel[i] = (i + 1 < c->L.size()) ? fdm_kernel_choice(c->L[i]) : SEM_SMOOTHER_NONE;
+    info->smoother_mt[i] = c->L[i].fdm ? c->L[i].f_mt : 0;
   }
   info->coarse_n = c->C.nc;
   info->device_bytes = c->device_bytes;
@@ -896,6 +920,7 @@ int sem_get_info(const sem_ctx* c, sem_info* info) {
 int sem_node_xyz(const sem_ctx* c, int level, double* xyz, int on_device) {
   const int nl = c ? (c->dist ? dist_levels(c) : (int)c->L.size()) : 0;
   if (!c || !xyz || level < 0 || level >= nl) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   const auto& v = c->dist ? dist_xyz(c, level) : c->L[level].xyz;
   if (on_device) {
     if (cudaMemcpy(xyz, v.data(), v.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return SEM_ECUDA;
@@ -908,6 +933,7 @@ int sem_node_xyz(const sem_ctx* c, int level, double* xyz, int on_device) {
 int sem_dirichlet_mask(const sem_ctx* c, int level, uint8_t* mask, int on_device) {
   const int nl = c ? (c->dist ? dist_levels(c) : (int)c->L.size()) : 0;
   if (!c || !mask || level < 0 || level >= nl) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   const auto& v = c->dist ? dist_dir(c, level) : c->L[level].dir_host;
   if (on_device) {
     if (cudaMemcpy(mask, v.data(), v.size(), cudaMemcpyHostToDevice) != cudaSuccess) return SEM_ECUDA;
@@ -919,6 +945,7 @@ int sem_dirichlet_mask(const sem_ctx* c, int level, uint8_t* mask, int on_device
 
 int sem_apply_laplace(sem_ctx* c, const double* u, double* y, int level, int masked) {
   if (!c || !u || !y || u == y) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   if (c->dist) {
     try {
       return dist_apply(c, u, y, level, masked);
@@ -943,6 +970,7 @@ int sem_apply_laplace(sem_ctx* c, const double* u, double* y, int level, int mas
 
 int pmg_vcycle(sem_ctx* c, const double* r, double* z) {
   if (!c || !r || !z || r == z) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     if (c->dist) return dist_vcycle(c, r, z);
     vcycle(c, 0, r, z);
@@ -954,6 +982,7 @@ int pmg_vcycle(sem_ctx* c, const double* r, double* z) {
 
 int laplace_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
   if (!c) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     if (c->dist) {
       if (!phiD || !phi || !(tol >= 0.0)) return SEM_EINVAL;
@@ -968,6 +997,7 @@ int laplace_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol,
 int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
   if (!c || !node_xyz || (strategy != 1 && strategy != 2)) return SEM_EINVAL;
   if (c->dist) return SEM_EUNSUPPORTED;
+  DeviceGuard guard(c->device);
   try {
     const int p = c->P, Nf = n_prism(p), E = c->E;
     std::vector<double> X(node_xyz, node_xyz + (size_t)E * Nf * 3);
@@ -997,6 +1027,7 @@ int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
 int laplace_solve_guess(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
   if (!c) return SEM_EINVAL;
   if (c->dist) return SEM_EUNSUPPORTED;
+  DeviceGuard guard(c->device);
   try {
     return do_solve(c, rhs, phiD, tol, phi, rep, 1);
   } catch (const SemError& e) {
@@ -1007,6 +1038,7 @@ int laplace_solve_guess(sem_ctx* c, const double* rhs, const double* phiD, doubl
 int laplace_solve_host(sem_ctx* c, const double* rhs_host, const double* phiD_host, double tol, double* phi_host,
                        sem_report* rep) {
   if (!c || !phiD_host || !phi_host) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     sem_info inf;
     sem_get_info(c, &inf);
@@ -1032,6 +1064,7 @@ int laplace_solve_host(sem_ctx* c, const double* rhs_host, const double* phiD_ho
 int sem_prolong(sem_ctx* c, int level, const double* uc, double* uf) {
   if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !uc || !uf || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     launch_prolong(c, level, uc, uf);
   } catch (const SemError& e) {
@@ -1043,6 +1076,7 @@ int sem_prolong(sem_ctx* c, int level, const double* uc, double* uf) {
 int sem_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
   if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !rf || !rc || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     launch_restrict(c, level, rf, rc);
   } catch (const SemError& e) {
@@ -1054,6 +1088,7 @@ int sem_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
 int sem_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose) {
   if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !r || !u || level < 0 || level + 1 >= (int)c->L.size()) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     launch_schwarz(c, level, r, u, transpose);
   } catch (const SemError& e) {
@@ -1065,6 +1100,7 @@ int sem_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose
 int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
   if (c && c->dist) return SEM_EUNSUPPORTED;
   if (!c || !r || !z) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     coarse_solve(c, r, z);
   } catch (const SemError& e) {
@@ -1075,6 +1111,7 @@ int sem_coarse_solve(sem_ctx* c, const double* r, double* z) {
 
 int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_us, double* alg_bytes) {
   if (!c || reps < 1 || kernel < 0 || kernel > 2) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
   try {
     sem_ctx* t = c->dist ? dist_part0(c) : c;
     if (kernel == 2) level = (int)t->L.size() - 1;
@@ -1137,6 +1174,7 @@ int64_t sem_launch_count(const sem_ctx* c, int reset) {
 
 void sem_destroy(sem_ctx* c) {
   if (!c) return;
+  DeviceGuard guard(c->device);
   cudaDeviceSynchronize();
   dist_destroy(c);
   for (int i = 0; i < 2; ++i)

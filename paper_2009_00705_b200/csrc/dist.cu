@@ -328,6 +328,8 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
     launch_init_masked(c, 0, rhs.empty() ? nullptr : rhs[i], r[i], 2);
     launch_apply(c, 0, q[i], r[i], AP_GATHER_ALL | AP_NEGATE);
     CUDA_CHECK(cudaMemsetAsync(u[i], 0, sizeof(double) * c->L[0].n, c->stream));
+    if (o.outer != 0)  // PDC / MG: keep this rank's partial b_F (summed by every later exchange)
+      CUDA_CHECK(cudaMemcpyAsync(ro[i], r[i], sizeof(double) * c->L[0].n, cudaMemcpyDeviceToDevice, c->stream));
   });
   exchange(D, 0, r);
   double h[4];
@@ -389,8 +391,7 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
       R.vcycles++;
       each(D, [&](sem_ctx* c, int i) {
         launch_axpy(c, c->L[0].n, 1.0, z[i], u[i]);
-        launch_init_masked(c, 0, rhs.empty() ? nullptr : rhs[i], r[i], 2);
-        launch_apply(c, 0, q[i], r[i], AP_GATHER_ALL | AP_NEGATE);
+        CUDA_CHECK(cudaMemcpyAsync(r[i], ro[i], sizeof(double) * c->L[0].n, cudaMemcpyDeviceToDevice, c->stream));
         launch_apply(c, 0, u[i], r[i], AP_NEGATE);
       });
       exchange(D, 0, r);
@@ -690,6 +691,11 @@ void dist_info(const sem_ctx* c, sem_info* info) {
       info->schwarz_bytes[i] += pc->L[i].schwarz_bytes;
       info->schwarz_nk_sum[i] += pc->L[i].nk_sum;
       info->schwarz_packed[i] += pc->L[i].packed;
+    }
+    const sem_ctx* p0 = D.parts[0];
+    if (i + 1 < D.gn.size() && i < p0->L.size()) {
+      info->smoother_kernel[i] = fdm_kernel_choice(p0->L[i]);
+      info->smoother_mt[i] = p0->L[i].fdm ? p0->L[i].f_mt : 0;
     }
   }
   info->coarse_n = D.coarse->C.nc;

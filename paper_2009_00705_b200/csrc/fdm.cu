@@ -1001,11 +1001,8 @@ static void fdm_cta_launch(sem_ctx* c, const DeviceLevel& L, const double* r, do
   const int ldz0 = 8 * L.f_nv_max, ldz = ldz0 + ((4 - ldz0 % 8) + 8) % 8;
   const int ldb = std::max(L.f_ldr, ldz);
   const int smem = (8 * MT * (8 * MT + 4) + 2 * 8 * MT * ldb) * (int)sizeof(double);
-  static int attr = 0;
-  if (smem > attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_fdm_cta<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = smem;
-  }
+  static int attr[kMaxDev] = {0};
+  smem_opt_in(k_fdm_cta<MT>, smem, attr);
   k_fdm_cta<MT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_cidx, L.f_Sh, L.f_lh, L.f_Svp, L.f_lvp, L.W, r, u,
                                                        transpose, ldb, L.f_skip, L.f_udesc);
   CUDA_CHECK(cudaGetLastError());
@@ -1023,11 +1020,8 @@ static bool fdm_cta_enabled() {
 template <int MT, int NVT>
 static void fdm_warp_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
   const int smem = (8 * MT * (8 * MT + 4) + 8 * MT * L.f_ldr) * (int)sizeof(double);
-  static int attr = 0;
-  if (smem > attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_fdm_warp<MT, NVT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = smem;
-  }
+  static int attr[kMaxDev] = {0};
+  smem_opt_in(k_fdm_warp<MT, NVT>, smem, attr);
   k_fdm_warp<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
                                                              L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
                                                              L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_ldr,
@@ -1057,11 +1051,8 @@ static void fdm_col_launch(sem_ctx* c, const DeviceLevel& L, const double* r, do
       throw SemError(SEM_ECUDA, std::string("error pending before the FDM sweep: ") + cudaGetErrorString(pending));
   }
   const int smem = 2 * 8 * MT * FDM_LD * (int)sizeof(double);
-  static int attr = 0;  // opt in whenever the request grows (static smem counts against the 48 KB default)
-  if (smem > attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_fdm_col<MT, NVT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = smem;
-  }
+  static int attr[kMaxDev] = {0};
+  smem_opt_in(k_fdm_col<MT, NVT>, smem, attr);
   k_fdm_col<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
                                                             L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
                                                             L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_skip);
@@ -1099,12 +1090,25 @@ static int fdm_simple() {
   return v;
 }
 
+// Which FDM sweep kernel a level runs (sem_info.smoother_kernel; the dispatch below)
+int fdm_kernel_choice(const DeviceLevel& L) {
+  if (!L.fdm) return SEM_SMOOTHER_DENSE;
+  if (!fdm_simple() && L.f_warp) {
+    if (L.f_nvt == 1) return SEM_SMOOTHER_FDM_WARP1;
+    if (fdm_cta_enabled() && L.f_mt >= 5) return SEM_SMOOTHER_FDM_CTA;  // p >= 6: CTA-shared horizontal transforms
+    return SEM_SMOOTHER_FDM_WARP2;
+  }
+  if (!fdm_simple() && L.f_mt <= 16 && L.f_nvt <= 3) return SEM_SMOOTHER_FDM_COL;
+  return SEM_SMOOTHER_FDM_GENERIC;
+}
+
 void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose) {
   const DeviceLevel& L = c->L[level];
   if (c->E_own == 0) return;
-  if (!fdm_simple() && L.f_warp) {
-    if (L.f_nvt == 1) fdm_warp_dispatch<1>(c, L, r, u, transpose);
-    else if (fdm_cta_enabled() && L.f_mt >= 5) {  // p >= 6: CTA-shared horizontal transforms
+  const int kind = fdm_kernel_choice(L);
+  if (kind == SEM_SMOOTHER_FDM_WARP1 || kind == SEM_SMOOTHER_FDM_WARP2 || kind == SEM_SMOOTHER_FDM_CTA) {
+    if (kind == SEM_SMOOTHER_FDM_WARP1) fdm_warp_dispatch<1>(c, L, r, u, transpose);
+    else if (kind == SEM_SMOOTHER_FDM_CTA) {
       switch (L.f_mt) {
         case 5: fdm_cta_launch<5>(c, L, r, u, transpose); break;
         case 6: fdm_cta_launch<6>(c, L, r, u, transpose); break;
@@ -1115,7 +1119,7 @@ void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose
     c->launches++;
     return;
   }
-  if (!fdm_simple() && L.f_mt <= 16 && L.f_nvt <= 3) {
+  if (kind == SEM_SMOOTHER_FDM_COL) {
     if (L.f_nvt == 1) fdm_col_dispatch<1>(c, L, r, u, transpose);
     else if (L.f_nvt == 2) fdm_col_dispatch<2>(c, L, r, u, transpose);
     else fdm_col_dispatch<3>(c, L, r, u, transpose);
@@ -1124,11 +1128,8 @@ void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose
   }
   const int box = L.f_nh_max * L.f_nv_max;
   const int smem = (2 * box + L.f_nv_max * L.f_nv_max) * (int)sizeof(double);
-  static int attr = 0;
-  if (smem > attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_fdm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = smem;
-  }
+  static int attr[kMaxDev] = {0};
+  smem_opt_in(k_fdm, smem, attr);
   k_fdm<<<c->E_own, 256, smem, c->stream>>>(L.f_col, L.f_hoff, L.f_moff, L.f_nv, L.f_voff, L.f_lvoff, L.f_ioff,
                                             L.f_idx, L.f_Sh, L.f_lh, L.f_Sv, L.f_lv, L.W, r, u, transpose, box,
                                             L.f_skip);

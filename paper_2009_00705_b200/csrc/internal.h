@@ -26,6 +26,39 @@ struct SemError : std::runtime_error {
                             std::string(#x) + ": " + cudaGetErrorString(_e));                  \
   } while (0)
 
+// per-device caches of kernel attributes (dynamic shared-memory opt-in, grid size):
+// cudaFuncSetAttribute acts on the current device only
+constexpr int kMaxDev = 64;
+
+// Every C-ABI entry point that touches the device switches to the ctx's device and
+// restores the caller's current device on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = -1;
+    if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDev) ? d : 0;
+}
+
+// opt a kernel in to `smem` bytes of dynamic shared memory on the current device
+template <class F>
+inline void smem_opt_in(F* f, int smem, int (&cache)[kMaxDev]) {
+  const int d = cur_device();
+  if (smem > cache[d]) {
+    CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cache[d] = smem;
+  }
+}
+
 // apply-kernel flags
 enum : int {
   AP_GATHER_ALL = 1,   // read u on Dirichlet nodes too (else treated as 0)
@@ -147,6 +180,7 @@ struct sem_ctx {
   int64_t launches = 0;
   int64_t device_bytes = 0;
   double setup_ms = 0.0;
+  double t_apply_ms = 0.0;      // one finest-level operator apply (timed at setup; work units)
   std::vector<void*> allocs;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // CUDA graphs of the V-cycle (PCG's z = V(r) with the ctx's own buffers; single domain, dense coarse)
@@ -168,6 +202,7 @@ void build_p1_matrices(sem_ctx* c, int level, const double* d_D);
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);
 void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose);
 void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose);
+int fdm_kernel_choice(const DeviceLevel& L);
 void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc);
 void launch_prolong(sem_ctx* c, int level, const double* uc, double* uf);
 void launch_coarse(sem_ctx* c, const double* r, double* z);

@@ -187,11 +187,8 @@ __global__ void __launch_bounds__(256) k_apply(int E, const int32_t* __restrict_
 template <int P>
 static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags) {
   using D = AD<P>;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_apply<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
-    attr = true;
-  }
+  static int attr[kMaxDev] = {0};
+  smem_opt_in(k_apply<P>, D::SMEM, attr);
   if (c->E_own == 0) return;
   const int grid = (c->E_own + D::NE - 1) / D::NE;
   k_apply<P><<<grid, D::T, D::SMEM, c->stream>>>(c->E_own, L.conn, L.G, L.mats, u, y, flags);
@@ -454,20 +451,14 @@ void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int trans
   }
   const int npad = 16 * L.max_tiles_1d;
   const int smem = 9 * npad * (int)sizeof(double);
-  static int attr_set = 0, attr_set32 = 0;
+  static int attr_set[kMaxDev] = {0}, attr_set32[kMaxDev] = {0};
   if (L.nsub == 0) return;
   if (L.tiles32) {  // mixed precision: FP32 storage of the exact inverses, FP64 arithmetic
-    if (smem > 48 * 1024 && smem > attr_set32) {
-      CUDA_CHECK(cudaFuncSetAttribute(k_schwarz<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr_set32 = smem;
-    }
+    if (smem > 48 * 1024) smem_opt_in(k_schwarz<float>, smem, attr_set32);
     k_schwarz<float><<<L.nsub, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles32, L.W, r, u,
                                                          transpose, npad);
   } else {
-    if (smem > 48 * 1024 && smem > attr_set) {
-      CUDA_CHECK(cudaFuncSetAttribute(k_schwarz<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr_set = smem;
-    }
+    if (smem > 48 * 1024) smem_opt_in(k_schwarz<double>, smem, attr_set);
     k_schwarz<double><<<L.nsub, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u,
                                                           transpose, npad);
   }

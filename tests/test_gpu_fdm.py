@@ -8,9 +8,11 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from oracle import pmg, sem  # noqa: E402
-from tests.test_gpu_parity import Case, SOLVE_TOL, STEP_TOL, rel  # noqa: E402
+from oracle import fdm, pmg, sem  # noqa: E402
+from tests._mapping import lib_to_oracle, streamed_apply_lib  # noqa: E402
+from tests.test_gpu_parity import Case, SOLVE_TOL, STEP_TOL, make_solver, rel  # noqa: E402
 from workloads import config1, config2, random_vector  # noqa: E402
+from workloads.configs import delaunay_basin  # noqa: E402
 
 if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
@@ -29,7 +31,14 @@ CASES = {
     "c2_o0": lambda: (config2(p=4, nx=32, ny=2, nz=3), 0),
     "c5r": lambda: (_c5_replica(), 1),            # hull: FDM / exact-dense hybrid (reading O35)
     "c2p6": lambda: (config2(p=6, nx=24, ny=2, nz=2), 1),   # n_v = 9: two n-tiles per box
+    # unstructured p = 6 (random Delaunay, 48 triangles x 3 layers): two patches of n_h = 57 > 56, so
+    # ceil(n_h / 8) = 8 and the level-0 sweep runs k_fdm_cta<8> (config 5's level-0 kernel)
+    "d6cta8": lambda: (_d6(), 1),
 }
+
+
+def _d6():
+    return delaunay_basin("fdm_cta8", 6, n_in=16, nz=3, seed=1)
 
 
 def _c5_replica():
@@ -107,3 +116,68 @@ def test_config5_replica_dense_smoother_solve():
     out = np.zeros(lev.n)
     out[perm] = phi.cpu().numpy()
     assert rep["converged"] and rel(out, sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+
+
+def test_d6_runs_fdm_cta8():
+    """The d6cta8 case above provably exercises k_fdm_cta<8> on level 0."""
+    s = make_solver(_d6(), local_solve=1)
+    assert s.info["smoother_kernel"][0] == "k_fdm_cta<MT>" and s.info["smoother_mt"][0] == 8
+    s.close()
+
+
+def test_fdm_cta8_on_p6_hull_replica():
+    """Config-5 construction at p = 6 (hull 8 x 2 x 0.6 in a 10 x 4 basin, spacing
+    0.5 / 1 / 2: 6,240 prisms, 692,779 DOF) whose level-0 FDM sweep runs
+    k_fdm_cta<8> (largest patch n_h = 58).  The oracle cannot hold every local
+    inverse of this mesh, so the residual r is supported on the free nodes of the
+    column with the largest regular patch: only the subdomains meeting that
+    support contribute, and the oracle sums exactly those (eq 4.4 with W of
+    eq 4.6 from every subdomain's set, readings O33, O35).  Every entry of the
+    library's correction is compared.  Then the solve: the oracle residual of the
+    library's solution (to 1e-12) over every row, by the streamed oracle apply."""
+    from workloads.config5 import config5
+    m = config5(p=6, hf=0.5, Lx=10.0, Ly=4.0)
+    s = make_solver(m, local_solve=1)
+    assert s.info["smoother_kernel"][0] == "k_fdm_cta<MT>" and s.info["smoother_mt"][0] == 8
+    lev = sem.build_level(m, 6)
+    xyz = s.node_xyz(0)
+    perm = lib_to_oracle(xyz, lev.xyz, tol=1e-9)
+    cols = fdm.Columns(m, lev)
+    reg = fdm.regular(cols, 1)
+    sets, _ = pmg.hybrid_sets(m, lev, 1)
+    cnt = np.zeros(lev.n)
+    for I in sets:
+        cnt[I] += 1.0
+    W = np.where(lev.dirichlet, 0.0, 1.0 / np.maximum(cnt, 1.0))
+    ncol = cols.tri_h.shape[0]
+    regcol = np.zeros(ncol, dtype=bool)
+    regcol[cols.col[reg]] = True
+    nh = np.array([len(cols.patch(c, 1)) if regcol[c] else 0 for c in range(ncol)])
+    cstar = int(np.argmax(nh))
+    assert nh[cstar] > 56
+    supp = np.unique(lev.conn[cols.col_elems[cstar]])
+    supp = supp[~lev.dirichlet[supp]]
+    r = np.zeros(lev.n)
+    r[supp] = np.random.default_rng(61).uniform(-1, 1, len(supp))
+    touched = [k for k, I in enumerate(sets) if np.intersect1d(I, supp, assume_unique=True).size]
+    assert reg[touched].all() and len(touched) >= 3
+    blocks = fdm.fdm_blocks(m, lev, 1, cols, elems=touched)
+    for tr in (False, True):
+        rr = W * r if tr else r
+        z = np.zeros(lev.n)
+        for ids, Binv in blocks:
+            z[ids] += Binv @ rr[ids]
+        zo = z if tr else W * z
+        u = s.empty(0)
+        s.schwarz(0, torch.from_numpy(np.ascontiguousarray(r[perm])).cuda(), u, transpose=tr)
+        got = np.zeros(lev.n)
+        got[perm] = u.cpu().numpy()
+        assert rel(got, zo) <= STEP_TOL
+    # solve: oracle residual of the library solution over every row
+    phiD = m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])
+    phi, rep = s.solve(torch.from_numpy(phiD).cuda(), tol=1e-12)
+    assert rep["converged"]
+    dm = s.dirichlet_mask(0)
+    Y = streamed_apply_lib(m, 6, xyz, np.stack([phi.cpu().numpy(), np.where(dm, phiD, 0.0)], axis=1))
+    assert np.linalg.norm(Y[~dm, 0]) <= 1e-11 * np.linalg.norm(Y[~dm, 1])
+    s.close()

@@ -7,7 +7,16 @@ vertices (every prism holding the vertex), with the element vectors gathered
 from the library's vector by node coordinates.  Properties that hold at any
 size are checked on the whole vectors: A 1 = 0, <x, A y> = <A x, y>,
 <x, V y> = <V x, y>, R = P^T.  The full-size solve is checked row by row:
-its oracle residual at sampled free rows vanishes against the row's scale."""
+its oracle residual at sampled free rows vanishes against the row's scale.
+
+Whole vectors (SURVEY §8(c) parity protocol, steps 5(a)-(b)): the oracle's
+streamed element apply (oracle/sem.py apply_streamed: y_e = D^T (G (.) D u_e)
+with the oracle's own geometry, element matrices never formed) over EVERY
+element, in a process pool over the host cores, gives A u at every row -- the
+library's apply must match it to rel-L2 <= 1e-12 -- and the oracle residual
+of the library's full-size solution: ||(A phi)_F|| / ||(A phi_D0)_F|| (phi_D0 =
+the Dirichlet data, 0 elsewhere; rhs = 0, so b_F = -(A phi_D0)_F) <= 1e-11 for
+a solve to 1e-12."""
 import numpy as np
 import pytest
 from scipy.spatial import cKDTree
@@ -17,6 +26,7 @@ pytestmark = pytest.mark.gpu
 
 import paper_2009_00705_b200 as lib  # noqa: E402
 from oracle import refelem as R, sem  # noqa: E402
+from tests._mapping import streamed_apply_lib  # noqa: E402
 from tests.test_gpu_parity import make_solver  # noqa: E402
 from workloads import config3, random_vector  # noqa: E402
 
@@ -148,45 +158,72 @@ def test_full_config3_solution_rows(c3full):
     assert np.max(np.abs(res) / scale) <= 1e-9
 
 
-def test_full_config5_apply_and_properties():
-    """Config 5 at full size (52.8 M DOF; FDM/dense hybrid smoother, as bench.py
-    --config config5 runs it): sampled interior rows of the apply vs the oracle,
-    A 1 = 0 and symmetry on the whole vectors, V-cycle symmetry."""
+def _whole_vector_checks(F, u, seed_sol_tol=1e-12):
+    """Library apply of u vs the oracle's streamed apply at every row; library
+    solve to rel. residual 1e-12 and the oracle residual of its solution."""
+    s = F.s
+    n = s.n_dof(0)
+    y = s.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    phiD = F.m.phi(F.xyz[:, 0], F.xyz[:, 1], F.xyz[:, 2])
+    phi, rep = s.solve(torch.from_numpy(phiD).cuda(), tol=seed_sol_tol)
+    assert rep["converged"] and rep["rel_res"] <= seed_sol_tol
+    ph = phi.cpu().numpy()
+    dm = s.dirichlet_mask(0)
+    np.testing.assert_array_equal(ph[dm], phiD[dm])
+    phiD0 = np.where(dm, phiD, 0.0)
+    Y = streamed_apply_lib(F.m, F.p, F.xyz, np.stack([u, ph, phiD0], axis=1), tree=F.tree)
+    err = np.linalg.norm(y - Y[:, 0]) / np.linalg.norm(Y[:, 0])
+    assert err <= 1e-12, err
+    free = ~dm
+    res = np.linalg.norm(Y[free, 1]) / np.linalg.norm(Y[free, 2])
+    assert res <= 1e-11, res
+    return err, res
+
+
+def test_full_config3_whole_vector_apply_and_solution_residual(c3full):
+    """Config 3 at full size (4.2 M DOF, bench.py's headline configuration): the
+    library's A u equals the oracle's streamed apply at all 4,224,681 rows, and
+    the oracle residual of the library's solution (solved to 1e-12) is <= 1e-11."""
+    _whole_vector_checks(c3full, random_vector(c3full.s.n_dof(0), seed=13))
+
+
+def test_full_config5_whole_vector_apply_and_solution_residual():
+    """Config 5 at full size (52.8 M DOF, 477,600 prisms, p = 6; FDM / exact-dense
+    hybrid smoother as bench.py runs it): A u vs the oracle's streamed apply at
+    every row; the oracle residual of the library's solution; A 1 = 0; V-cycle
+    symmetry (its P=1 problem is solved iteratively to 1e-10, reading O9)."""
     from workloads.config5 import config5
     F = Full(config5(), local_solve=1)
     s = F.s
     n = s.n_dof(0)
+    assert s.info["smoother_kernel"][0] == "k_fdm_cta<MT>"
     u = random_vector(n, seed=21)
-    y = s.apply(torch.from_numpy(u).cuda()).cpu().numpy()
-    rng = np.random.default_rng(1)
-    el = np.sort(rng.choice(F.m.n_elem, 100, replace=False))
-    ids = F.elem_ids(el)
-    Ae = F.elem_mats(el)
-    inner = _interior_locals(F.p)
-    yo = np.einsum("eij,ej->ei", Ae, u[ids])[:, inner].ravel()
-    assert np.linalg.norm(y[ids[:, inner]].ravel() - yo) <= 1e-12 * np.linalg.norm(yo)
+    _whole_vector_checks(F, u)
     one = torch.ones(n, dtype=torch.float64, device="cuda")
-    assert s.apply(one).abs().max().item() <= 1e-11 * np.abs(y).max()
+    ymax = s.apply(torch.from_numpy(u).cuda()).abs().max().item()
+    assert s.apply(one).abs().max().item() <= 1e-11 * ymax
     x = torch.from_numpy(random_vector(n, 7)).cuda()
     dm = torch.from_numpy(s.dirichlet_mask(0)).cuda()
     x[dm] = 0
     z = torch.from_numpy(random_vector(n, 8)).cuda()
     z[dm] = 0
     vx, vz = s.vcycle(x), s.vcycle(z)
-    # the P=1 problem (243,654 free DOF) is solved iteratively to 1e-10 (reading O9): symmetric to that level
     assert abs((x @ vz).item() - (vx @ z).item()) <= 1e-9 * x.norm().item() * vz.norm().item()
     s.close()
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("p", [8])
-def test_full_config4_apply_rows(p):
+def test_full_config4_whole_vector(p):
     """Config 4 at full size (~11.5 M DOF, p = 8: the CTA-batched DMMA kernel) with
-    the FDM smoother of the sweep: sampled interior rows and A 1 = 0."""
+    the FDM smoother of the sweep: A u vs the oracle's streamed apply at every
+    row, the oracle residual of the solution, sampled element rows, A 1 = 0."""
     from workloads import config4
     F = Full(config4(p), local_solve=1)
     s = F.s
     n = s.n_dof(0)
     u = random_vector(n, seed=31)
+    _whole_vector_checks(F, u)
     y = s.apply(torch.from_numpy(u).cuda()).cpu().numpy()
     rng = np.random.default_rng(2)
     el = np.sort(rng.choice(F.m.n_elem, 60, replace=False))

@@ -329,3 +329,43 @@ def test_mixed_precision_storage(c2):
     phi, rep = s.solve(c2.to_lib(0, phiD), tol=1e-13)
     assert rep["converged"]
     assert rel(c2.to_orc(0, phi), sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+
+
+@pytest.mark.parametrize("levels", [(6, 3, 1), (5, 3, 1)])
+def test_explicit_level_tables(levels):
+    """Explicit coarsening tables through opts.levels: 6 -> 3 -> 1 (Table 5.1,
+    P:391) and 5 -> 3 -> 1 (Table 5.4 with P_xy = P_z): the library's
+    hierarchy is the requested one; V-cycle, solve and iteration count match the
+    oracle built on the same schedule."""
+    p = levels[0]
+    m = config2(p=6, nx=12, ny=2, nz=2) if p == 6 else _c3_small()
+    C = Case(m, levels=list(levels))
+    assert C.s.info["level_p"] == list(levels)
+    nF = C.mg.levels[0].A.shape[0]
+    r = random_vector(nF, seed=19)
+    assert rel(C.lib_to_free(0, C.s.vcycle(C.free_to_lib(0, r))), C.mg.vcycle(r)) <= STEP_TOL
+    lev, perm = C.levels[0]
+    phiD = m.phi(*lev.xyz.T)
+    phi, rep = C.s.solve(C.to_lib(0, phiD), tol=1e-13)
+    assert rep["converged"] and rel(C.to_orc(0, phi), sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+    A, b = sem.dirichlet_lift(lev, phiD)
+    _, info = pmg.pcg(C.mg, b, rtol=1e-13)
+    assert abs(rep["iters"] - info["iters"]) <= 1
+
+
+def test_standalone_mg_outer2(c1):
+    """outer = 2: the V-cycle of Alg 4.1 iterated as the solver, u <- u + V(b - A u)
+    (the same stationary iteration as PDC with the MG preconditioner, Alg 4.2):
+    reaches the sparse-direct solution; iteration count = the oracle's PDC's."""
+    m = c1.m
+    s = make_solver(m, outer=2)
+    lev, perm = c1.levels[0]
+    phiD = m.phi(*lev.xyz.T)
+    phi, rep = s.solve(torch.from_numpy(phiD[perm]).cuda(), tol=1e-12)
+    out = np.zeros(lev.n)
+    out[perm] = phi.cpu().numpy()
+    assert rep["converged"] and rel(out, sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+    A, b = sem.dirichlet_lift(lev, phiD)
+    _, info = pmg.pdc(c1.mg, b, rtol=1e-12)
+    assert abs(rep["iters"] - info["iters"]) <= 1 and rep["vcycles"] == rep["iters"]
+    assert rep["wu"] > 0

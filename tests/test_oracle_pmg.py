@@ -162,3 +162,35 @@ def test_overlap_improves_contraction():
         rho.append(nx_)
     assert rho[0] > rho[1] > rho[2], rho
     assert rho[1] < 0.2
+
+
+def test_smoother_matches_dense_formula_eq44():
+    """eq 4.4 written out densely: S^{-1} = W sum_k R_k^T (R_k A R_k^T)^{-1} R_k
+    with explicit 0/1 restriction matrices on a two-prism mesh (overlap 0: R_k picks
+    element k's free nodes, read off its connectivity), W = (sum_k R_k R_k^T)^{-1}
+    non-constant (1/2 on the shared face).  Smoother.apply must be W on the LEFT
+    for S^{-1} and on the RIGHT for S^{-T} (reading O14); swapping them fails,
+    since the dense S^{-1} is not symmetric here."""
+    m = config1(p=2, nx=1, ny=1, nz=1)             # one quad -> 2 triangles x 1 layer = 2 prisms
+    lev = sem.build_system(m, 2)
+    F = lev.free
+    nF = len(F)
+    fid = -np.ones(lev.n, dtype=np.int64)
+    fid[F] = np.arange(nF)
+    AFF = lev.A[F][:, F].toarray()
+    Rk = []
+    for e in range(lev.conn.shape[0]):
+        nodes = sorted({int(fid[g]) for g in lev.conn[e] if fid[g] >= 0})
+        R_ = np.zeros((len(nodes), nF))
+        R_[np.arange(len(nodes)), nodes] = 1.0
+        Rk.append(R_)
+    W = np.diag(1.0 / sum(R_.T @ R_ for R_ in Rk).diagonal())
+    assert len(set(np.round(W.diagonal(), 12))) == 2     # 1 and 1/2: non-constant
+    Ssum = sum(R_.T @ np.linalg.inv(R_ @ AFF @ R_.T) @ R_ for R_ in Rk)
+    S_inv = W @ Ssum
+    assert np.linalg.norm(S_inv - S_inv.T) > 1e-3 * np.linalg.norm(S_inv)
+    sm = pmg.build_smoother(lev, lev.A[F][:, F].tocsr(), overlap=0)
+    r = np.random.default_rng(12).uniform(-1, 1, nF)
+    np.testing.assert_allclose(sm.apply(r), S_inv @ r, rtol=1e-12, atol=1e-12 * np.abs(S_inv @ r).max())
+    np.testing.assert_allclose(sm.apply(r, transpose=True), S_inv.T @ r, rtol=1e-12,
+                               atol=1e-12 * np.abs(S_inv.T @ r).max())

@@ -242,6 +242,58 @@ def config4(p: int, scale: float = 1.0, seed: int = 4) -> PrismMesh:
     return basin(f"config4_p{p}", p, 32.0, n, nz, seed)
 
 
+def delaunay_basin(name, p, Lx=2.0, Ly=1.0, n_in=24, n_bx=6, n_by=3, nz=2, seed=0, amp=0.03) -> PrismMesh:
+    """Small unstructured layered basin: Delaunay triangulation (scipy.spatial.Delaunay)
+    of n_in uniform random interior points plus evenly spaced boundary points, nz
+    sigma-layers under eta = amp cos(pi x / Lx) cos(pi y / Ly) (walls: homogeneous
+    Neumann, exact for the standing-wave phi below; free surface Dirichlet).  Random
+    Delaunay meshes have high-valence vertices, hence larger Schwarz patches than the
+    structured configs (used to reach the n_h > 56 FDM kernel on a small mesh).
+    Draw order: interior points (n_in, 2)."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(seed)
+    pin = rng.uniform(0.05, 0.95, size=(n_in, 2)) * np.array([Lx, Ly])
+    xs = np.linspace(0.0, Lx, n_bx + 1)
+    ys = np.linspace(0.0, Ly, n_by + 1)
+    bnd = [(x, 0.0) for x in xs] + [(x, Ly) for x in xs] + [(0.0, y) for y in ys[1:-1]] + [(Lx, y) for y in ys[1:-1]]
+    vert2d = np.concatenate([np.asarray(bnd), pin])
+    tri = Delaunay(vert2d).simplices.astype(np.int32)
+    a = vert2d[tri]
+    area = 0.5 * ((a[:, 1, 0] - a[:, 0, 0]) * (a[:, 2, 1] - a[:, 0, 1]) - (a[:, 2, 0] - a[:, 0, 0]) * (a[:, 1, 1] - a[:, 0, 1]))
+    tri[area < 0] = tri[area < 0][:, [0, 2, 1]]
+    eps = 1e-12
+    btag = np.zeros(tri.shape, dtype=bool)
+    for f, (i, j) in enumerate([(0, 1), (1, 2), (2, 0)]):
+        A, B = vert2d[tri[:, i]], vert2d[tri[:, j]]
+        for c, L in ((0, Lx), (1, Ly)):
+            for val in (0.0, L):
+                btag[:, f] |= (np.abs(A[:, c] - val) < eps) & (np.abs(B[:, c] - val) < eps)
+    h = 1.0
+    kx, ky = math.pi / Lx, math.pi / Ly
+    k = math.hypot(kx, ky)
+    om = math.sqrt(G_ACC * k * math.tanh(k * h))
+    eta = lambda x, y: amp * np.cos(kx * x) * np.cos(ky * y)
+    phi = lambda x, y, z: (G_ACC * amp / om) * np.cosh(k * (z + h)) / math.cosh(k * h) * np.cos(kx * x) * np.cos(ky * y)
+    nv2, T = vert2d.shape[0], tri.shape[0]
+    sig = np.arange(nz + 1) / nz
+    zv = -h + sig[:, None] * (eta(vert2d[:, 0], vert2d[:, 1])[None, :] + h)
+    vertices = np.empty(((nz + 1) * nv2, 3))
+    vertices[:, 0] = np.tile(vert2d[:, 0], nz + 1)
+    vertices[:, 1] = np.tile(vert2d[:, 1], nz + 1)
+    vertices[:, 2] = zv.ravel()
+    t_idx = np.repeat(np.arange(T), nz)
+    s_idx = np.tile(np.arange(nz), T)
+    prisms = np.empty((T * nz, 6), dtype=np.int32)
+    prisms[:, 0:3] = tri[t_idx] + (s_idx * nv2)[:, None]
+    prisms[:, 3:6] = tri[t_idx] + ((s_idx + 1) * nv2)[:, None]
+    face_tag = np.zeros((T * nz, 5), dtype=np.uint8)
+    face_tag[:, 0] = np.where(s_idx == 0, 2, 0)
+    face_tag[:, 1] = np.where(s_idx == nz - 1, 1, 0)
+    face_tag[:, 2:5] = np.where(btag[t_idx], 2, 0)
+    return PrismMesh(name=name, p=p, vertices=vertices, prisms=prisms, face_tag=face_tag, vert2d=vert2d, tri=tri,
+                     nz=nz, h=h, eta=eta, phi=phi, meta=dict(seed=seed, n_in=n_in, Lx=Lx, Ly=Ly, nz=nz))
+
+
 def random_vector(n: int, seed: int) -> np.ndarray:
     """u ~ U(-1,1) (no cancellation, SURVEY §8(c) parity protocol)."""
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
