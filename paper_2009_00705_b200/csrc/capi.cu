@@ -211,15 +211,18 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
     c->C.q = dalloc<double>(c, L.n);
     CUDA_CHECK(cudaMemsetAsync(c->C.dinv, 0, sizeof(double) * L.n, c->stream));
     Scratch sc;
+    double* off = sc.get<double>((size_t)L.n);   // A[i][node above i] (vertical edges)
+    CUDA_CHECK(cudaMemsetAsync(off, 0, sizeof(double) * L.n, c->stream));
     const int64_t chunk = std::min<int64_t>(E, 1 << 20);
     double* Ae = sc.get<double>((size_t)chunk * L.N * L.N);
     for (int64_t e0 = 0; e0 < E; e0 += chunk) {
       const int ne = (int)std::min<int64_t>(chunk, E - e0);
       launch_elem_matrices(c, (int)c->L.size() - 1, d_D, Ae, (int)e0, ne);
       launch_diag_accum_range(c, L.conn + (size_t)e0 * L.N, L.N, ne, Ae, c->C.dinv);
+      launch_offdiag_accum(c, L.conn + (size_t)e0 * L.N, ne, Ae, off);
     }
-    launch_invert_masked(c, (int)c->L.size() - 1, c->C.dinv);
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    setup_coarse_lines(c, topo.conn, topo.dir, c->C.dinv, off);
     return;
   }
   c->C.nc = nc;
@@ -574,43 +577,6 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
 
 void read_scalars(sem_ctx* c, int n);
 
-// ------------------------------------------------------------------ iterative coarse solve
-// x = A_1^-1 b on the free nodes of the coarsest level by Jacobi-preconditioned CG
-// from x = 0 to ||r|| <= coarse_rtol ||b|| (reading O9).  Convergence is checked
-// every 8 iterations (one host sync each).
-void coarse_pcg(sem_ctx* c, const double* b, double* x) {
-  const int li = (int)c->L.size() - 1;
-  const DeviceLevel& L = c->L[li];
-  Coarse& C = c->C;
-  const int64_t n = L.n;
-  double* s = c->scal + 16;  // [0] p.q  [2] r.r  [4],[6] z.r ping-pong (+1: r.r from jacobi_dot)
-  CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
-  launch_init_masked(c, li, b, C.r, 1);
-  int dcur = 4, dnew = 6;
-  launch_jacobi_dot(c, n, C.dinv, C.r, C.z, s + dcur);
-  CUDA_CHECK(cudaMemcpyAsync(c->hscal, s + dcur, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_CHECK(cudaStreamSynchronize(c->stream));
-  const double nb = std::sqrt(c->hscal[1]);
-  if (nb == 0.0) return;
-  const double thr = c->opts.coarse_rtol * nb;
-  launch_xpby(c, n, C.p, C.z, nullptr, nullptr, 1);
-  for (int it = 1; it <= c->opts.coarse_maxit; ++it) {
-    CUDA_CHECK(cudaMemsetAsync(C.q, 0, sizeof(double) * n, c->stream));
-    launch_apply(c, li, C.p, C.q, 0);
-    launch_dot2(c, n, C.p, C.q, nullptr, nullptr, nullptr, s + 0);
-    launch_axpy_pcg(c, n, x, C.r, C.p, C.q, s + dcur, s + 0, s + 2);
-    C.iters++;
-    if ((it & 7) == 0 || it == c->opts.coarse_maxit) {
-      CUDA_CHECK(cudaMemcpyAsync(c->hscal, s + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_CHECK(cudaStreamSynchronize(c->stream));
-      if (std::sqrt(c->hscal[0]) <= thr) return;
-    }
-    launch_jacobi_dot(c, n, C.dinv, C.r, C.z, s + dnew);
-    launch_xpby(c, n, C.p, C.z, s + dnew, s + dcur, 0);
-    std::swap(dcur, dnew);
-  }
-}
-
 void coarse_solve(sem_ctx* c, const double* f, double* u) {
   if (c->C.iterative) coarse_pcg(c, f, u);
   else launch_coarse(c, f, u);
@@ -665,7 +631,7 @@ void vcycle_pcg(sem_ctx* c, const double* r, double* z) {
     return (e && atoi(e)) ? 1 : 0;
   }();
   const int slot = (z == c->pw) ? 0 : ((z == c->zw) ? 1 : -1);
-  if (off || c->C.iterative || slot < 0 || r != c->bw || c->vc_eager < 1) {
+  if (off || slot < 0 || r != c->bw || c->vc_eager < 1) {
     vcycle(c, 0, r, z);
     c->vc_eager++;
     return;
@@ -712,7 +678,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   const int64_t n = L.n;
   sem_report R;
   memset(&R, 0, sizeof(R));
-  c->C.iters = 0;
+  coarse_reset_iters(c);
   CUDA_CHECK(cudaEventRecord(c->ev0, c->stream));
   double* u = c->xw;   // free-node iterate
   double* r = c->bw;   // residual
@@ -812,7 +778,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   CUDA_CHECK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   R.t_ms = ms;
   R.wu = c->t_apply_ms > 0 ? ms / c->t_apply_ms : 0.0;
-  R.coarse_iters = (int)c->C.iters;
+  R.coarse_iters = (int)coarse_iters(c, false);
   R.rel_res = nf > 0 ? rn / nf : 0.0;
   if (R.n_hist > 1) {
     const int m = R.n_hist - 1;
@@ -1179,6 +1145,7 @@ void sem_destroy(sem_ctx* c) {
   dist_destroy(c);
   for (int i = 0; i < 2; ++i)
     if (c->vc_graph[i]) cudaGraphExecDestroy(c->vc_graph[i]);
+  coarse_destroy(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hscal) cudaFreeHost(c->hscal);

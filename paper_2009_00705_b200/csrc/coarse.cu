@@ -1,0 +1,341 @@
+// Iterative P=1 coarse solve ("A^-1"; reading O9): preconditioned CG on the
+// matrix-free P=1 operator to ||r|| <= coarse_rtol ||b||, for coarse problems too
+// large for the stored dense inverse.
+//
+// Preconditioner: vertical-line block Jacobi.  The P=1 nodes of a layered prism mesh
+// form vertical lines (a prism's top vertex v3+m sits above its bottom vertex v0+m);
+// the coarse operator restricted to one line is tridiagonal (the lines' own vertical
+// edges), and it carries the strong coupling of thin layers (config 4: d_xy / d_z = 4,
+// so the vertical couplings are ~16x the horizontal ones).  Each line is solved
+// exactly by the Thomas algorithm with factors precomputed at setup; on meshes whose
+// prisms do not stack consistently every line is a single node (point Jacobi).
+//
+// The whole solve runs on the device: the stop test is a CUDA-graph WHILE node whose
+// condition a one-thread kernel sets after every iteration, so no host round trip
+// happens inside the solve and the V-cycle that contains it can itself be captured
+// and replayed from a CUDA graph (capi.cu vcycle_pcg).  Outside a capture the solve
+// is replayed from a cached graph of its own.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+#include "setup_util.h"
+
+namespace sem {
+
+// device scalar slots of the coarse solve (C.cs)
+enum : int { CS_PQ = 0, CS_RR = 1, CS_ZR_OLD = 2, CS_ZR_NEW = 3, CS_RR0 = 4, CS_RR_DUP = 5, CS_THR2 = 6, CS_IT = 7,
+             CS_TOTAL = 8, CS_N = 16 };
+
+static int cgrid(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)std::max<int64_t>(g, 1);
+}
+
+// off[i] += A_e[m][m+3] for the vertical edge (i = bottom m, j = top m) of every P=1 prism (setup)
+__global__ void k_offdiag_accum(int64_t E, const int32_t* __restrict__ conn, const double* __restrict__ Ae,
+                                double* __restrict__ off) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= E * 3) return;
+  const int64_t e = idx / 3;
+  const int m = (int)(idx % 3);
+  const int32_t i = conn[e * 6 + m], j = conn[e * 6 + m + 3];
+  if (i >= 0 && j >= 0) atomicAdd(off + i, Ae[(e * 6 + m) * 6 + m + 3]);
+}
+
+// z = T^-1 r on every line (Thomas algorithm with precomputed factors), out[0] += z.r, out[1] += r.r
+__global__ void k_line_solve(int nlines, const int64_t* __restrict__ loff, const int32_t* __restrict__ lnode,
+                             const double* __restrict__ ta, const double* __restrict__ tinv,
+                             const double* __restrict__ tc, const double* __restrict__ r, double* __restrict__ z,
+                             double* out) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlines; l += gridDim.x * blockDim.x) {
+    const int64_t b = loff[l], e = loff[l + 1];
+    double d = 0.0;
+    for (int64_t t = b; t < e; ++t) {  // forward elimination: d'_t = (r_t - a_t d'_{t-1}) / den_t
+      d = (r[lnode[t]] - ta[t] * d) * tinv[t];
+      z[lnode[t]] = d;
+    }
+    double x = 0.0;
+    for (int64_t t = e - 1; t >= b; --t) {  // back substitution: x_t = d'_t - c'_t x_{t+1}
+      const int32_t g = lnode[t];
+      x = z[g] - tc[t] * x;
+      z[g] = x;
+      const double rg = r[g];
+      s0 = fma(x, rg, s0);
+      s1 = fma(rg, rg, s1);
+    }
+  }
+  // block reduction + one atomic per block
+  __shared__ double sh0[32], sh1[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh0[w] = s0;
+    sh1[w] = s1;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    s0 = lane < nw ? sh0[lane] : 0.0;
+    s1 = lane < nw ? sh1[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane == 0) {
+      atomicAdd(out, s0);
+      atomicAdd(out + 1, s1);
+    }
+  }
+}
+
+__global__ void k_zero_slots(double* cs, int a, int b, int c2, int d) {
+  cs[a] = 0.0;
+  cs[b] = 0.0;
+  if (c2 >= 0) cs[c2] = 0.0;
+  if (d >= 0) cs[d] = 0.0;
+}
+
+// after the prologue: thr^2 = rtol^2 ||b||^2 (||b||^2 = r.r of the initial residual), loop iff b != 0
+__global__ void k_coarse_start(double* cs, double rtol2, cudaGraphConditionalHandle h) {
+  cs[CS_THR2] = rtol2 * cs[CS_RR_DUP];
+  cs[CS_IT] = 0.0;
+  cs[CS_ZR_OLD] = cs[CS_ZR_NEW];
+  const unsigned go = cs[CS_RR_DUP] > 0.0 ? 1u : 0u;
+  cs[CS_PQ] = 0.0;
+  cs[CS_RR] = 0.0;
+  cs[CS_ZR_NEW] = 0.0;
+  cs[CS_RR_DUP] = 0.0;
+  cudaGraphSetConditional(h, go);
+}
+
+// end of one CG iteration: beta used, shift z.r, count, stop test ||r||^2 <= thr^2 or maxit,
+// zero the reduction slots of the next iteration
+__global__ void k_coarse_next(double* cs, double maxit, cudaGraphConditionalHandle h) {
+  const double rr = cs[CS_RR];
+  cs[CS_ZR_OLD] = cs[CS_ZR_NEW];
+  cs[CS_IT] += 1.0;
+  cs[CS_TOTAL] += 1.0;
+  const unsigned go = (rr > cs[CS_THR2] && cs[CS_IT] < maxit) ? 1u : 0u;
+  cs[CS_PQ] = 0.0;
+  cs[CS_RR] = 0.0;
+  cs[CS_ZR_NEW] = 0.0;
+  cs[CS_RR_DUP] = 0.0;
+  cudaGraphSetConditional(h, go);
+}
+
+static void line_solve(sem_ctx* c, const double* r, double* z, double* out2) {
+  Coarse& C = c->C;
+  k_line_solve<<<cgrid(C.nlines, 128), 128, 0, c->stream>>>(C.nlines, C.loff, C.lnode, C.ta, C.tinv, C.tc, r, z,
+                                                             out2);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// ---------------------------------------------------------------- setup
+// Lines of the P=1 level (host) and their Thomas factors from the assembled diagonal and
+// vertical off-diagonals.  conn: [E][6] level ids; dir: Dirichlet mask; diag, off on the device.
+void setup_coarse_lines(sem_ctx* c, const std::vector<int32_t>& conn, const std::vector<uint8_t>& dir,
+                        const double* d_diag, const double* d_off) {
+  Coarse& C = c->C;
+  const int64_t n = (int64_t)dir.size();
+  const int64_t E = (int64_t)conn.size() / 6;
+  std::vector<int32_t> up(n, -1), down(n, -1);
+  bool consistent = true;
+  for (int64_t e = 0; e < E && consistent; ++e)
+    for (int m = 0; m < 3; ++m) {
+      const int32_t i = conn[e * 6 + m], j = conn[e * 6 + m + 3];
+      if (dir[i] || dir[j]) continue;
+      if ((up[i] >= 0 && up[i] != j) || (down[j] >= 0 && down[j] != i)) {
+        consistent = false;
+        break;
+      }
+      up[i] = j;
+      down[j] = i;
+    }
+  std::vector<double> diag(n), off(n);
+  CUDA_CHECK(cudaMemcpy(diag.data(), d_diag, n * 8, cudaMemcpyDeviceToHost));
+  CUDA_CHECK(cudaMemcpy(off.data(), d_off, n * 8, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> loff{0};
+  std::vector<int32_t> lnode;
+  std::vector<double> ta, tinv, tc;
+  lnode.reserve(n);
+  for (int64_t s = 0; s < n; ++s) {
+    if (dir[s] || (consistent && down[s] >= 0)) continue;  // line starts: free nodes with nothing below
+    double cprev = 0.0, aprev = 0.0;
+    int64_t t0 = (int64_t)lnode.size();
+    for (int32_t g = (int32_t)s; g >= 0; g = consistent ? up[g] : -1) {
+      const bool first = (int64_t)lnode.size() == t0;
+      const double a = first ? 0.0 : aprev;               // A[g][below]
+      const double den = diag[g] - a * cprev;
+      if (!(den > 0.0)) throw SemError(SEM_ESINGULAR, "coarse line block is not SPD");
+      const int32_t nx = consistent ? up[g] : -1;
+      const double cg = nx >= 0 ? off[g] : 0.0;            // A[g][above]
+      lnode.push_back(g);
+      ta.push_back(a);
+      tinv.push_back(1.0 / den);
+      tc.push_back(cg / den);
+      cprev = cg / den;
+      aprev = cg;
+    }
+    loff.push_back((int64_t)lnode.size());
+  }
+  int64_t nfree = 0;
+  for (int64_t i = 0; i < n; ++i) nfree += !dir[i];
+  if ((int64_t)lnode.size() != nfree) throw SemError(SEM_EINVAL, "coarse lines do not cover the free nodes");
+  C.nlines = (int)(loff.size() - 1);
+  C.line_max = 0;
+  for (int l = 0; l < C.nlines; ++l) C.line_max = std::max<int64_t>(C.line_max, loff[l + 1] - loff[l]);
+  C.loff = upload(c, loff);
+  C.lnode = upload(c, lnode);
+  C.ta = upload(c, ta);
+  C.tinv = upload(c, tinv);
+  C.tc = upload(c, tc);
+  C.cs = dalloc<double>(c, CS_N);
+  CUDA_CHECK(cudaMemset(C.cs, 0, CS_N * sizeof(double)));
+  CUDA_CHECK(cudaMemset(C.z, 0, n * sizeof(double)));
+}
+
+void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double* Ae, double* off) {
+  const int64_t tot = (int64_t)ne * 3;
+  k_offdiag_accum<<<(int)((tot + 255) / 256), 256, 0, c->stream>>>(ne, conn, Ae, off);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- solve
+// Enqueue the whole PCG on c->stream, which must be capturing: prologue, then a
+// conditional WHILE node whose body (one CG iteration) is captured through a
+// second stream.  x = A_1^-1 b from x = 0.
+static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
+  const int li = (int)c->L.size() - 1;
+  const DeviceLevel& L = c->L[li];
+  Coarse& C = c->C;
+  const int64_t n = L.n;
+  double* cs = C.cs;
+  // prologue: x = 0, r = b (free nodes), z = T^-1 r, p = z; ||b||^2, z.r
+  k_zero_slots<<<1, 1, 0, c->stream>>>(cs, CS_ZR_NEW, CS_RR_DUP, -1, -1);
+  launch_init_masked(c, li, nullptr, x, 1);
+  launch_init_masked(c, li, b, C.r, 1);
+  line_solve(c, C.r, C.z, cs + CS_ZR_NEW);  // [ZR_NEW] = z.r, [RR_DUP] = r.r
+  launch_xpby(c, n, C.p, C.z, nullptr, nullptr, 1);
+  cudaStreamCaptureStatus st;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CUDA_CHECK(cudaStreamGetCaptureInfo(c->stream, &st, nullptr, &graph, &deps, &ndeps));
+  if (st != cudaStreamCaptureStatusActive) throw SemError(SEM_ECUDA, "coarse PCG emitted outside a capture");
+  cudaGraphConditionalHandle h;
+  CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+  const double rt = c->opts.coarse_rtol;
+  k_coarse_start<<<1, 1, 0, c->stream>>>(cs, rt * rt, h);
+  c->launches += 2;
+  CUDA_CHECK(cudaStreamGetCaptureInfo(c->stream, &st, nullptr, &graph, &deps, &ndeps));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CUDA_CHECK(cudaGraphAddNode(&node, graph, deps, ndeps, &cp));
+  CUDA_CHECK(cudaStreamUpdateCaptureDependencies(c->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (!C.body_stream) CUDA_CHECK(cudaStreamCreateWithFlags(&C.body_stream, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(C.body_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  cudaStream_t keep = c->stream;
+  c->stream = C.body_stream;
+  const int64_t l0 = c->launches;
+  try {
+    // q = A p; p.q; x += alpha p, r -= alpha q (||r||^2); z = T^-1 r (z.r); p = z + beta p; stop test
+    launch_init_masked(c, li, nullptr, C.q, 1);
+    launch_apply(c, li, C.p, C.q, 0);
+    launch_dot2(c, n, C.p, C.q, nullptr, nullptr, nullptr, cs + CS_PQ, false);
+    launch_axpy_pcg(c, n, x, C.r, C.p, C.q, cs + CS_ZR_OLD, cs + CS_PQ, cs + CS_RR, nullptr, false);
+    line_solve(c, C.r, C.z, cs + CS_ZR_NEW);
+    launch_xpby(c, n, C.p, C.z, cs + CS_ZR_NEW, cs + CS_ZR_OLD, 0);
+    k_coarse_next<<<1, 1, 0, c->stream>>>(cs, (double)c->opts.coarse_maxit, h);
+    CUDA_CHECK(cudaGetLastError());
+    c->launches++;
+  } catch (...) {
+    c->stream = keep;
+    cudaGraph_t g2;
+    cudaStreamEndCapture(C.body_stream, &g2);
+    throw;
+  }
+  C.body_launches = c->launches - l0;
+  c->stream = keep;
+  cudaGraph_t g2 = nullptr;
+  CUDA_CHECK(cudaStreamEndCapture(C.body_stream, &g2));
+}
+
+void coarse_pcg(sem_ctx* c, const double* b, double* x) {
+  Coarse& C = c->C;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CUDA_CHECK(cudaStreamIsCapturing(c->stream, &st));
+  if (st == cudaStreamCaptureStatusActive) {
+    emit_coarse_pcg(c, b, x);
+    return;
+  }
+  // eager: replay the solve's own graph on the coarsest level's buffers
+  const int li = (int)c->L.size() - 1;
+  DeviceLevel& L = c->L[li];
+  if (!C.exec) {
+    if (!C.cap_stream) CUDA_CHECK(cudaStreamCreateWithFlags(&C.cap_stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    cudaStream_t keep = c->stream;
+    c->stream = C.cap_stream;
+    const int64_t l0 = c->launches;
+    cudaGraph_t g = nullptr;
+    CUDA_CHECK(cudaStreamBeginCapture(C.cap_stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      emit_coarse_pcg(c, L.f, L.u);
+    } catch (...) {
+      cudaStreamEndCapture(C.cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c->stream = keep;
+      throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(C.cap_stream, &g));
+    c->stream = keep;
+    C.exec_launches = c->launches - l0;
+    c->launches = l0;
+    CUDA_CHECK(cudaGraphInstantiate(&C.exec, g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+  }
+  if (b != L.f) CUDA_CHECK(cudaMemcpyAsync(L.f, b, L.n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_CHECK(cudaGraphLaunch(C.exec, c->stream));
+  c->launches += C.exec_launches;
+  if (x != L.u) CUDA_CHECK(cudaMemcpyAsync(x, L.u, L.n * 8, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// total inner iterations since the last reset (synchronises the stream)
+int64_t coarse_iters(sem_ctx* c, bool reset) {
+  if (!c->C.iterative || !c->C.cs) return 0;
+  double v = 0.0;
+  CUDA_CHECK(cudaMemcpyAsync(&v, c->C.cs + CS_TOTAL, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (reset) CUDA_CHECK(cudaMemsetAsync(c->C.cs + CS_TOTAL, 0, sizeof(double), c->stream));
+  return (int64_t)v;
+}
+
+void coarse_reset_iters(sem_ctx* c) {
+  if (c->C.iterative && c->C.cs) CUDA_CHECK(cudaMemsetAsync(c->C.cs + CS_TOTAL, 0, sizeof(double), c->stream));
+}
+
+void coarse_destroy(sem_ctx* c) {
+  Coarse& C = c->C;
+  if (C.exec) cudaGraphExecDestroy(C.exec);
+  if (C.cap_stream) cudaStreamDestroy(C.cap_stream);
+  if (C.body_stream) cudaStreamDestroy(C.body_stream);
+  C.exec = nullptr;
+  C.cap_stream = C.body_stream = nullptr;
+}
+
+}  // namespace sem

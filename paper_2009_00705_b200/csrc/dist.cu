@@ -311,7 +311,7 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
   const sem_opts& o = c0->opts;
   sem_report R;
   memset(&R, 0, sizeof(R));
-  D.coarse->C.iters = 0;
+  coarse_reset_iters(D.coarse);
   CUDA_CHECK(cudaEventRecord(c0->ev0, c0->stream));
   Vecs u, r, p, q, z, ro;
   for (auto* c : D.parts) {
@@ -413,7 +413,7 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
   float ms = 0.f;
   CUDA_CHECK(cudaEventElapsedTime(&ms, c0->ev0, c0->ev1));
   R.t_ms = ms;
-  R.coarse_iters = (int)D.coarse->C.iters;
+  R.coarse_iters = (int)coarse_iters(D.coarse, false);
   R.rel_res = nf > 0 ? rn / nf : 0.0;
   if (R.n_hist > 1) R.q_mean = std::pow(R.res_hist[R.n_hist - 1] / R.res_hist[0], 1.0 / (R.n_hist - 1));
   if (status == SEM_OK && !R.converged) status = SEM_ENOTCONV;

@@ -140,11 +140,19 @@ struct Coarse {
   double* Apack = nullptr;      // lower-triangular 64x64 tiles of Ainv (Ainv freed), k_coarse_symv
   float* Apack32 = nullptr;     // the same in FP32 storage (opts.mixed_precision, reading O36)
   double* x = nullptr;          // [nc] work
-  // iterative path (reading O9): Jacobi-preconditioned CG on the P=1 operator
+  // iterative path (reading O9): vertical-line block-Jacobi PCG on the P=1 operator (coarse.cu)
   int iterative = 0;
-  double* dinv = nullptr;       // [n] inverse diagonal, 0 on Dirichlet nodes
+  double* dinv = nullptr;       // [n] diagonal during setup
   double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
-  int64_t iters = 0;            // inner iterations since the last reset
+  int nlines = 0;               // vertical lines of free P=1 nodes (bottom to top)
+  int64_t line_max = 0;
+  int64_t* loff = nullptr;      // [nlines+1]
+  int32_t* lnode = nullptr;     // [nfree] node of every line position
+  double *ta = nullptr, *tinv = nullptr, *tc = nullptr;   // Thomas factors per line position
+  double* cs = nullptr;         // device scalars of the solve (coarse.cu CS_*)
+  cudaGraphExec_t exec = nullptr;                 // standalone graph of the solve (coarsest L.f -> L.u)
+  cudaStream_t cap_stream = nullptr, body_stream = nullptr;
+  int64_t exec_launches = 0, body_launches = 0;
 };
 
 // dist.cu (partitioned solve; c->dist != nullptr)
@@ -207,9 +215,18 @@ void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc);
 void launch_prolong(sem_ctx* c, int level, const double* uc, double* uf);
 void launch_coarse(sem_ctx* c, const double* r, double* z);
 void launch_dot2(sem_ctx* c, int64_t n, const double* a, const double* b, const double* d, const double* e,
-                 const uint8_t* mask, double* out2);
+                 const uint8_t* mask, double* out2, bool clear = true);
 void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* p, const double* q,
-                     const double* num, const double* den, double* rr, const uint8_t* mask = nullptr);
+                     const double* num, const double* den, double* rr, const uint8_t* mask = nullptr,
+                     bool clear = true);
+// coarse.cu: iterative P=1 solve (line-Jacobi PCG, device-side stop test in a CUDA-graph WHILE node)
+void coarse_pcg(sem_ctx* c, const double* b, double* x);
+void setup_coarse_lines(sem_ctx* c, const std::vector<int32_t>& conn, const std::vector<uint8_t>& dir,
+                        const double* d_diag, const double* d_off);
+void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double* Ae, double* off);
+int64_t coarse_iters(sem_ctx* c, bool reset);
+void coarse_reset_iters(sem_ctx* c);
+void coarse_destroy(sem_ctx* c);
 void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den, int mode);
 void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi);
 void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);

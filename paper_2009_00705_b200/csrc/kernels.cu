@@ -766,8 +766,8 @@ __global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __
 }
 
 void launch_dot2(sem_ctx* c, int64_t n, const double* a, const double* b, const double* d, const double* e,
-                 const uint8_t* mask, double* out2) {
-  CUDA_CHECK(cudaMemsetAsync(out2, 0, sizeof(double) * (d ? 2 : 1), c->stream));
+                 const uint8_t* mask, double* out2, bool clear) {
+  if (clear) CUDA_CHECK(cudaMemsetAsync(out2, 0, sizeof(double) * (d ? 2 : 1), c->stream));
   k_dot2<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, b, d, e, mask, out2);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
@@ -789,8 +789,8 @@ __global__ void k_axpy_pcg(int64_t n, double* __restrict__ u, double* __restrict
 }
 
 void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* p, const double* q,
-                     const double* num, const double* den, double* rr, const uint8_t* mask) {
-  CUDA_CHECK(cudaMemsetAsync(rr, 0, sizeof(double), c->stream));
+                     const double* num, const double* den, double* rr, const uint8_t* mask, bool clear) {
+  if (clear) CUDA_CHECK(cudaMemsetAsync(rr, 0, sizeof(double), c->stream));
   k_axpy_pcg<<<grid_for(n, 256), 256, 0, c->stream>>>(n, u, r, p, q, num, den, rr, mask);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;

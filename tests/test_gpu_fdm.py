@@ -175,8 +175,8 @@ def test_fdm_cta8_on_p6_hull_replica():
         assert rel(got, zo) <= STEP_TOL
     # solve: oracle residual of the library solution over every row
     phiD = m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])
-    phi, rep = s.solve(torch.from_numpy(phiD).cuda(), tol=1e-12)
-    assert rep["converged"]
+    phi, rep = s.solve(torch.from_numpy(phiD).cuda(), tol=1e-12, check=False)
+    assert rep["converged"], rep["res_hist"][-12:]
     dm = s.dirichlet_mask(0)
     Y = streamed_apply_lib(m, 6, xyz, np.stack([phi.cpu().numpy(), np.where(dm, phiD, 0.0)], axis=1))
     assert np.linalg.norm(Y[~dm, 0]) <= 1e-11 * np.linalg.norm(Y[~dm, 1])

@@ -165,8 +165,8 @@ def _whole_vector_checks(F, u, seed_sol_tol=1e-12):
     n = s.n_dof(0)
     y = s.apply(torch.from_numpy(u).cuda()).cpu().numpy()
     phiD = F.m.phi(F.xyz[:, 0], F.xyz[:, 1], F.xyz[:, 2])
-    phi, rep = s.solve(torch.from_numpy(phiD).cuda(), tol=seed_sol_tol)
-    assert rep["converged"] and rep["rel_res"] <= seed_sol_tol
+    phi, rep = s.solve(torch.from_numpy(phiD).cuda(), tol=seed_sol_tol, check=False)
+    assert rep["converged"] and rep["rel_res"] <= seed_sol_tol, (rep["iters"], rep["res_hist"][-12:])
     ph = phi.cpu().numpy()
     dm = s.dirichlet_mask(0)
     np.testing.assert_array_equal(ph[dm], phiD[dm])
