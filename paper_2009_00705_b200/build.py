@@ -5,7 +5,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = ["csrc/refelem.cpp", "csrc/topology.cpp", "csrc/partition.cpp", "csrc/kernels.cu", "csrc/apply_dmma.cu", "csrc/apply_warp.cu",
+SRC = ["csrc/refelem.cpp", "csrc/topology.cpp", "csrc/partition.cpp", "csrc/kernels.cu", "csrc/apply_dmma.cu", "csrc/apply_warp.cu", "csrc/apply_quad.cu",
        "csrc/capi.cu", "csrc/coarse.cu", "csrc/dist.cu", "csrc/fdm.cpp", "csrc/fdm.cu"]
 LIB = os.path.join(HERE, "libsem_pmg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

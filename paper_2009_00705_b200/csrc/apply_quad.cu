@@ -1,0 +1,345 @@
+// Operator apply, FOUR elements per warp, FP64 tensor cores (sm_100a DMMA) for the
+// triangle stages and FP64 FMA for the vertical stages.
+//
+// The same operator as k_apply_warp / k_apply (eq 3.8): y (+/-)= sum_e
+// Q_e^T D^T (G (.) D Q_e u), sum-factorised vertical-first:
+//
+//   A    Ut[m][q] = sum_l u[m][l] Bt[q][l],  Udt[m][q] = sum_l u[m][l] Dt[q][l]      (FMA)
+//   B    g_c[a][q] = sum_m B_c[a][m] U_c[m][q]   (c = r, s on Ut; c = 0 on Udt)    (DMMA)
+//   G    w = G g at every cubature point (a, q)                                     (FMA)
+//   B^T  Vt[m][q] = sum_a Br[a][m] w_r + Bs[a][m] w_s,  Vdt[m][q] = sum_a B0[a][m] w_0 (DMMA)
+//   A^T  y[m][l] = sum_q Vt[m][q] Bt[q][l] + Vdt[m][q] Dt[q][l]                    (FMA)
+//
+// Why four elements: the triangle stages carry ~85 % of the flops.  With one element
+// per warp (k_apply_warp) their DMMA tiles are padded along the vertical points (p+1 =
+// 6 of 8 columns at p = 5).  Here the M dimension of both triangle GEMMs is the pair
+// (vertical point q, element e) of four elements, row = 8 mt + r4 with e = r4 & 3 and
+// q = 2 mt + (r4 >> 2): (p+1) x 4 rows fill whole 8-row tiles (p = 3, 5), and every
+// lane only ever holds data of ONE element (e = (lane >> 2) & 3).  Consequences:
+//   * stage A's outputs are computed by each lane directly in the A-fragment layout
+//     of stage B (FMA, no padding along the 6-point vertical dimension);
+//   * stage B's C fragment (row, a = 8 na + 2 c4 + i) is stage B^T's A fragment
+//     without any shuffle: the contraction index a of stage B^T is enumerated as
+//     k-step i <-> a = 8 na + 2 c4 + i (a permutation of k, applied to the B operand
+//     read from shared memory as well);
+//   * stage A^T is again per lane (FMA) over the lane's own three q values, then one
+//     xor-16 shuffle adds the partner lane's other three.
+// DMMA per element at p = 5: 135 (k_apply_warp: 195).
+//
+// Data movement: the geometric factors of the four elements' current a-tile are
+// staged by four TMA bulk copies (cp.async.bulk + mbarrier) into a per-warp ring of
+// 2 slots (the a-tile-major layout of k_g_tiles, shared with k_apply_warp); u is
+// gathered through the connectivity into registers, y scattered with FP64 atomics.
+// Persistent CTAs of 8 warps.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "internal.h"
+
+namespace sem {
+
+namespace aq {
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+}  // namespace aq
+
+template <int P>
+struct AQ {
+  static constexpr int N1 = P + 1, NT = N1 * (N1 + 1) / 2, QT = N1 * N1, QV = N1, Q = QT * QV, N = NT * N1;
+  static constexpr int MTQ = aq::cdiv(N1, 2);   // row tiles over (q, e)
+  static constexpr int KM = aq::cdiv(NT, 4);    // k-steps over triangle nodes (stage B)
+  static constexpr int MTA = aq::cdiv(QT, 8);   // a-tiles
+  static constexpr int NM = aq::cdiv(NT, 8);    // n-tiles over triangle nodes (stage B^T)
+  static constexpr int NALAST = QT - 8 * (MTA - 1);
+  static constexpr int QE = (QV + 1) / 2;       // k_g_tiles' q permutation: even points first
+  static constexpr int LDM = 8 * aq::cdiv(NT, 8) + 4;   // row stride of Bm (= 4 mod 8)
+  static constexpr int ROWSA = 8 * MTA;
+  static constexpr int BM = 3 * ROWSA * LDM;    // Br, Bs, B0 [a][m], zero padded
+  static constexpr int BT = 2 * QV * N1;        // Bt, Dt [q][l]
+  static constexpr int W = 8;                   // warps per CTA
+  static constexpr int R = 2;                   // ring slots per warp
+  static constexpr int TSE = 6 * QV * 8;        // doubles of one element's a-tile (full tile)
+  static constexpr int TS = 4 * TSE;            // doubles of one slot (four elements)
+  static constexpr int NYL = aq::cdiv(N1, 2);   // vertical output nodes scattered per lane
+  static constexpr int SMEM = (BM + BT + W * R * TS) * 8 + W * R * 8;
+  static_assert(SMEM <= 227 * 1024, "apply_quad shared memory");
+};
+
+// host: Bm [3][ROWSA][LDM] (Br, Bs, B0 at [a][m]) followed by Bt, Dt [q][l]
+std::vector<double> quad_apply_mats(const LevelRef& R) {
+  auto run = [&](auto tag) {
+    using D = AQ<decltype(tag)::value>;
+    std::vector<double> v(D::BM + D::BT, 0.0);
+    const double* B[3] = {R.Br.data(), R.Bs.data(), R.B0.data()};
+    for (int c = 0; c < 3; ++c)
+      for (int a = 0; a < D::QT; ++a)
+        for (int m = 0; m < D::NT; ++m) v[(c * D::ROWSA + a) * D::LDM + m] = B[c][a * D::NT + m];
+    for (int i = 0; i < D::QV * D::N1; ++i) {
+      v[D::BM + i] = R.Bt[i];
+      v[D::BM + D::QV * D::N1 + i] = R.Dt[i];
+    }
+    return v;
+  };
+  switch (R.p) {
+    case 3: return run(std::integral_constant<int, 3>{});
+    case 4: return run(std::integral_constant<int, 4>{});
+    case 5: return run(std::integral_constant<int, 5>{});
+  }
+  return {};
+}
+
+__device__ __forceinline__ void aq_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t aq_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+template <int P>
+__global__ void __launch_bounds__(32 * AQ<P>::W, 1)
+    k_apply_quad(int E, const int32_t* __restrict__ conn, const double* __restrict__ Gw,
+                 const double* __restrict__ mats, const double* __restrict__ u, double* __restrict__ y, int flags) {
+  using D = AQ<P>;
+  extern __shared__ __align__(128) double sm[];
+  double* Bm = sm;                        // [3][ROWSA][LDM]
+  double* sBt = sm + D::BM;               // [QV][N1]
+  double* sDt = sBt + D::QV * D::N1;
+  double* ringall = sm + D::BM + D::BT;   // [W][R][4][TSE]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(ringall + D::W * D::R * D::TS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r4 = lane >> 2, c4 = lane & 3, el = r4 & 3, h = r4 >> 2;
+  for (int i = tid; i < D::BM + D::BT; i += 32 * D::W) sm[i] = __ldg(mats + i);
+  if (lane == 0) {
+    for (int b = 0; b < D::R; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(aq_smem(mbar + D::R * warp + b)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double sgn = (flags & AP_NEGATE) ? -1.0 : 1.0;
+  const int nquad = (E + 3) >> 2;
+  const int qstride = gridDim.x * D::W;
+  const int q0 = blockIdx.x * D::W + warp;
+  double* ring = ringall + warp * D::R * D::TS;
+  // copy t of this warp: quad q0 + (t / MTA) qstride, a-tile t % MTA, slot t % R: four bulk copies
+  auto issue = [&](int t) {
+    const int qd = q0 + (t / D::MTA) * qstride, ma = t % D::MTA;
+    if (qd >= nquad || lane != 0) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const int ne = min(4, E - 4 * qd);
+    const uint32_t one = (uint32_t)(6 * D::QV * (ma < D::MTA - 1 ? 8 : D::NALAST)) * 8u;
+    const uint32_t mb = aq_smem(mbar + D::R * warp + t % D::R);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(one * ne) : "memory");
+    for (int k = 0; k < ne; ++k)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              aq_smem(ring + (t % D::R) * D::TS + k * D::TSE)),
+          "l"(Gw + (size_t)(4 * qd + k) * 6 * D::Q + (size_t)ma * 48 * D::QV), "r"(one), "r"(mb)
+          : "memory");
+  };
+  if (q0 < nquad)
+    for (int t = 0; t < D::R; ++t) issue(t);
+  int tk = 0;
+  for (int qd = q0; qd < nquad; qd += qstride, tk += D::MTA) {
+    const int e = 4 * qd + el;
+    const bool ev = e < E;
+    const int32_t* ce = conn + (size_t)(ev ? e : 0) * D::N;
+    // ---- stage A (FMA): lane's A fragments of stage B, m = 4 ks + c4, q = 2 mt + h
+    double Ua[D::MTQ][D::KM], Ud[D::MTQ][D::KM];
+    {
+      double uu[D::KM][D::N1];
+#pragma unroll
+      for (int ks = 0; ks < D::KM; ++ks)
+#pragma unroll
+        for (int l = 0; l < D::N1; ++l) {
+          const int m = 4 * ks + c4;
+          double v = 0.0;
+          if (ev && m < D::NT) {
+            const int g = __ldg(ce + m + D::NT * l);
+            if (g >= 0) v = __ldg(u + g);
+            else if (flags & AP_GATHER_ALL) v = __ldg(u + ~g);
+          }
+          uu[ks][l] = v;
+        }
+#pragma unroll
+      for (int mt = 0; mt < D::MTQ; ++mt) {
+        const int q = 2 * mt + h;
+#pragma unroll
+        for (int ks = 0; ks < D::KM; ++ks) Ua[mt][ks] = Ud[mt][ks] = 0.0;
+        if (q < D::QV) {
+#pragma unroll
+          for (int l = 0; l < D::N1; ++l) {
+            const double bt = sBt[q * D::N1 + l], dt = sDt[q * D::N1 + l];
+#pragma unroll
+            for (int ks = 0; ks < D::KM; ++ks) {
+              Ua[mt][ks] = fma(uu[ks][l], bt, Ua[mt][ks]);
+              Ud[mt][ks] = fma(uu[ks][l], dt, Ud[mt][ks]);
+            }
+          }
+        }
+      }
+    }
+    double Vt[D::MTQ][D::NM][2], Vd[D::MTQ][D::NM][2];
+#pragma unroll
+    for (int mt = 0; mt < D::MTQ; ++mt)
+#pragma unroll
+      for (int nm = 0; nm < D::NM; ++nm) Vt[mt][nm][0] = Vt[mt][nm][1] = Vd[mt][nm][0] = Vd[mt][nm][1] = 0.0;
+#pragma unroll 1
+    for (int na = 0; na < D::MTA; ++na) {
+      const int t = tk + na;
+      {  // wait for copy t
+        const uint32_t mb = aq_smem(mbar + D::R * warp + t % D::R);
+        const uint32_t par = (uint32_t)(t / D::R) & 1u;
+        uint32_t done = 0;
+        while (!done)
+          asm volatile(
+              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+              : "=r"(done)
+              : "r"(mb), "r"(par)
+              : "memory");
+      }
+      // ---- stage B: g_c^T[(q,e)][a] for this a-tile, B operand = B_c[a = 8 na + r4][m = 4 ks + c4]
+      double g[3][D::MTQ][2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int mt = 0; mt < D::MTQ; ++mt) g[c][mt][0] = g[c][mt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < D::KM; ++ks) {
+        const int off = (8 * na + r4) * D::LDM + 4 * ks + c4;
+        const double br = Bm[off], bs = Bm[D::ROWSA * D::LDM + off], b0 = Bm[2 * D::ROWSA * D::LDM + off];
+#pragma unroll
+        for (int mt = 0; mt < D::MTQ; ++mt) {
+          aq_dmma(g[0][mt][0], g[0][mt][1], Ua[mt][ks], br);
+          aq_dmma(g[1][mt][0], g[1][mt][1], Ua[mt][ks], bs);
+          aq_dmma(g[2][mt][0], g[2][mt][1], Ud[mt][ks], b0);
+        }
+      }
+      // ---- w = G g at the lane's points (a = 8 na + 2 c4 + i, q = 2 mt + h) of element el
+      const int nat = (na < D::MTA - 1) ? 8 : D::NALAST;
+      const double* Gt = ring + (t % D::R) * D::TS + el * D::TSE;
+      const int cs = D::QV * nat;   // component stride in the tile
+#pragma unroll
+      for (int mt = 0; mt < D::MTQ; ++mt) {
+        const int q = 2 * mt + h;
+        const int qp = (q & 1) ? D::QE + (q >> 1) : (q >> 1);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int al = 2 * c4 + i;
+          double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+          if (ev && q < D::QV && al < nat) {
+            const double* gp = Gt + qp * nat + al;
+            const double gxx = gp[0], gxy = gp[cs], gxz = gp[2 * cs], gyy = gp[3 * cs], gyz = gp[4 * cs],
+                         gzz = gp[5 * cs];
+            const double x0 = g[0][mt][i], x1 = g[1][mt][i], x2 = g[2][mt][i];
+            w0 = gxx * x0 + gxy * x1 + gxz * x2;
+            w1 = gxy * x0 + gyy * x1 + gyz * x2;
+            w2 = gxz * x0 + gyz * x1 + gzz * x2;
+          }
+          g[0][mt][i] = w0;
+          g[1][mt][i] = w1;
+          g[2][mt][i] = w2;
+        }
+      }
+      __syncwarp();  // every lane is done with this slot before it is refilled
+      issue(t + D::R);
+      // ---- stage B^T: V^T[(q,e)][m] += w^T[(q,e)][a] B_c[a][m]; k-step i <-> a = 8 na + 2 c4 + i
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+#pragma unroll
+        for (int nm = 0; nm < D::NM; ++nm) {
+          const int off = (8 * na + 2 * c4 + i) * D::LDM + 8 * nm + r4;
+          const double br = Bm[off], bs = Bm[D::ROWSA * D::LDM + off], b0 = Bm[2 * D::ROWSA * D::LDM + off];
+#pragma unroll
+          for (int mt = 0; mt < D::MTQ; ++mt) {
+            aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[0][mt][i], br);
+            aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[1][mt][i], bs);
+            aq_dmma(Vd[mt][nm][0], Vd[mt][nm][1], g[2][mt][i], b0);
+          }
+        }
+      }
+    }
+    // ---- stage A^T (FMA): y[m][l] over the lane's q = 2 mt + h, partner lane (h ^ 1) adds the rest
+    double yp[D::NM][2][D::N1];
+#pragma unroll
+    for (int nm = 0; nm < D::NM; ++nm)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int l = 0; l < D::N1; ++l) yp[nm][i][l] = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < D::MTQ; ++mt) {
+      const int q = 2 * mt + h;
+      if (q < D::QV) {
+#pragma unroll
+        for (int l = 0; l < D::N1; ++l) {
+          const double bt = sBt[q * D::N1 + l], dt = sDt[q * D::N1 + l];
+#pragma unroll
+          for (int nm = 0; nm < D::NM; ++nm)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              yp[nm][i][l] = fma(Vt[mt][nm][i], bt, fma(Vd[mt][nm][i], dt, yp[nm][i][l]));
+        }
+      }
+    }
+#pragma unroll
+    for (int nm = 0; nm < D::NM; ++nm)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int l = 0; l < D::N1; ++l) yp[nm][i][l] += __shfl_xor_sync(0xffffffffu, yp[nm][i][l], 16);
+    if (ev) {
+#pragma unroll
+      for (int nm = 0; nm < D::NM; ++nm)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int m = 8 * nm + 2 * c4 + i;
+          if (m < D::NT) {
+#pragma unroll
+            for (int l = 0; l < D::N1; ++l) {
+              if ((l < D::NYL) != (h == 0)) continue;   // lane h = 0 scatters the lower l, h = 1 the upper
+              const int gq = __ldg(ce + m + D::NT * l);
+              if (gq >= 0) atomicAdd(y + gq, sgn * yp[nm][i][l]);
+              else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~gq, sgn * yp[nm][i][l]);
+            }
+          }
+        }
+    }
+  }
+}
+
+template <int P>
+static void apply_quad_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags) {
+  using D = AQ<P>;
+  static int grid_maxes[kMaxDev] = {0};
+  const int dev = cur_device();
+  int& grid_max = grid_maxes[dev];
+  if (!grid_max) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_apply_quad<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
+    int per_sm = 0, sms = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_quad<P>, 32 * D::W, D::SMEM));
+    grid_max = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  if (c->E_own == 0) return;
+  const int nquad = (c->E_own + 3) / 4;
+  const int need = (nquad + D::W - 1) / D::W;
+  const int grid = need < grid_max ? need : grid_max;
+  k_apply_quad<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(c->E_own, L.conn, L.Gw, L.qmats, u, y, flags);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+bool launch_apply_quad(sem_ctx* c, int level, const double* u, double* y, int flags) {
+  const DeviceLevel& L = c->L[level];
+  if (!L.qmats || !L.Gw) return false;
+  switch (L.p) {
+    case 3: apply_quad_P<3>(c, L, u, y, flags); break;
+    case 4: apply_quad_P<4>(c, L, u, y, flags); break;
+    case 5: apply_quad_P<5>(c, L, u, y, flags); break;
+    default: return false;
+  }
+  c->launches++;
+  return true;
+}
+
+}  // namespace sem

@@ -77,7 +77,8 @@ struct DeviceLevel {
   double* mats = nullptr;       // B0 Br Bs [qt][nt|1], Bt Dt [qv][n1]
   double* frag = nullptr;       // DMMA fragment-ordered reference operands (apply_dmma.cu)
   double* wmats = nullptr;      // reference operands of the warp-per-element apply (apply_warp.cu), p <= 6
-  double* Gw = nullptr;         // a-tile-major copy of G for k_apply_warp (apply_warp.cu)
+  double* Gw = nullptr;         // a-tile-major copy of G for k_apply_warp / k_apply_quad
+  double* qmats = nullptr;      // reference operands of the four-elements-per-warp apply (apply_quad.cu), 3 <= p <= 5
   double* Ae1 = nullptr;        // P <= 2 levels: packed element matrices [N(N+1)/2][E] (k_apply_em)
   // Schwarz (not on the coarsest level)
   int32_t* sidx = nullptr;      // padded to 16 per subdomain, -1 = padding
@@ -205,6 +206,8 @@ void launch_apply_dmma(sem_ctx* c, int level, const double* u, double* y, int fl
 std::vector<double> dmma_fragments(const LevelRef& R);
 std::vector<double> warp_apply_mats(const LevelRef& R);
 bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags);
+std::vector<double> quad_apply_mats(const LevelRef& R);
+bool launch_apply_quad(sem_ctx* c, int level, const double* u, double* y, int flags);
 void build_g_tiles(sem_ctx* c, int level);
 void build_p1_matrices(sem_ctx* c, int level, const double* d_D);
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);

@@ -266,7 +266,7 @@ void build_p1_matrices(sem_ctx* c, int level, const double* d_D) {
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
   {
     const DeviceLevel& L = c->L[level];
-    if (L.p <= 2 && L.Ae1 && c->opts.apply_kernel == 0) {
+    if (L.p <= 2 && L.Ae1 && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3)) {
       if (c->E_own > 0) {
         if (L.p == 1)
           k_apply_em<6><<<(c->E_own + 127) / 128, 128, 0, c->stream>>>(c->E_own, (int64_t)c->E, L.conn, L.Ae1, u,
@@ -280,7 +280,8 @@ void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) 
       return;
     }
   }
-  if (c->opts.apply_kernel == 0 && launch_apply_warp(c, level, u, y, flags)) return;
+  if (c->opts.apply_kernel == 3 && launch_apply_quad(c, level, u, y, flags)) return;
+  if ((c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3) && launch_apply_warp(c, level, u, y, flags)) return;
   if (c->opts.apply_kernel != 1) {
     launch_apply_dmma(c, level, u, y, flags);
     return;

@@ -222,11 +222,11 @@ def test_literal_smoother_option(c1):
     assert rel(out[lev.free], mg.vcycle(r)) <= STEP_TOL
 
 
-@pytest.mark.parametrize("apply_kernel", [0, 1, 2])
+@pytest.mark.parametrize("apply_kernel", [0, 1, 2, 3])
 @pytest.mark.parametrize("p", range(1, 9))
 def test_config4_construction_every_order(p, apply_kernel):
     """Config-4 construction (scaled replica) at every order p = 1..8, both operator
-    kernels (0 = warp-per-element DMMA, 1 = FMA, 2 = batched DMMA): apply and solve parity; p = 1 is the
+    kernels (0 = warp-per-element DMMA, 1 = FMA, 2 = batched DMMA, 3 = four elements per warp): apply and solve parity; p = 1 is the
     single-level coarse solve (O26).  3x3 (p <= 5) or 2x2 quads x 2 layers = 36 / 16
     prisms: several element batches with a ragged last batch for every p."""
     from workloads.configs import basin
