@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the variant solves (FDM local solves, mixed-precision storage) reported beside the headline")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-4 p-sweep block")
+    ap.add_argument("--sweep-one", default="", help=argparse.SUPPRESS)
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="validation only: run the partitioned solve with R emulated ranks on one GPU")
     return ap.parse_args()
@@ -229,10 +231,10 @@ def run_config5(args, lib, peak):
     xyz = s.node_xyz(0)
     phiD = torch.from_numpy(m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])).cuda()
     phi = s.empty(0)
-    for _ in range(max(1, min(args.warmup, 2))):
+    for _ in range(args.warmup):
         s.solve(phiD, args.tol, out=phi)
     torch.cuda.synchronize()
-    steps = max(1, min(args.steps, 3))
+    steps = args.steps
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s.stream)
     for _ in range(steps):
@@ -243,10 +245,13 @@ def run_config5(args, lib, peak):
     us, b = s.bench_kernel("schwarz", 0, 5)
     ua, ba = s.bench_kernel("apply", 0, 5)
     i = s.info
+    sroof = solve_roofline(s, rep, ms, peak)
     out = {"name": "config5", "workload": WORKLOAD["config5"], "smoother": "FDM / exact-dense hybrid (O33, O35)",
            "value": i["n_free"] / (ms * 1e-3) / 1e6, "unit": "MDOF/s", "ms_per_step": ms, "steps": steps,
            "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "n_dof": i["n_dof"],
-           "n_free": i["n_free"], "coarse": f"P=1, {i['coarse_n']} free DOF (Jacobi-PCG)", "setup_s": setup_s,
+           "n_free": i["n_free"], "coarse": f"P=1, {i['coarse_n']} free DOF (line-Jacobi PCG, "
+           f"{rep['coarse_iters']} inner iterations per solve)", "setup_s": setup_s, "warmup": args.warmup,
+           "solve_roofline": sroof, "smoother_kernels": i["smoother_kernel"],
            "device_GB": i["device_bytes"] / 1e9,
            "smoother_kernel": {"kernel": "k_fdm_cta<8> + k_schwarz<double> (O35 subset)", "us": us,
                                "alg_bytes_per_launch": b, "achieved_GBs": b / us / 1e3, "frac_hbm": b / us / 1e3 / peak},
@@ -254,6 +259,99 @@ def run_config5(args, lib, peak):
     s.close()
     del s
     torch.cuda.empty_cache()
+    return out
+
+
+def solve_roofline(s, rep, ms, peak, nu=(3, 3)):
+    """Algorithmic HBM bytes of one whole solve (DESIGN.md §7 byte model) / solve time.
+    Per level: the library's own per-launch algorithmic bytes of one smoother sweep and
+    one operator apply (sem_bench_kernel); a V-cycle does nu1 + nu2 sweeps and nu1 + nu2
+    applies per smoothed level (Alg 4.1 with the first pre-sweep from u = 0), residual
+    inits (17 B/node), restriction + prolongation (~16 B per fine + coarse node each)
+    and the coarse solve (the stored inverse's bytes, or per inner iteration one P=1
+    apply + 10 vector passes); PCG adds per iteration one finest apply and 10 vector
+    passes (8 B/node each), the lift one apply."""
+    i = s.info
+    L = i["n_levels"]
+    nd = i["level_n_dof"]
+    vc = 0.0
+    for li in range(L - 1):
+        _, bs = s.bench_kernel("schwarz", li, 1)
+        _, ba = s.bench_kernel("apply", li, 1)
+        vc += (nu[0] + nu[1]) * (bs + ba) + (nu[0] + nu[1]) * 17.0 * nd[li] + 2 * 16.0 * (nd[li] + nd[li + 1])
+    _, ba0 = s.bench_kernel("apply", 0, 1)
+    _, bac = s.bench_kernel("apply", L - 1, 1)
+    vcycles, iters = max(rep["vcycles"], 1), rep["iters"]
+    try:
+        _, bc = s.bench_kernel("coarse", 0, 1)
+        coarse = vcycles * bc
+    except Exception:
+        coarse = rep["coarse_iters"] * (bac + 80.0 * nd[-1])
+    total = vcycles * vc + coarse + iters * (ba0 + 80.0 * nd[0]) + ba0 + 32.0 * nd[0]
+    ach = total / (ms * 1e-3) / 1e9
+    return {"model_bytes": total, "achieved_GBs": ach, "peak": peak, "frac": ach / peak,
+            "note": "algorithmic bytes of every kernel of the solve (byte model of DESIGN.md §7) / solve time"}
+
+
+SWEEP = [("dense_o1", "exact dense local inverses, overlap 1 (the paper's smoother, eq 4.4, P:320)",
+          dict(local_solve=0, overlap=1)),
+         ("fdm_refined", "FDM local solves (O33), refined overlap ceil((P+1)/2) (P:536)",
+          dict(local_solve=1, overlap=-1))]
+
+
+def sweep_one(args, p, variant):
+    """One config-4 point (subprocess: frees the device between points)."""
+    import torch
+    import paper_2009_00705_b200 as lib
+    from workloads import config4
+    extra = [v for v in SWEEP if v[0] == variant][0][2]
+    t0 = time.perf_counter()
+    m = config4(p)
+    nodes = m.node_xyz(lib.reference_nodes(p))
+    t0 = time.perf_counter()
+    s = lib.Solver(m.vertices, m.prisms, m.face_tag, p, node_xyz=nodes, **(extra if p > 1 else {}))
+    setup_s = time.perf_counter() - t0
+    del nodes
+    xyz = s.node_xyz(0)
+    phiD = torch.from_numpy(m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])).cuda()
+    phi = s.empty(0)
+    for _ in range(args.warmup):
+        s.solve(phiD, args.tol, out=phi, check=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s.stream)
+    for _ in range(args.steps):
+        _, rep = s.solve(phiD, args.tol, out=phi, check=False)
+    e1.record(s.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak = json.load(open(peaks_path))["hbm_gbs"] if os.path.exists(peaks_path) else 6470.8
+    i = s.info
+    out = {"p": p, "variant": variant if p > 1 else "coarse solver only (single level, O26)",
+           "n_elem": i["n_elem"], "n_dof": i["n_dof"], "n_free": i["n_free"], "levels": i["level_p"],
+           "coarse_n": i["coarse_n"], "vcycles": rep["vcycles"], "iters": rep["iters"], "q_mean": rep["q_mean"],
+           "converged": rep["converged"], "coarse_iters": rep["coarse_iters"], "ms_per_step": ms,
+           "MDOF_s": i["n_free"] / (ms * 1e-3) / 1e6, "setup_s": setup_s, "device_GB": i["device_bytes"] / 1e9,
+           "smoother_kernels": i["smoother_kernel"],
+           "solve_roofline": solve_roofline(s, rep, ms, peak) if p > 1 else None}
+    print("SWEEP " + json.dumps(out), flush=True)
+
+
+def run_sweep(args):
+    """BASELINE.json config 4: ~10 M DOF per p, p = 1..8, each point in its own process."""
+    out = []
+    for p in range(1, 9):
+        for variant, desc, _ in (SWEEP if p > 1 else SWEEP[:1]):
+            cmd = [sys.executable, os.path.abspath(__file__), "--sweep-one", f"{p}:{variant}", "--steps",
+                   str(args.steps), "--warmup", str(args.warmup), "--tol", str(args.tol)]
+            try:
+                r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+                lines = [l[6:] for l in r.stdout.splitlines() if l.startswith("SWEEP ")]
+                out.append(json.loads(lines[-1]) if lines else {"p": p, "variant": variant,
+                                                                 "error": (r.stderr or "")[-400:]})
+            except subprocess.TimeoutExpired:
+                out.append({"p": p, "variant": variant, "error": "timeout"})
     return out
 
 
@@ -265,6 +363,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.sweep_one:
+        import torch
+        torch.cuda.set_device(local)
+        p, variant = args.sweep_one.split(":")
+        sweep_one(args, int(p), variant)
         return
     import torch
     torch.cuda.set_device(local)
@@ -337,10 +441,14 @@ def main():
     roof = {"kernel": ("k_fdm" if args.smoother == "fdm" else "k_schwarz") + " (level 0, one sweep" + (", this rank's partition)" if world > 1 else ")"),
             "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
             "alg_bytes_per_launch": b_s, "launch_us": us_s,
-            "traffic_note": "ncu dram__bytes_read+write per launch in profiles/schwarz_r1_raw.csv (28.9 GB, N=1)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "when" in peaks else "fallback 6650 GB/s"}
-    if world == 1 and args.emulate_ranks <= 1 and args.config == "config3" and args.smoother == "dense" and not args.mixed:
-        roof["traffic"] = 28.92e9
+    tpath = os.path.join(ROOT, "profiles", "r2_schwarz_traffic.json")
+    if world == 1 and args.emulate_ranks <= 1 and args.config == "config3" and args.smoother == "dense" \
+            and not args.mixed and os.path.exists(tpath):
+        tr = json.load(open(tpath))       # one ncu --set full capture of this kernel on this workload
+        if abs(tr.get("alg_bytes_per_launch", 0) - b_s) < 1e-6 * b_s:
+            roof["traffic"] = tr["dram_bytes_per_launch"]
+            roof["traffic_note"] = tr["source"]
     ach_a = b_a / (us_a * 1e-6) / 1e9
     apply = {"kernel": "k_apply_warp<%d> (FP64 tensor cores, warp per element)" % m.p, "us": us_a,
              "alg_bytes_per_launch": b_a,
@@ -361,11 +469,18 @@ def main():
         e2e = {"value": n_free / t_e2e / 1e6, "unit": "MDOF/s",
                "h2d_bytes_per_step": info["n_dof"] * 8, "d2h_bytes_per_step": info["n_dof"] * 8,
                "ms_per_step": t_e2e * 1e3, "api": "laplace_solve_host (pinned host buffers)"}
+    sroof = solve_roofline(s, reps[-1], ms_step, peak) if world == 1 and args.emulate_ranks <= 1 else None
     variants = None
+    sweep = None
     if world == 1 and args.emulate_ranks <= 1 and not args.no_variants:
         variants = run_variants(args, lib, m, phiD_h, peak, kw)
         if args.config == "config3":
+            s.close()
+            del s
+            torch.cuda.empty_cache()
             variants.append(run_config5(args, lib, peak))
+    if world == 1 and args.emulate_ranks <= 1 and not args.no_sweep and args.config == "config3":
+        sweep = run_sweep(args)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = oracle_sample(args.tol)
@@ -391,7 +506,8 @@ def main():
                              if args.emulate_ranks > 1 else "single GPU"), "setup_s": setup_s},
             "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "q_mean": rep["q_mean"],
             "work_units": ms_step * 1e3 / us_a,    # solve time / one finest operator apply (O25)
-            "roofline": roof, "apply": apply, "variants": variants, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "solve_roofline": sroof, "apply": apply, "variants": variants,
+            "config4_sweep": sweep, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
         }
