@@ -259,6 +259,36 @@ int sem_coarse_solve(sem_ctx *ctx, const double *r, double *z);
  * alg_bytes: algorithmic bytes per launch. */
 int sem_bench_kernel(sem_ctx *ctx, int kernel, int level, int reps, double *mean_us, double *alg_bytes);
 
+/* ---- FNPF time stages (eq 2.1a-b and 2.2; readings O37-O40) ----
+ * The fully nonlinear potential-flow model that re-solves the Laplace problem at
+ * every Runge-Kutta stage.  State: the free-surface elevation eta (z of the
+ * free-surface node) and the surface potential phi~, DEVICE vectors of length
+ * n_surface in the order of sem_fnpf_surface_nodes.  Needs a sigma-layered mesh
+ * (every node on the vertical line of one free-surface node; SEM_EUNSUPPORTED
+ * otherwise, e.g. under a body) and a single-domain ctx.
+ *
+ * sem_fnpf_init: node_xyz = the nodal map passed to sem_setup (host, [n_prism][N][3],
+ * copied); strategy 1 = the paper's strategy I (only the finest operator follows the
+ * free surface; smoothers and coarse operators from t = 0), 2 = every
+ * level's operator follows it (smoothers and coarse inverse from t = 0). */
+int sem_fnpf_init(sem_ctx *ctx, const double *node_xyz, int strategy, int64_t *n_surface);
+/* library node id (finest level) of every free-surface node, host [n_surface] */
+int sem_fnpf_surface_nodes(const sem_ctx *ctx, int32_t *node_ids);
+/* One stage: move the fluid volume to eta (sigma map, O37), solve eq 2.2 with
+ * phi = phi~ on the free surface to tol (warm-started from the previous stage),
+ * recover w~ = dphi/dz (O38) and the surface gradients (O39), and return the rates
+ * of eq 2.1a-b: deta = -grad eta.grad phi~ + w~ (1 + |grad eta|^2),
+ * dphis = -g eta - (|grad phi~|^2 - w~^2 (1 + |grad eta|^2)) / 2, g = 9.81;
+ * w (may be NULL) receives w~.  linear = 1: the small-amplitude version on the
+ * t = 0 geometry (deta = w~, dphis = -g eta).  Returns SEM_ENOTCONV if the solve
+ * did not converge (the rates are still written). */
+int fnpf_rhs(sem_ctx *ctx, const double *eta, const double *phis, double *deta, double *dphis, double *w,
+             double tol, int linear, sem_report *rep);
+/* One classical RK4 step of length dt (ERK4; reading O40: four stages, one
+ * Laplace solve each), eta and phis updated in place; iters (may be NULL) receives
+ * the PCG iterations of the four stage solves. */
+int fnpf_erk4_step(sem_ctx *ctx, double *eta, double *phis, double dt, double tol, int linear, int *iters);
+
 /* Generate an NCCL unique id (128 bytes) for opts.nccl_id (call on rank 0). */
 int sem_nccl_unique_id(void *id_out);
 

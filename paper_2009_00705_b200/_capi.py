@@ -75,6 +75,10 @@ _lib.sem_restrict.argtypes = [_vp, C.c_int, _vp, _vp]
 _lib.sem_schwarz.argtypes = [_vp, C.c_int, _vp, _vp, C.c_int]
 _lib.sem_coarse_solve.argtypes = [_vp, _vp, _vp]
 _lib.sem_nccl_unique_id.argtypes = [_vp]
+_lib.sem_fnpf_init.argtypes = [_vp, _dp, C.c_int, C.POINTER(C.c_int64)]
+_lib.sem_fnpf_surface_nodes.argtypes = [_vp, _vp]
+_lib.fnpf_rhs.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_int, C.POINTER(SemReport)]
+_lib.fnpf_erk4_step.argtypes = [_vp, _vp, _vp, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int)]
 _lib.sem_bench_kernel.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 _lib.sem_launch_count.argtypes = [_vp, C.c_int]
 _lib.sem_launch_count.restype = C.c_int64
@@ -91,7 +95,7 @@ _lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.sem_host_partition.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp]
 
-EXPORTS = ["laplace_solve_guess", "sem_update_geometry", "sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+EXPORTS = ["sem_fnpf_init", "sem_fnpf_surface_nodes", "fnpf_rhs", "fnpf_erk4_step", "laplace_solve_guess", "sem_update_geometry", "sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
            "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
            "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
            "sem_destroy", "sem_strerror", "sem_last_error"]
@@ -333,6 +337,33 @@ class Solver:
         """sem_update_geometry: new nodal map [n_prism][N(p)][3] (same topology)."""
         nx = np.ascontiguousarray(node_xyz, dtype=np.float64)
         _check(_lib.sem_update_geometry(self._ctx, nx.ctypes.data_as(_dp), int(strategy)), "sem_update_geometry")
+
+    # ---------------------------------------------------------------- FNPF stages (NEXT-4)
+    def fnpf_init(self, node_xyz, strategy=1):
+        """sem_fnpf_init: returns the library node ids of the free-surface nodes."""
+        nx = np.ascontiguousarray(node_xyz, dtype=np.float64)
+        ns = C.c_int64()
+        _check(_lib.sem_fnpf_init(self._ctx, nx.ctypes.data_as(_dp), int(strategy), C.byref(ns)), "sem_fnpf_init")
+        ids = np.zeros(ns.value, dtype=np.int32)
+        _check(_lib.sem_fnpf_surface_nodes(self._ctx, C.c_void_p(ids.ctypes.data)), "sem_fnpf_surface_nodes")
+        return ids
+
+    def fnpf_rhs(self, eta, phis, tol, linear=False):
+        """fnpf_rhs: (deta, dphis, w, report) for the surface state (CUDA tensors)."""
+        de, dp, w = (self._torch.empty_like(eta) for _ in range(3))
+        rep = SemReport()
+        code = _lib.fnpf_rhs(self._ctx, _ptr(eta), _ptr(phis), _ptr(de), _ptr(dp), _ptr(w), tol, int(linear),
+                             C.byref(rep))
+        if code not in (0, SEM_ENOTCONV):
+            raise SemError(code, "fnpf_rhs")
+        return de, dp, w, rep.as_dict()
+
+    def fnpf_erk4_step(self, eta, phis, dt, tol, linear=False):
+        """fnpf_erk4_step: eta, phis (CUDA tensors) advanced in place; returns the PCG iterations."""
+        it = C.c_int()
+        _check(_lib.fnpf_erk4_step(self._ctx, _ptr(eta), _ptr(phis), dt, tol, int(linear), C.byref(it)),
+               "fnpf_erk4_step")
+        return it.value
 
     def solve_host(self, dirichlet_phi_host, tol, out_host, rhs_host=None):
         """Host buffers (numpy arrays or pinned CPU tensors), copies inside the call."""

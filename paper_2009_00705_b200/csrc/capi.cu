@@ -1121,6 +1121,51 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
   return SEM_OK;
 }
 
+int sem_fnpf_init(sem_ctx* c, const double* node_xyz, int strategy, int64_t* n_surface) {
+  if (!c || !node_xyz) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
+  try {
+    fnpf_init(c, node_xyz, strategy);
+    if (n_surface) *n_surface = fnpf_surface(c, nullptr);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
+int sem_fnpf_surface_nodes(const sem_ctx* c, int32_t* node_ids) {
+  if (!c || !node_ids || !c->fnpf) return SEM_EINVAL;
+  fnpf_surface(c, node_ids);
+  return SEM_OK;
+}
+
+int fnpf_rhs(sem_ctx* c, const double* eta, const double* phis, double* deta, double* dphis, double* w, double tol,
+             int linear, sem_report* rep) {
+  if (!c || !c->fnpf || !eta || !phis || !deta || !dphis || !(tol >= 0.0)) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
+  try {
+    sem_report R;
+    fnpf_stage(c, eta, phis, deta, dphis, w, tol, linear, &R);
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    if (rep) *rep = R;
+    return R.converged ? SEM_OK : SEM_ENOTCONV;
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+}
+
+int fnpf_erk4_step(sem_ctx* c, double* eta, double* phis, double dt, double tol, int linear, int* iters) {
+  if (!c || !c->fnpf || !eta || !phis || !(tol >= 0.0)) return SEM_EINVAL;
+  DeviceGuard guard(c->device);
+  try {
+    fnpf_erk4(c, eta, phis, dt, tol, linear, iters);
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
 int sem_nccl_unique_id(void* id_out) {
   if (!id_out) return SEM_EINVAL;
   try {
@@ -1147,6 +1192,7 @@ void sem_destroy(sem_ctx* c) {
   for (int i = 0; i < 2; ++i)
     if (c->vc_graph[i]) cudaGraphExecDestroy(c->vc_graph[i]);
   coarse_destroy(c);
+  fnpf_destroy(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hscal) cudaFreeHost(c->hscal);

@@ -27,8 +27,10 @@
 namespace sem {
 
 // device scalar slots of the coarse solve (C.cs)
-enum : int { CS_PQ = 0, CS_RR = 1, CS_ZR_OLD = 2, CS_ZR_NEW = 3, CS_RR0 = 4, CS_RR_DUP = 5, CS_THR2 = 6, CS_IT = 7,
+// (k_line_solve writes z.r and r.r to two consecutive slots: CS_ZR_NEW, CS_RR_DUP)
+enum : int { CS_PQ = 0, CS_RR = 1, CS_ZR_OLD = 2, CS_ZR_NEW = 3, CS_RR_DUP = 4, CS_THR2 = 6, CS_IT = 7,
              CS_TOTAL = 8, CS_N = 16 };
+static_assert(CS_RR_DUP == CS_ZR_NEW + 1, "line solve output slots");
 
 static int cgrid(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;

@@ -133,6 +133,7 @@ struct DeviceLevel {
 };
 
 struct Dist;  // dist.cu
+struct Fnpf;  // fnpf.cu
 
 struct Coarse {
   int64_t nc = 0;               // free coarse nodes
@@ -186,6 +187,8 @@ struct sem_ctx {
   double *host_in = nullptr, *host_in2 = nullptr, *host_out = nullptr;               // device staging for *_host
   // ---- partitioned solve (dist.cu): nranks > 1
   sem::Dist* dist = nullptr;
+  // ---- FNPF time stages (fnpf.cu)
+  sem::Fnpf* fnpf = nullptr;
   int64_t launches = 0;
   int64_t device_bytes = 0;
   double setup_ms = 0.0;
@@ -230,6 +233,13 @@ void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double*
 int64_t coarse_iters(sem_ctx* c, bool reset);
 void coarse_reset_iters(sem_ctx* c);
 void coarse_destroy(sem_ctx* c);
+// fnpf.cu: FNPF time stage (eq 2.1)
+void fnpf_init(sem_ctx* c, const double* node_xyz, int strategy);
+void fnpf_stage(sem_ctx* c, const double* eta, const double* phis, double* deta, double* dphis, double* w,
+                double tol, int linear, sem_report* rep);
+void fnpf_erk4(sem_ctx* c, double* eta, double* phis, double dt, double tol, int linear, int* iters);
+int64_t fnpf_surface(const sem_ctx* c, int32_t* ids);
+void fnpf_destroy(sem_ctx* c);
 void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den, int mode);
 void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi);
 void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);
