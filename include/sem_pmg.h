@@ -118,6 +118,12 @@ typedef struct {
                                  (rounded once at setup) and applied with FP64 arithmetic -- the
                                  mixed-precision multigrid of P:35; the preconditioner stays a fixed
                                  symmetric linear operator, the outer PCG and the operator stay FP64. */
+  int deterministic;          /* 0 (default): FP64 atomics in the gather-scatter and the reductions (results
+                                 agree run to run to rounding).  1: bit-reproducible solves:
+                                 every scatter is launched per colour of node-disjoint elements /
+                                 subdomains, reductions sum per-block partials in a fixed order, the dense
+                                 coarse solve is a row-wise GEMV of the full inverse, FDM levels use the
+                                 generic k_fdm.  Slower; single-domain ctx only (SEM_EUNSUPPORTED otherwise). */
 } sem_opts;
 
 typedef struct {

@@ -28,7 +28,7 @@ class SemOpts(C.Structure):
                 ("verbose", C.c_int), ("apply_kernel", C.c_int), ("coarse_solver", C.c_int),
                 ("coarse_rtol", C.c_double), ("coarse_maxit", C.c_int), ("nranks", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("local_solve", C.c_int),
-                ("mixed_precision", C.c_int)]
+                ("mixed_precision", C.c_int), ("deterministic", C.c_int)]
 
 
 class SemReport(C.Structure):

@@ -59,6 +59,45 @@ double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// ------------------------------------------------------------------ deterministic mode
+void colour_sets(int64_t nsets, const std::vector<int64_t>& off, const std::vector<int32_t>& idx, int64_t nnodes,
+                 const std::vector<uint8_t>* skip, std::vector<int64_t>& coff, std::vector<int32_t>& clist) {
+  for (int words = 2;; words *= 2) {  // colour bitsets per node, widened until the greedy colouring fits
+    std::vector<uint64_t> used((size_t)nnodes * words, 0);
+    std::vector<int> col(nsets, -1);
+    int ncol = 0;
+    bool ok = true;
+    for (int64_t k = 0; k < nsets && ok; ++k) {
+      if (skip && (*skip)[k]) continue;
+      std::vector<uint64_t> m(words, 0);
+      for (int64_t t = off[k]; t < off[k + 1]; ++t)
+        if (idx[t] >= 0)
+          for (int w = 0; w < words; ++w) m[w] |= used[(size_t)idx[t] * words + w];
+      int cc = -1;
+      for (int w = 0; w < words && cc < 0; ++w)
+        if (~m[w]) cc = 64 * w + __builtin_ctzll(~m[w]);
+      if (cc < 0) {
+        ok = false;
+        break;
+      }
+      col[k] = cc;
+      ncol = std::max(ncol, cc + 1);
+      for (int64_t t = off[k]; t < off[k + 1]; ++t)
+        if (idx[t] >= 0) used[(size_t)idx[t] * words + cc / 64] |= 1ull << (cc % 64);
+    }
+    if (!ok) continue;
+    coff.assign(ncol + 1, 0);
+    for (int64_t k = 0; k < nsets; ++k)
+      if (col[k] >= 0) coff[col[k] + 1]++;
+    for (int q = 0; q < ncol; ++q) coff[q + 1] += coff[q];
+    clist.assign(coff[ncol], 0);
+    std::vector<int64_t> pos(coff.begin(), coff.end() - 1);
+    for (int64_t k = 0; k < nsets; ++k)
+      if (col[k] >= 0) clist[pos[col[k]]++] = (int32_t)k;   // ascending set id within a colour
+    return;
+  }
+}
+
 // ------------------------------------------------------------------ Schwarz setup
 void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas, cusolverDnHandle_t sol,
                    const double* d_D, int verbose) {
@@ -97,6 +136,11 @@ void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas
   if (c->opts.mixed_precision) L.tiles32 = dalloc<float>(c, (size_t)toff[E]);
   else L.tiles = dalloc<double>(c, (size_t)toff[E]);
   L.W = upload(c, S.W);
+  if (c->opts.deterministic) {  // colours of node-disjoint subdomains (one k_schwarz launch each)
+    std::vector<int32_t> cl;
+    colour_sets(E, S.off, S.idx, L.n, nullptr, L.scol_off, cl);
+    L.scol = upload(c, cl);
+  }
 
   Scratch sc;
   const int32_t* d_idx = sc.put(S.idx);
@@ -252,6 +296,13 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
   CUDA_CHECK(cudaStreamSynchronize(c->stream));
   if (hinfo != 0) throw SemError(SEM_ESINGULAR, "coarse inverse failed (info " + std::to_string(hinfo) + ")");
   launch_symmetrize(c, c->C.Ainv, nc);
+  if (c->opts.deterministic) {  // full symmetric inverse, row-wise fixed-order GEMV (k_coarse_gemv_det)
+    c->C.Afull = dalloc<double>(c, (size_t)nc * nc);
+    CUDA_CHECK(cudaMemcpyAsync(c->C.Afull, c->C.Ainv, (size_t)nc * nc * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    c->C.Ainv = nullptr;
+    return;
+  }
   {  // packed lower-triangular tiles (FP64, or FP32 storage under mixed precision, O36):
      // the GEMV reads half of the symmetric inverse
     const int64_t T = (nc + 63) / 64, len = T * (T + 1) / 2 * 4096;
@@ -269,6 +320,7 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
 void check_opts(const sem_opts& o) {
   if (o.local_solve < 0 || o.local_solve > 1) throw SemError(SEM_EINVAL, "bad options: local_solve");
   if (o.mixed_precision < 0 || o.mixed_precision > 1) throw SemError(SEM_EINVAL, "bad options: mixed_precision");
+  if (o.deterministic < 0 || o.deterministic > 1) throw SemError(SEM_EINVAL, "bad options: deterministic");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
       o.apply_kernel > 3 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
       o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
@@ -553,11 +605,23 @@ void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
   prepare_global(mesh, p, o, gm);
   c->E_global = gm.hm.E;
   if (o.nranks > 1) {
+    if (o.deterministic) throw SemError(SEM_EUNSUPPORTED, "deterministic mode: single-domain ctx only");
     setup_distributed(c, gm);
   } else {
     std::vector<int> lids(gm.sched.size());
     for (size_t i = 0; i < lids.size(); ++i) lids[i] = (int)i;
     build_levels(c, gm, lids, nullptr, nullptr);
+    if (o.deterministic) {  // element colours: elements sharing a vertex (hence any node) differ
+      const DeviceLevel& Lc = c->L.back();
+      const std::vector<int32_t>& cv = Lc.conn_host;
+      std::vector<int64_t> off(c->E + 1);
+      for (int e = 0; e <= c->E; ++e) off[e] = (int64_t)e * Lc.N;
+      std::vector<int32_t> cl;
+      colour_sets(c->E, off, cv, Lc.n, nullptr, c->det.ecol_off, cl);
+      c->det.ecol = upload(c, cl);
+      c->det.part = dalloc<double>(c, 2 * 8192);
+      c->det.on = 1;
+    }
     // one finest-level apply, timed for the work-unit count of every solve (O25)
     const int64_t n0 = c->L[0].n;
     CUDA_CHECK(cudaMemsetAsync(c->pw, 0, sizeof(double) * n0, c->stream));

@@ -53,7 +53,7 @@ __global__ void k_offdiag_accum(int64_t E, const int32_t* __restrict__ conn, con
 __global__ void k_line_solve(int nlines, const int64_t* __restrict__ loff, const int32_t* __restrict__ lnode,
                              const double* __restrict__ ta, const double* __restrict__ tinv,
                              const double* __restrict__ tc, const double* __restrict__ r, double* __restrict__ z,
-                             double* out) {
+                             double* out, double* part) {
   double s0 = 0.0, s1 = 0.0;
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlines; l += gridDim.x * blockDim.x) {
     const int64_t b = loff[l], e = loff[l + 1];
@@ -93,8 +93,13 @@ __global__ void k_line_solve(int nlines, const int64_t* __restrict__ loff, const
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     }
     if (lane == 0) {
-      atomicAdd(out, s0);
-      atomicAdd(out + 1, s1);
+      if (part) {  // deterministic mode: fixed-order sum in det_finalize
+        part[2 * blockIdx.x] = s0;
+        part[2 * blockIdx.x + 1] = s1;
+      } else {
+        atomicAdd(out, s0);
+        atomicAdd(out + 1, s1);
+      }
     }
   }
 }
@@ -136,10 +141,11 @@ __global__ void k_coarse_next(double* cs, double maxit, cudaGraphConditionalHand
 
 static void line_solve(sem_ctx* c, const double* r, double* z, double* out2) {
   Coarse& C = c->C;
-  k_line_solve<<<cgrid(C.nlines, 128), 128, 0, c->stream>>>(C.nlines, C.loff, C.lnode, C.ta, C.tinv, C.tc, r, z,
-                                                             out2);
+  const int gb = cgrid(C.nlines, 128);
+  k_line_solve<<<gb, 128, 0, c->stream>>>(C.nlines, C.loff, C.lnode, C.ta, C.tinv, C.tc, r, z, out2, c->det.part);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
+  if (c->det.part) det_finalize(c, gb, out2, out2 + 1);
 }
 
 // ---------------------------------------------------------------- setup

@@ -295,6 +295,11 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
     std::vector<uint8_t> skip(E);
     for (int e = 0; e < E; ++e) skip[e] = F.regular[e] ? 0 : 1;
     L.f_skip = upload(c, skip);
+    if (c->opts.deterministic) {  // colours of node-disjoint FDM boxes (one k_fdm launch each)
+      std::vector<int32_t> cl;
+      colour_sets(E, F.ioff, F.idx, L.n, &skip, L.fcol_off, cl);
+      L.fcol = upload(c, cl);
+    }
   }
   // algorithmic bytes of one sweep (column-batched kernel): per column S_h, l_h and the patch
   // node ids [n_h][Z_c+1]; per element S_v, l_v
@@ -316,9 +321,9 @@ __global__ void __launch_bounds__(256) k_fdm(const int32_t* __restrict__ col, co
                                              const double* __restrict__ Sv, const double* __restrict__ lv,
                                              const double* __restrict__ W, const double* __restrict__ r,
                                              double* __restrict__ u, int transpose, int box_max,
-                                             const uint8_t* __restrict__ skip) {
+                                             const uint8_t* __restrict__ skip, const int32_t* __restrict__ elist) {
   extern __shared__ double sm[];
-  const int k = blockIdx.x;
+  const int k = elist ? elist[blockIdx.x] : blockIdx.x;
   if (skip[k]) return;
   const int c = col[k];
   const int nh = (int)(hoff[c + 1] - hoff[c]);
@@ -1093,6 +1098,7 @@ static int fdm_simple() {
 // Which FDM sweep kernel a level runs (sem_info.smoother_kernel; the dispatch below)
 int fdm_kernel_choice(const DeviceLevel& L) {
   if (!L.fdm) return SEM_SMOOTHER_DENSE;
+  if (!L.fcol_off.empty()) return SEM_SMOOTHER_FDM_GENERIC;   // deterministic mode: colour batches of k_fdm
   if (!fdm_simple() && L.f_warp) {
     if (L.f_nvt == 1) return SEM_SMOOTHER_FDM_WARP1;
     if (fdm_cta_enabled() && L.f_mt >= 5) return SEM_SMOOTHER_FDM_CTA;  // p >= 6: CTA-shared horizontal transforms
@@ -1130,9 +1136,19 @@ void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose
   const int smem = (2 * box + L.f_nv_max * L.f_nv_max) * (int)sizeof(double);
   static int attr[kMaxDev] = {0};
   smem_opt_in(k_fdm, smem, attr);
-  k_fdm<<<c->E_own, 256, smem, c->stream>>>(L.f_col, L.f_hoff, L.f_moff, L.f_nv, L.f_voff, L.f_lvoff, L.f_ioff,
-                                            L.f_idx, L.f_Sh, L.f_lh, L.f_Sv, L.f_lv, L.W, r, u, transpose, box,
-                                            L.f_skip);
+  if (c->det.on) {  // deterministic: one launch per colour of node-disjoint FDM boxes
+    for (size_t q = 0; q + 1 < L.fcol_off.size(); ++q) {
+      const int nb = (int)(L.fcol_off[q + 1] - L.fcol_off[q]);
+      if (nb == 0) continue;
+      k_fdm<<<nb, 256, smem, c->stream>>>(L.f_col, L.f_hoff, L.f_moff, L.f_nv, L.f_voff, L.f_lvoff, L.f_ioff, L.f_idx,
+                                          L.f_Sh, L.f_lh, L.f_Sv, L.f_lv, L.W, r, u, transpose, box, L.f_skip,
+                                          L.fcol + L.fcol_off[q]);
+    }
+  } else {
+    k_fdm<<<c->E_own, 256, smem, c->stream>>>(L.f_col, L.f_hoff, L.f_moff, L.f_nv, L.f_voff, L.f_lvoff, L.f_ioff,
+                                              L.f_idx, L.f_Sh, L.f_lh, L.f_Sv, L.f_lv, L.W, r, u, transpose, box,
+                                              L.f_skip, nullptr);
+  }
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }

@@ -106,6 +106,9 @@ struct DeviceLevel {
   int64_t f_bytes = 0;          // algorithmic bytes of one FDM sweep (fdm.cu)
   int nsub = 0;                 // dense subdomains (all owned elements, or the O35 subset of an FDM level)
   uint8_t* f_skip = nullptr;    // [E] 1 = subdomain solved densely (O35), skipped by the FDM kernels
+  // deterministic mode (opts.deterministic): colours of node-disjoint subdomains, one launch each
+  std::vector<int64_t> scol_off, fcol_off;   // [colours+1] into scol / fcol
+  int32_t *scol = nullptr, *fcol = nullptr;  // dense subdomain ids / FDM element ids, grouped by colour
   int64_t nk_sum = 0, packed = 0;
   int max_tiles_1d = 0;
   // transfer from the next coarser level (level+1 -> this)
@@ -132,6 +135,20 @@ struct DeviceLevel {
   double *sendbuf = nullptr, *recvbuf = nullptr;
 };
 
+// deterministic mode (opts.deterministic): colour-ordered gather-scatter and
+// fixed-order reductions make repeated solves bit-identical
+struct Det {
+  int on = 0;
+  std::vector<int64_t> ecol_off;  // [colours+1] element colours (no two elements of a colour share a node)
+  int32_t* ecol = nullptr;        // element ids grouped by colour
+  double* part = nullptr;         // per-block partial sums [2][blocks] of the reductions
+};
+// greedy colouring of node sets (set k = idx[off[k] .. off[k+1]), entries < 0 ignored, sets with
+// skip[k] != 0 left out): returns colour offsets and the set ids grouped by colour
+void colour_sets(int64_t nsets, const std::vector<int64_t>& off, const std::vector<int32_t>& idx, int64_t nnodes,
+                 const std::vector<uint8_t>* skip, std::vector<int64_t>& coff, std::vector<int32_t>& clist);
+void det_finalize(sem_ctx* c, int nb, double* out0, double* out1);
+
 struct Dist;  // dist.cu
 struct Fnpf;  // fnpf.cu
 
@@ -140,6 +157,7 @@ struct Coarse {
   int32_t* fidx = nullptr;      // [nc] compact -> level gid
   double* Ainv = nullptr;       // [nc][nc] row-major, symmetric (dense path)
   double* Apack = nullptr;      // lower-triangular 64x64 tiles of Ainv (Ainv freed), k_coarse_symv
+  double* Afull = nullptr;      // deterministic mode: the full symmetric inverse [nc][nc]
   float* Apack32 = nullptr;     // the same in FP32 storage (opts.mixed_precision, reading O36)
   double* x = nullptr;          // [nc] work
   // iterative path (reading O9): vertical-line block-Jacobi PCG on the P=1 operator (coarse.cu)
@@ -187,6 +205,7 @@ struct sem_ctx {
   double *host_in = nullptr, *host_in2 = nullptr, *host_out = nullptr;               // device staging for *_host
   // ---- partitioned solve (dist.cu): nranks > 1
   sem::Dist* dist = nullptr;
+  sem::Det det;                 // deterministic mode (opts.deterministic)
   // ---- FNPF time stages (fnpf.cu)
   sem::Fnpf* fnpf = nullptr;
   int64_t launches = 0;

@@ -40,7 +40,8 @@ struct AD {
 template <int P>
 __global__ void __launch_bounds__(256) k_apply(int E, const int32_t* __restrict__ conn,
                                                const double* __restrict__ G, const double* __restrict__ mats,
-                                               const double* __restrict__ u, double* __restrict__ y, int flags) {
+                                               const double* __restrict__ u, double* __restrict__ y, int flags,
+                                               const int32_t* __restrict__ elist) {
   using D = AD<P>;
   extern __shared__ double sm[];
   double* sB0 = sm;
@@ -56,11 +57,13 @@ __global__ void __launch_bounds__(256) k_apply(int E, const int32_t* __restrict_
 
   for (int i = tid; i < D::SM_MATS; i += D::T) sm[i] = __ldg(mats + i);
   // gather u_e = Q_e u (Dirichlet entries as 0 unless AP_GATHER_ALL)
+  // slot e0 + j holds element elist[e0 + j] (deterministic colour batches) or e0 + j
+  auto elem = [&](int slot) { return elist ? __ldg(elist + slot) : slot; };
   for (int i = tid; i < D::NE * D::N; i += D::T) {
     const int e = e0 + i / D::N;
     double v = 0.0;
     if (e < E) {
-      const int c = __ldg(conn + (size_t)e * D::N + (i % D::N));
+      const int c = __ldg(conn + (size_t)elem(e) * D::N + (i % D::N));
       if (c >= 0) v = u[c];
       else if (flags & AP_GATHER_ALL) v = u[~c];
     }
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(256) k_apply(int E, const int32_t* __restrict_
     const int it = tid + k * D::T;
     const int e = it / D::Q, q = it % D::Q;
     if (it < D::NE * D::Q && e0 + e < E) {
-      const double* g = G + (size_t)(e0 + e) * 6 * D::Q + q;
+      const double* g = G + (size_t)elem(e0 + e) * 6 * D::Q + q;
 #pragma unroll
       for (int c = 0; c < 6; ++c) gv[k][c] = __ldg(g + c * D::Q);
     } else {
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(256) k_apply(int E, const int32_t* __restrict_
     if (e0 + e >= E) continue;
     const double v = part[(0 * D::NE + e) * D::N + n] + part[(1 * D::NE + e) * D::N + n] +
                      part[(2 * D::NE + e) * D::N + n];
-    const int c = __ldg(conn + (size_t)(e0 + e) * D::N + n);
+    const int c = __ldg(conn + (size_t)elem(e0 + e) * D::N + n);
     if (c >= 0) atomicAdd(y + c, sgn * v);
     else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~c, sgn * v);
   }
@@ -190,8 +193,17 @@ static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y
   static int attr[kMaxDev] = {0};
   smem_opt_in(k_apply<P>, D::SMEM, attr);
   if (c->E_own == 0) return;
+  if (c->det.on) {  // deterministic: one launch per element colour (no two elements of a colour share a node)
+    for (size_t k = 0; k + 1 < c->det.ecol_off.size(); ++k) {
+      const int cnt = (int)(c->det.ecol_off[k + 1] - c->det.ecol_off[k]);
+      k_apply<P><<<(cnt + D::NE - 1) / D::NE, D::T, D::SMEM, c->stream>>>(cnt, L.conn, L.G, L.mats, u, y, flags,
+                                                                        c->det.ecol + c->det.ecol_off[k]);
+    }
+    CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   const int grid = (c->E_own + D::NE - 1) / D::NE;
-  k_apply<P><<<grid, D::T, D::SMEM, c->stream>>>(c->E_own, L.conn, L.G, L.mats, u, y, flags);
+  k_apply<P><<<grid, D::T, D::SMEM, c->stream>>>(c->E_own, L.conn, L.G, L.mats, u, y, flags, nullptr);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -264,7 +276,7 @@ void build_p1_matrices(sem_ctx* c, int level, const double* d_D) {
 }
 
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
-  {
+  if (!c->det.on) {
     const DeviceLevel& L = c->L[level];
     if (L.p <= 2 && L.Ae1 && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3)) {
       if (c->E_own > 0) {
@@ -280,9 +292,10 @@ void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) 
       return;
     }
   }
-  if (c->opts.apply_kernel == 3 && launch_apply_quad(c, level, u, y, flags)) return;
-  if ((c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3) && launch_apply_warp(c, level, u, y, flags)) return;
-  if (c->opts.apply_kernel != 1) {
+  if (!c->det.on && c->opts.apply_kernel == 3 && launch_apply_quad(c, level, u, y, flags)) return;
+  if (!c->det.on && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3) && launch_apply_warp(c, level, u, y, flags))
+    return;
+  if (!c->det.on && c->opts.apply_kernel != 1) {
     launch_apply_dmma(c, level, u, y, flags);
     return;
   }
@@ -358,11 +371,11 @@ __global__ void __launch_bounds__(256) k_schwarz(const int32_t* __restrict__ sid
                                                  const int64_t* __restrict__ tile_off,
                                                  const TT* __restrict__ tiles, const double* __restrict__ W,
                                                  const double* __restrict__ r, double* __restrict__ u, int transpose,
-                                                 int npad_max) {
+                                                 int npad_max, const int32_t* __restrict__ slist) {
   extern __shared__ double sm[];
   double* x = sm;                 // [npad_max]
   double* yw = sm + npad_max;     // [8][npad_max]
-  const int k = blockIdx.x;
+  const int k = slist ? slist[blockIdx.x] : blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = sidx_off[k];
   const int np = (int)(sidx_off[k + 1] - base);
@@ -454,14 +467,22 @@ void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int trans
   const int smem = 9 * npad * (int)sizeof(double);
   static int attr_set[kMaxDev] = {0}, attr_set32[kMaxDev] = {0};
   if (L.nsub == 0) return;
-  if (L.tiles32) {  // mixed precision: FP32 storage of the exact inverses, FP64 arithmetic
-    if (smem > 48 * 1024) smem_opt_in(k_schwarz<float>, smem, attr_set32);
-    k_schwarz<float><<<L.nsub, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles32, L.W, r, u,
-                                                         transpose, npad);
-  } else {
-    if (smem > 48 * 1024) smem_opt_in(k_schwarz<double>, smem, attr_set);
-    k_schwarz<double><<<L.nsub, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u,
-                                                          transpose, npad);
+  if (smem > 48 * 1024) {
+    smem_opt_in(k_schwarz<float>, smem, attr_set32);
+    smem_opt_in(k_schwarz<double>, smem, attr_set);
+  }
+  // deterministic: one launch per subdomain colour (node-disjoint subdomains)
+  const size_t ncol = c->det.on ? L.scol_off.size() - 1 : 1;
+  for (size_t q = 0; q < ncol; ++q) {
+    const int nb = c->det.on ? (int)(L.scol_off[q + 1] - L.scol_off[q]) : L.nsub;
+    const int32_t* sl = c->det.on ? L.scol + L.scol_off[q] : nullptr;
+    if (nb == 0) continue;
+    if (L.tiles32)  // mixed precision: FP32 storage of the exact inverses, FP64 arithmetic
+      k_schwarz<float><<<nb, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles32, L.W, r, u,
+                                                     transpose, npad, sl);
+    else
+      k_schwarz<double><<<nb, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u,
+                                                      transpose, npad, sl);
   }
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
@@ -506,12 +527,12 @@ __global__ void k_prolong(int E, int ntf, int n1f, int ntc, int n1c, const int32
 __global__ void k_restrict(int E, int ntf, int n1f, int ntc, int n1c, const int32_t* __restrict__ connf,
                            const uint8_t* __restrict__ owner, const int32_t* __restrict__ connc,
                            const double* __restrict__ Itri, const double* __restrict__ I1,
-                           const double* __restrict__ rf, double* __restrict__ rc) {
+                           const double* __restrict__ rf, double* __restrict__ rc, const int32_t* __restrict__ elist) {
   extern __shared__ double sm[];
   const int Nf = ntf * n1f, Nc = ntc * n1c;
   double* xf = sm;               // [Nf]
   double* S = sm + Nf;           // [ntf][n1c]
-  const int e = blockIdx.x;
+  const int e = elist ? elist[blockIdx.x] : blockIdx.x;
   for (int n = threadIdx.x; n < Nf; n += blockDim.x) {
     const int g = connf[(size_t)e * Nf + n];
     xf[n] = (owner[(size_t)e * Nf + n] && g >= 0) ? rf[g] : 0.0;
@@ -551,8 +572,16 @@ void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc) {
   CUDA_CHECK(cudaMemsetAsync(rc, 0, sizeof(double) * C.n, c->stream));
   const int smem = (F.N + F.ref.nt * C.ref.n1) * (int)sizeof(double);
   if (c->E_own == 0) return;
-  k_restrict<<<c->E_own, 128, smem, c->stream>>>(c->E_own, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
-                                             F.Itri, F.I1, rf, rc);
+  if (c->det.on) {  // deterministic: element colours
+    for (size_t k = 0; k + 1 < c->det.ecol_off.size(); ++k) {
+      const int cnt = (int)(c->det.ecol_off[k + 1] - c->det.ecol_off[k]);
+      k_restrict<<<cnt, 128, smem, c->stream>>>(cnt, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner, C.conn,
+                                                F.Itri, F.I1, rf, rc, c->det.ecol + c->det.ecol_off[k]);
+    }
+  } else {
+    k_restrict<<<c->E_own, 128, smem, c->stream>>>(c->E_own, F.ref.nt, F.ref.n1, C.ref.nt, C.ref.n1, F.conn, F.owner,
+                                                   C.conn, F.Itri, F.I1, rf, rc, nullptr);
+  }
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
 }
@@ -706,8 +735,32 @@ __global__ void __launch_bounds__(256, 3) k_coarse_symv(int64_t n, int T, const 
   }
 }
 
+__device__ __forceinline__ double warp_sum(double v);
+
+// deterministic mode: z[fidx[i]] = sum_j A[i][j] x[j] over the full symmetric inverse, one warp
+// per row, each lane summing a fixed column stride, a fixed shuffle tree (no atomics)
+__global__ void k_coarse_gemv_det(int64_t n, const double* __restrict__ A, const double* __restrict__ x,
+                                  const int32_t* __restrict__ fidx, double* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const double* a = A + i * n;
+  double s = 0.0;
+  for (int64_t j = lane; j < n; j += 32) s = fma(a[j], x[j], s);
+  s = warp_sum(s);
+  if (lane == 0) z[fidx[i]] = s;
+}
+
 void launch_coarse(sem_ctx* c, const double* r, double* z) {
   const DeviceLevel& L = c->L.back();
+  if (c->C.Afull) {
+    CUDA_CHECK(cudaMemsetAsync(z, 0, sizeof(double) * L.n, c->stream));
+    k_gather<<<grid_for(c->C.nc, 256), 256, 0, c->stream>>>(c->C.nc, c->C.fidx, r, c->C.x);
+    k_coarse_gemv_det<<<(int)((c->C.nc + 7) / 8), 256, 0, c->stream>>>(c->C.nc, c->C.Afull, c->C.x, c->C.fidx, z);
+    CUDA_CHECK(cudaGetLastError());
+    c->launches += 2;
+    return;
+  }
   if (c->C.Apack || c->C.Apack32) {
     CUDA_CHECK(cudaMemsetAsync(z, 0, sizeof(double) * L.n, c->stream));
     k_gather<<<grid_for(c->C.nc, 256), 256, 0, c->stream>>>(c->C.nc, c->C.fidx, r, c->C.x);
@@ -733,7 +786,10 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ void block_sum2_atomic(double a, double b, double* out0, double* out1) {
+// Block sums of (a, b): atomically added to out0 / out1, or (deterministic mode, part != NULL)
+// written to part[2 blockIdx.x + {0, 1}] and summed in a fixed order by k_det_finalize.
+__device__ __forceinline__ void block_sum2_atomic(double a, double b, double* out0, double* out1,
+                                                  double* part = nullptr) {
   __shared__ double s0[32], s1[32];
   a = warp_sum(a);
   b = warp_sum(b);
@@ -747,37 +803,66 @@ __device__ __forceinline__ void block_sum2_atomic(double a, double b, double* ou
     a = warp_sum(a);
     b = warp_sum(b);
     if (lane == 0) {
-      atomicAdd(out0, a);
-      if (out1) atomicAdd(out1, b);
+      if (part) {
+        part[2 * blockIdx.x] = a;
+        part[2 * blockIdx.x + 1] = b;
+      } else {
+        atomicAdd(out0, a);
+        if (out1) atomicAdd(out1, b);
+      }
     }
   }
+}
+
+// out0 += sum_b part[2b], out1 += sum_b part[2b+1] in a fixed order (one warp)
+__global__ void k_det_finalize(int nb, const double* __restrict__ part, double* out0, double* out1) {
+  const int lane = threadIdx.x;
+  double a = 0.0, b = 0.0;
+  for (int i = lane; i < nb; i += 32) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    *out0 += a;
+    if (out1) *out1 += b;
+  }
+}
+
+void det_finalize(sem_ctx* c, int nb, double* out0, double* out1) {
+  k_det_finalize<<<1, 32, 0, c->stream>>>(nb, c->det.part, out0, out1);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
 }
 
 // out2[0] += a.b ; out2[1] += d.e (if d); over mask[i] != 0 only (if mask)
 __global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
                        const double* __restrict__ d, const double* __restrict__ e, const uint8_t* __restrict__ mask,
-                       double* out2) {
+                       double* out2, double* part) {
   double s0 = 0.0, s1 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (mask && !mask[i]) continue;
     s0 = fma(a[i], b[i], s0);
     if (d) s1 = fma(d[i], e[i], s1);
   }
-  block_sum2_atomic(s0, s1, out2, d ? out2 + 1 : nullptr);
+  block_sum2_atomic(s0, s1, out2, d ? out2 + 1 : nullptr, part);
 }
 
 void launch_dot2(sem_ctx* c, int64_t n, const double* a, const double* b, const double* d, const double* e,
                  const uint8_t* mask, double* out2, bool clear) {
   if (clear) CUDA_CHECK(cudaMemsetAsync(out2, 0, sizeof(double) * (d ? 2 : 1), c->stream));
-  k_dot2<<<grid_for(n, 256), 256, 0, c->stream>>>(n, a, b, d, e, mask, out2);
+  const int gb = grid_for(n, 256);
+  k_dot2<<<gb, 256, 0, c->stream>>>(n, a, b, d, e, mask, out2, c->det.part);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
+  if (c->det.part) det_finalize(c, gb, out2, d ? out2 + 1 : nullptr);
 }
 
 // alpha = num / den; u += alpha p; r -= alpha q; rr += r.r
 __global__ void k_axpy_pcg(int64_t n, double* __restrict__ u, double* __restrict__ r, const double* __restrict__ p,
                            const double* __restrict__ q, const double* num, const double* den, double* rr,
-                           const uint8_t* __restrict__ mask) {
+                           const uint8_t* __restrict__ mask, double* part) {
   const double alpha = *num / *den;
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -786,15 +871,17 @@ __global__ void k_axpy_pcg(int64_t n, double* __restrict__ u, double* __restrict
     r[i] = ri;
     if (!mask || mask[i]) s = fma(ri, ri, s);
   }
-  block_sum2_atomic(s, 0.0, rr, nullptr);
+  block_sum2_atomic(s, 0.0, rr, nullptr, part);
 }
 
 void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* p, const double* q,
                      const double* num, const double* den, double* rr, const uint8_t* mask, bool clear) {
   if (clear) CUDA_CHECK(cudaMemsetAsync(rr, 0, sizeof(double), c->stream));
-  k_axpy_pcg<<<grid_for(n, 256), 256, 0, c->stream>>>(n, u, r, p, q, num, den, rr, mask);
+  const int gb = grid_for(n, 256);
+  k_axpy_pcg<<<gb, 256, 0, c->stream>>>(n, u, r, p, q, num, den, rr, mask, c->det.part);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
+  if (c->det.part) det_finalize(c, gb, rr, nullptr);
 }
 
 // p = z + beta p: beta = num[0] / den (mode 0); p = z (mode 1);
@@ -826,7 +913,7 @@ void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y) {
 
 // z = dinv .* r; out2[0] += z.r; out2[1] += r.r
 __global__ void k_jacobi_dot(int64_t n, const double* __restrict__ d, const double* __restrict__ r,
-                             double* __restrict__ z, double* out2) {
+                             double* __restrict__ z, double* out2, double* part) {
   double s0 = 0.0, s1 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double ri = r[i], zi = d[i] * ri;
@@ -834,14 +921,16 @@ __global__ void k_jacobi_dot(int64_t n, const double* __restrict__ d, const doub
     s0 = fma(zi, ri, s0);
     s1 = fma(ri, ri, s1);
   }
-  block_sum2_atomic(s0, s1, out2, out2 + 1);
+  block_sum2_atomic(s0, s1, out2, out2 + 1, part);
 }
 
 void launch_jacobi_dot(sem_ctx* c, int64_t n, const double* dinv, const double* r, double* z, double* out2) {
   CUDA_CHECK(cudaMemsetAsync(out2, 0, 2 * sizeof(double), c->stream));
-  k_jacobi_dot<<<grid_for(n, 256), 256, 0, c->stream>>>(n, dinv, r, z, out2);
+  const int gb = grid_for(n, 256);
+  k_jacobi_dot<<<gb, 256, 0, c->stream>>>(n, dinv, r, z, out2, c->det.part);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
+  if (c->det.part) det_finalize(c, gb, out2, out2 + 1);
 }
 
 // diag[g] += Ae[e][n][n] over free nodes (setup)
