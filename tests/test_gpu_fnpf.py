@@ -83,7 +83,8 @@ def test_fnpf_erk4_step_parity():
 def test_fnpf_standing_wave_period(linear):
     """eta0 = A cos(k x), phi~0 = 0 in the closed box (k = pi, h = 1): after one
     period T = 2 pi / omega, omega^2 = g k tanh(k h), eta is back to eta0 within
-    1e-3 (linear version) / 1e-2 (fully nonlinear at A = 0.005, H/L = 0.005)."""
+    1e-3 (linear version) / 3e-2 (fully nonlinear at A = 0.005: the nonlinear
+    standing wave departs from the linear one at relative order k A = 0.016)."""
     p = 4
     m = config1(p=p, nx=4, ny=2, nz=2)
     s, S, perm, xy = _setup(m)
@@ -95,5 +96,5 @@ def test_fnpf_standing_wave_period(linear):
     tp = torch.zeros_like(te)
     for _ in range(32):
         s.fnpf_erk4_step(te, tp, T / 32, 1e-12, linear=linear)
-    assert np.linalg.norm(te.cpu().numpy() - eta0) <= (1e-3 if linear else 1e-2) * np.linalg.norm(eta0)
+    assert np.linalg.norm(te.cpu().numpy() - eta0) <= (1e-3 if linear else 3e-2) * np.linalg.norm(eta0)
     s.close()
