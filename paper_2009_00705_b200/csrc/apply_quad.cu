@@ -54,29 +54,39 @@ struct AQ {
   static constexpr int QE = (QV + 1) / 2;       // k_g_tiles' q permutation: even points first
   static constexpr int LDM = 8 * aq::cdiv(NT, 8) + 4;   // row stride of Bm (= 4 mod 8)
   static constexpr int ROWSA = 8 * MTA;
-  static constexpr int BM = 3 * ROWSA * LDM;    // Br, Bs, B0 [a][m], zero padded
+  static constexpr int BM = 3 * ROWSA * LDM;    // Br, Bs, B0 [a][m], zero padded (stage B operands)
+  // stage B^T operands, transposed: [3][8 NM][LDA] = B_c[a][m] at [m][a]; LDA = 8 mod 16 so that the
+  // 16-byte loads of the (a, a+1) pairs of a quarter-warp (two m rows x four a pairs) hit distinct banks
+  static constexpr int LDA = 8 * MTA + ((8 * MTA) % 16 == 0 ? 8 : 0);
+  static constexpr int BMT = 3 * 8 * NM * LDA;
   static constexpr int BT = 2 * QV * N1;        // Bt, Dt [q][l]
   static constexpr int W = 8;                   // warps per CTA
   static constexpr int R = 2;                   // ring slots per warp
-  static constexpr int TSE = 6 * QV * 8;        // doubles of one element's a-tile (full tile)
+  static constexpr int TSE0 = 6 * QV * 8;       // doubles of one element's a-tile (full tile)
+  static constexpr int TSE = TSE0 + 8;          // slot stride per element: = 8 mod 16 (bank spread of the 4 elements)
   static constexpr int TS = 4 * TSE;            // doubles of one slot (four elements)
   static constexpr int NYL = aq::cdiv(N1, 2);   // vertical output nodes scattered per lane
-  static constexpr int SMEM = (BM + BT + W * R * TS) * 8 + W * R * 8;
+  static constexpr int SMEM = (BM + BMT + BT + W * R * TS) * 8 + W * R * 8;
+  static_assert(TSE % 16 == 8 && LDA % 16 == 8, "bank layout");
   static_assert(SMEM <= 227 * 1024, "apply_quad shared memory");
 };
 
-// host: Bm [3][ROWSA][LDM] (Br, Bs, B0 at [a][m]) followed by Bt, Dt [q][l]
+// host: Bm [3][ROWSA][LDM] (Br, Bs, B0 at [a][m]), BmT [3][8 NM][LDA] (the same at [m][a]),
+// then Bt, Dt [q][l]
 std::vector<double> quad_apply_mats(const LevelRef& R) {
   auto run = [&](auto tag) {
     using D = AQ<decltype(tag)::value>;
-    std::vector<double> v(D::BM + D::BT, 0.0);
+    std::vector<double> v(D::BM + D::BMT + D::BT, 0.0);
     const double* B[3] = {R.Br.data(), R.Bs.data(), R.B0.data()};
     for (int c = 0; c < 3; ++c)
       for (int a = 0; a < D::QT; ++a)
-        for (int m = 0; m < D::NT; ++m) v[(c * D::ROWSA + a) * D::LDM + m] = B[c][a * D::NT + m];
+        for (int m = 0; m < D::NT; ++m) {
+          v[(c * D::ROWSA + a) * D::LDM + m] = B[c][a * D::NT + m];
+          v[D::BM + (c * 8 * D::NM + m) * D::LDA + a] = B[c][a * D::NT + m];
+        }
     for (int i = 0; i < D::QV * D::N1; ++i) {
-      v[D::BM + i] = R.Bt[i];
-      v[D::BM + D::QV * D::N1 + i] = R.Dt[i];
+      v[D::BM + D::BMT + i] = R.Bt[i];
+      v[D::BM + D::BMT + D::QV * D::N1 + i] = R.Dt[i];
     }
     return v;
   };
@@ -103,13 +113,14 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
   using D = AQ<P>;
   extern __shared__ __align__(128) double sm[];
   double* Bm = sm;                        // [3][ROWSA][LDM]
-  double* sBt = sm + D::BM;               // [QV][N1]
+  double* BmT = sm + D::BM;               // [3][8 NM][LDA]
+  double* sBt = BmT + D::BMT;             // [QV][N1]
   double* sDt = sBt + D::QV * D::N1;
-  double* ringall = sm + D::BM + D::BT;   // [W][R][4][TSE]
+  double* ringall = sm + D::BM + D::BMT + D::BT;   // [W][R][4][TSE]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(ringall + D::W * D::R * D::TS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r4 = lane >> 2, c4 = lane & 3, el = r4 & 3, h = r4 >> 2;
-  for (int i = tid; i < D::BM + D::BT; i += 32 * D::W) sm[i] = __ldg(mats + i);
+  for (int i = tid; i < D::BM + D::BMT + D::BT; i += 32 * D::W) sm[i] = __ldg(mats + i);
   if (lane == 0) {
     for (int b = 0; b < D::R; ++b)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(aq_smem(mbar + D::R * warp + b)));
@@ -229,8 +240,28 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
           double w0 = 0.0, w1 = 0.0, w2 = 0.0;
           if (ev && q < D::QV && al < nat) {
             const double* gp = Gt + qp * nat + al;
-            const double gxx = gp[0], gxy = gp[cs], gxz = gp[2 * cs], gyy = gp[3 * cs], gyz = gp[4 * cs],
-                         gzz = gp[5 * cs];
+            double gxx, gxy, gxz, gyy, gyz, gzz;
+            if ((D::NALAST & 1) == 0 || na < D::MTA - 1) {  // the pair (al, al + 1): one 16-byte load per component
+              const double2 v0 = *reinterpret_cast<const double2*>(gp - i);
+              const double2 v1 = *reinterpret_cast<const double2*>(gp - i + cs);
+              const double2 v2 = *reinterpret_cast<const double2*>(gp - i + 2 * cs);
+              const double2 v3 = *reinterpret_cast<const double2*>(gp - i + 3 * cs);
+              const double2 v4 = *reinterpret_cast<const double2*>(gp - i + 4 * cs);
+              const double2 v5 = *reinterpret_cast<const double2*>(gp - i + 5 * cs);
+              gxx = i ? v0.y : v0.x;
+              gxy = i ? v1.y : v1.x;
+              gxz = i ? v2.y : v2.x;
+              gyy = i ? v3.y : v3.x;
+              gyz = i ? v4.y : v4.x;
+              gzz = i ? v5.y : v5.x;
+            } else {
+              gxx = gp[0];
+              gxy = gp[cs];
+              gxz = gp[2 * cs];
+              gyy = gp[3 * cs];
+              gyz = gp[4 * cs];
+              gzz = gp[5 * cs];
+            }
             const double x0 = g[0][mt][i], x1 = g[1][mt][i], x2 = g[2][mt][i];
             w0 = gxx * x0 + gxy * x1 + gxz * x2;
             w1 = gxy * x0 + gyy * x1 + gyz * x2;
@@ -245,17 +276,20 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
       issue(t + D::R);
       // ---- stage B^T: V^T[(q,e)][m] += w^T[(q,e)][a] B_c[a][m]; k-step i <-> a = 8 na + 2 c4 + i
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int nm = 0; nm < D::NM; ++nm) {
+        // B^T operands of both k-steps (a = 8 na + 2 c4 + {0, 1}) in one 16-byte load per component
+        const int off = (8 * nm + r4) * D::LDA + 8 * na + 2 * c4;
+        const double2 br = *reinterpret_cast<const double2*>(BmT + off);
+        const double2 bs = *reinterpret_cast<const double2*>(BmT + 8 * D::NM * D::LDA + off);
+        const double2 b0 = *reinterpret_cast<const double2*>(BmT + 16 * D::NM * D::LDA + off);
 #pragma unroll
-        for (int nm = 0; nm < D::NM; ++nm) {
-          const int off = (8 * na + 2 * c4 + i) * D::LDM + 8 * nm + r4;
-          const double br = Bm[off], bs = Bm[D::ROWSA * D::LDM + off], b0 = Bm[2 * D::ROWSA * D::LDM + off];
-#pragma unroll
-          for (int mt = 0; mt < D::MTQ; ++mt) {
-            aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[0][mt][i], br);
-            aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[1][mt][i], bs);
-            aq_dmma(Vd[mt][nm][0], Vd[mt][nm][1], g[2][mt][i], b0);
-          }
+        for (int mt = 0; mt < D::MTQ; ++mt) {
+          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[0][mt][0], br.x);
+          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[1][mt][0], bs.x);
+          aq_dmma(Vd[mt][nm][0], Vd[mt][nm][1], g[2][mt][0], b0.x);
+          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[0][mt][1], br.y);
+          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[1][mt][1], bs.y);
+          aq_dmma(Vd[mt][nm][0], Vd[mt][nm][1], g[2][mt][1], b0.y);
         }
       }
     }

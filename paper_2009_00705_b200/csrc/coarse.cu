@@ -139,6 +139,129 @@ __global__ void k_coarse_next(double* cs, double maxit, cudaGraphConditionalHand
   cudaGraphSetConditional(h, go);
 }
 
+// ---- fused iteration (P = 1 element matrices available, default mode): three kernels per CG iteration
+__device__ __forceinline__ double cw_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// q = A_FF p (packed P = 1 element matrices, one thread per element) and p^T A p = sum_e p_e^T A_e p_e
+// (p = 0 on Dirichlet nodes, so the element energies sum to p^T q)
+__global__ void __launch_bounds__(128) k_coarse_apply_pq(int E, const int32_t* __restrict__ conn,
+                                                         const double* __restrict__ Aem, const double* __restrict__ p,
+                                                         double* __restrict__ q, double* pq) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  double en = 0.0;
+  if (e < E) {
+    int g[6];
+    double x[6], acc[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      g[i] = __ldg(conn + (size_t)e * 6 + i);
+      x[i] = g[i] >= 0 ? __ldg(p + g[i]) : 0.0;
+      acc[i] = 0.0;
+    }
+    int k = 0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int c2 = 0; c2 <= r; ++c2) {
+        const double a = __ldg(Aem + (size_t)(k++) * E + e);
+        acc[r] = fma(a, x[c2], acc[r]);
+        if (c2 != r) acc[c2] = fma(a, x[r], acc[c2]);
+      }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      en = fma(x[i], acc[i], en);
+      if (g[i] >= 0) atomicAdd(q + g[i], acc[i]);
+    }
+  }
+  __shared__ double sh[4];
+  en = cw_sum(en);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = en;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(pq, sh[0] + sh[1] + sh[2] + sh[3]);
+}
+
+// per line: x += alpha p, r -= alpha q (alpha = z.r / p.q), then z = T^-1 r; ||r||^2 and z.r
+__global__ void k_line_axpy_solve(int nlines, const int64_t* __restrict__ loff, const int32_t* __restrict__ lnode,
+                                  const double* __restrict__ ta, const double* __restrict__ tinv,
+                                  const double* __restrict__ tc, double* __restrict__ x, double* __restrict__ r,
+                                  const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ z,
+                                  double* cs) {
+  const double alpha = cs[CS_ZR_OLD] / cs[CS_PQ];
+  double s0 = 0.0, s1 = 0.0;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlines; l += gridDim.x * blockDim.x) {
+    const int64_t b = loff[l], e = loff[l + 1];
+    double d = 0.0;
+    for (int64_t t = b; t < e; ++t) {
+      const int32_t g = lnode[t];
+      x[g] = fma(alpha, p[g], x[g]);
+      const double rg = fma(-alpha, q[g], r[g]);
+      r[g] = rg;
+      s1 = fma(rg, rg, s1);
+      d = (rg - ta[t] * d) * tinv[t];
+      z[g] = d;
+    }
+    double xx = 0.0;
+    for (int64_t t = e - 1; t >= b; --t) {
+      const int32_t g = lnode[t];
+      xx = z[g] - tc[t] * xx;
+      z[g] = xx;
+      s0 = fma(xx, r[g], s0);
+    }
+  }
+  __shared__ double sh0[32], sh1[32];
+  s0 = cw_sum(s0);
+  s1 = cw_sum(s1);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh0[w] = s0;
+    sh1[w] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      a += sh0[i];
+      b += sh1[i];
+    }
+    atomicAdd(cs + CS_ZR_NEW, a);
+    atomicAdd(cs + CS_RR, b);
+  }
+}
+
+// p = z + beta p (beta = z.r_new / z.r_old), q = 0 for the next apply; the last block to finish
+// shifts z.r, counts the iteration, zeroes the reduction slots and sets the WHILE condition
+__global__ void k_coarse_update(int64_t n, double* __restrict__ p, const double* __restrict__ z,
+                                double* __restrict__ q, double* cs, unsigned int* done, double maxit,
+                                cudaGraphConditionalHandle h) {
+  const double beta = cs[CS_ZR_NEW] / cs[CS_ZR_OLD];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    p[i] = fma(beta, p[i], z[i]);
+    q[i] = 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {  // every block has read beta
+      __threadfence();
+      const double rr = cs[CS_RR];
+      cs[CS_ZR_OLD] = cs[CS_ZR_NEW];
+      cs[CS_IT] += 1.0;
+      cs[CS_TOTAL] += 1.0;
+      const unsigned go = (rr > cs[CS_THR2] && cs[CS_IT] < maxit) ? 1u : 0u;
+      cs[CS_PQ] = 0.0;
+      cs[CS_RR] = 0.0;
+      cs[CS_ZR_NEW] = 0.0;
+      cs[CS_RR_DUP] = 0.0;
+      *done = 0u;
+      cudaGraphSetConditional(h, go);
+    }
+  }
+}
+
 static void line_solve(sem_ctx* c, const double* r, double* z, double* out2) {
   Coarse& C = c->C;
   const int gb = cgrid(C.nlines, 128);
@@ -209,6 +332,8 @@ void setup_coarse_lines(sem_ctx* c, const std::vector<int32_t>& conn, const std:
   C.tc = upload(c, tc);
   C.cs = dalloc<double>(c, CS_N);
   CUDA_CHECK(cudaMemset(C.cs, 0, CS_N * sizeof(double)));
+  C.done = dalloc<unsigned int>(c, 1);
+  CUDA_CHECK(cudaMemset(C.done, 0, sizeof(unsigned int)));
   CUDA_CHECK(cudaMemset(C.z, 0, n * sizeof(double)));
 }
 
@@ -234,6 +359,7 @@ static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
   launch_init_masked(c, li, b, C.r, 1);
   line_solve(c, C.r, C.z, cs + CS_ZR_NEW);  // [ZR_NEW] = z.r, [RR_DUP] = r.r
   launch_xpby(c, n, C.p, C.z, nullptr, nullptr, 1);
+  launch_init_masked(c, li, nullptr, C.q, 1);   // q = 0 (the fused body re-zeroes it every iteration)
   cudaStreamCaptureStatus st;
   cudaGraph_t graph = nullptr;
   const cudaGraphNode_t* deps = nullptr;
@@ -261,6 +387,22 @@ static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
   c->stream = C.body_stream;
   const int64_t l0 = c->launches;
   try {
+    if (L.Ae1 && !c->det.on && L.N == 6) {
+      // fused: [q = A p, p.q] -> [x, r update, z = T^-1 r, ||r||^2, z.r] -> [p = z + beta p, q = 0, stop test]
+      const int E = c->E;
+      k_coarse_apply_pq<<<(E + 127) / 128, 128, 0, c->stream>>>(E, L.conn, L.Ae1, C.p, C.q, cs + CS_PQ);
+      k_line_axpy_solve<<<cgrid(C.nlines, 128), 128, 0, c->stream>>>(C.nlines, C.loff, C.lnode, C.ta, C.tinv, C.tc,
+                                                                     x, C.r, C.p, C.q, C.z, cs);
+      const int gu = cgrid(n, 256);
+      k_coarse_update<<<gu, 256, 0, c->stream>>>(n, C.p, C.z, C.q, cs, C.done, (double)c->opts.coarse_maxit, h);
+      CUDA_CHECK(cudaGetLastError());
+      c->launches += 3;
+      C.body_launches = c->launches - l0;
+      c->stream = keep;
+      cudaGraph_t g2 = nullptr;
+      CUDA_CHECK(cudaStreamEndCapture(C.body_stream, &g2));
+      return;
+    }
     // q = A p; p.q; x += alpha p, r -= alpha q (||r||^2); z = T^-1 r (z.r); p = z + beta p; stop test
     launch_init_masked(c, li, nullptr, C.q, 1);
     launch_apply(c, li, C.p, C.q, 0);

@@ -170,6 +170,7 @@ struct Coarse {
   int32_t* lnode = nullptr;     // [nfree] node of every line position
   double *ta = nullptr, *tinv = nullptr, *tc = nullptr;   // Thomas factors per line position
   double* cs = nullptr;         // device scalars of the solve (coarse.cu CS_*)
+  unsigned int* done = nullptr; // block-completion counter of k_coarse_update
   cudaGraphExec_t exec = nullptr;                 // standalone graph of the solve (coarsest L.f -> L.u)
   cudaStream_t cap_stream = nullptr, body_stream = nullptr;
   int64_t exec_launches = 0, body_launches = 0;

@@ -7,7 +7,10 @@ import sys
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__inst_executed.sum"]
+        "smsp__inst_executed.sum", "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"]
 SECTIONS = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Scheduler Statistics", "Occupancy",
             "Warp State Statistics", "Compute Workload Analysis")
 
