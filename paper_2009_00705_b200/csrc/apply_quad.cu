@@ -195,9 +195,29 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
     for (int mt = 0; mt < D::MTQ; ++mt)
 #pragma unroll
       for (int nm = 0; nm < D::NM; ++nm) Vt[mt][nm][0] = Vt[mt][nm][1] = Vd[mt][nm][0] = Vd[mt][nm][1] = 0.0;
+    // next quad's gather, prefetched into L1 during this quad (only 2 warps per scheduler: the
+    // connectivity -> u dependent loads of a quad start would otherwise stall the warp)
+    constexpr int NPF = (4 * D::N + 31) / 32;
+    const int qn = qd + qstride;
+    int pf[NPF];
 #pragma unroll 1
     for (int na = 0; na < D::MTA; ++na) {
       const int t = tk + na;
+      if (na == 0 && qn < nquad) {
+#pragma unroll
+        for (int k = 0; k < NPF; ++k) {
+          const int i = lane + 32 * k;
+          pf[k] = (i < 4 * D::N && 4 * qn + i / D::N < E) ? __ldg(conn + (size_t)4 * qn * D::N + i) : INT_MIN;
+        }
+      }
+      if (na == 1 && qn < nquad) {
+#pragma unroll
+        for (int k = 0; k < NPF; ++k)
+          if (pf[k] != INT_MIN) {
+            const double* a = u + (pf[k] >= 0 ? pf[k] : ~pf[k]);
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+          }
+      }
       {  // wait for copy t
         const uint32_t mb = aq_smem(mbar + D::R * warp + t % D::R);
         const uint32_t par = (uint32_t)(t / D::R) & 1u;
