@@ -90,7 +90,8 @@ typedef struct {
                                  tensor-core (DMMA) sum factorisation, one warp per element with
                                  TMA-staged geometric factors (p <= 6; p = 7, 8 use variant 2);
                                  1 CUDA-core FMA sum factorisation (reference variant);
-                                 2 DMMA with CTA-wide element batches                                */
+                                 2 DMMA with CTA-wide element batches; 3 DMMA with four elements per
+                                 warp (k_apply_quad, 3 <= p <= 5; the default (0) uses it at p = 3)    */
   int coarse_solver;          /* P=1 solve (reading O9): 0 auto (dense inverse if <= 46,000 free
                                  nodes, else iterative), 1 iterative (Jacobi-PCG, the outer PCG becomes
                                  flexible), 2 dense                                                  */

@@ -292,7 +292,11 @@ void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) 
       return;
     }
   }
-  if (!c->det.on && c->opts.apply_kernel == 3 && launch_apply_quad(c, level, u, y, flags)) return;
+  // default (0): the four-elements-per-warp kernel at p = 3 (measured 80 vs 97 us on config 3's p = 3
+  // level), the warp-per-element kernel at p = 4..6 (quad: 427 vs 299 us at p = 5)
+  if (!c->det.on && (c->opts.apply_kernel == 3 || (c->opts.apply_kernel == 0 && c->L[level].p == 3)) &&
+      launch_apply_quad(c, level, u, y, flags))
+    return;
   if (!c->det.on && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3) && launch_apply_warp(c, level, u, y, flags))
     return;
   if (!c->det.on && c->opts.apply_kernel != 1) {
