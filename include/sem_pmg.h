@@ -227,15 +227,22 @@ int laplace_solve(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
 int laplace_solve_guess(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
                         double tol, double *phi, sem_report *rep);
 
-/* New element geometry for the next time stage:
- * node_xyz is the nodal map in sem_mesh.node_xyz's layout (host, copied), with
- * the same mesh topology.  strategy 1 (the paper's strategy I): only the finest
- * operator follows the new geometry; the Schwarz inverses / FDM factors, the
- * coarse-level operators and the coarse inverse stay those of sem_setup (t = 0).
- * strategy 2: the operators of every level follow it (G, the P <= 2 element
- * matrices), the smoothers and the coarse inverse stay.  Node coordinates
- * (sem_node_xyz) are updated on the refreshed levels.  Single-domain ctx only.
- * Errors: SEM_EINVAL, SEM_EBADELEM (detJ <= 0), SEM_EUNSUPPORTED. */
+/* New element geometry for the next time stage (Fig 5.1;
+ * readings O41, O42): node_xyz is the nodal map in sem_mesh.node_xyz's layout (host,
+ * copied), with the same mesh topology.
+ *   strategy 1 (the paper's strategy I): only the finest operator follows the new
+ *     geometry; the Schwarz inverses / FDM factors, the coarse-level operators and the
+ *     coarse inverse stay those of sem_setup (t = 0);
+ *   strategy 2 ("operators only", not one of the paper's strategies): the operators
+ *     of every level follow it (G, the P <= 2 element matrices), the smoothers and the
+ *     coarse inverse stay;
+ *   strategy 4 (the paper's strategy III): every level's operator AND smoother (FDM
+ *     vertical factors, re-formed on the device) and the iterative coarse solve's
+ *     line-Jacobi preconditioner follow it; needs local_solve = 1 and coarse_solver
+ *     = 1 (SEM_EUNSUPPORTED otherwise).  Strategy II (3) needs the still-water
+ *     geometry: FNPF stages only (sem_fnpf_init).
+ * Node coordinates (sem_node_xyz) are updated on the refreshed levels.  Single-domain
+ * ctx only.  Errors: SEM_EINVAL, SEM_EBADELEM (detJ <= 0), SEM_EUNSUPPORTED. */
 int sem_update_geometry(sem_ctx *ctx, const double *node_xyz, int strategy);
 
 /* laplace_solve with HOST buffers (pinned recommended): copies rhs (if not
@@ -277,7 +284,12 @@ int sem_bench_kernel(sem_ctx *ctx, int kernel, int level, int reps, double *mean
  * sem_fnpf_init: node_xyz = the nodal map passed to sem_setup (host, [n_prism][N][3],
  * copied); strategy 1 = the paper's strategy I (only the finest operator follows the
  * free surface; smoothers and coarse operators from t = 0), 2 = every
- * level's operator follows it (smoothers and coarse inverse from t = 0). */
+ * level's operator follows it (smoothers and coarse inverse from t = 0), 3 = strategy
+ * II (the finest operator and smoother follow the free surface every stage; the
+ * coarse levels use the still-water (eta = 0) "LIN" operators and smoothers, formed
+ * here once), 4 = strategy III (every level's operator and smoother, and the coarse
+ * preconditioner, follow it every stage).  3 and 4 need local_solve = 1 (FDM smoother
+ * re-formation on the device); 4 needs coarse_solver = 1. */
 int sem_fnpf_init(sem_ctx *ctx, const double *node_xyz, int strategy, int64_t *n_surface);
 /* library node id (finest level) of every free-surface node, host [n_surface] */
 int sem_fnpf_surface_nodes(const sem_ctx *ctx, int32_t *node_ids);

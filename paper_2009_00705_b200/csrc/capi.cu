@@ -317,6 +317,31 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
 
 void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cublasHandle_t blas, int verbose);
 
+// the dense coarse inverse re-formed from the coarsest level's current G (FNPF strategy II at
+// initialisation; cuSOLVER, setup-time only)
+void coarse_rebuild_dense(sem_ctx* c) {
+  DeviceLevel& L = c->L.back();
+  LevelTopo T;
+  T.p = L.p;
+  T.N = L.N;
+  T.n = L.n;
+  T.nfree = L.nfree;
+  T.conn = L.conn_host;
+  T.dir = L.dir_host;
+  cusolverDnHandle_t sol;
+  CUSOLVER_CHECK(cusolverDnCreate(&sol));
+  struct HG {
+    cusolverDnHandle_t s;
+    ~HG() { cusolverDnDestroy(s); }
+  } hg{sol};
+  CUSOLVER_CHECK(cusolverDnSetStream(sol, c->stream));
+  Scratch s2;
+  c->C.Apack = nullptr;
+  c->C.Apack32 = nullptr;
+  c->C.Afull = nullptr;
+  setup_coarse(c, T, sol, s2.put(L.ref.Dfull));
+}
+
 void check_opts(const sem_opts& o) {
   if (o.local_solve < 0 || o.local_solve > 1) throw SemError(SEM_EINVAL, "bad options: local_solve");
   if (o.mixed_precision < 0 || o.mixed_precision > 1) throw SemError(SEM_EINVAL, "bad options: mixed_precision");
@@ -1026,15 +1051,18 @@ int laplace_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol,
 }
 
 int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
-  if (!c || !node_xyz || (strategy != 1 && strategy != 2)) return SEM_EINVAL;
+  if (!c || !node_xyz || (strategy != 1 && strategy != 2 && strategy != 4)) return SEM_EINVAL;
   if (c->dist) return SEM_EUNSUPPORTED;
   DeviceGuard guard(c->device);
   try {
+    if (strategy == 4 && c->L.size() > 1 && (!c->L[0].fdm || !c->C.iterative))
+      throw SemError(SEM_EUNSUPPORTED, "strategy III (4) re-forms smoothers and coarse preconditioner every stage: "
+                                       "needs local_solve = 1 and coarse_solver = 1");
     const int p = c->P, Nf = n_prism(p), E = c->E;
     std::vector<double> X(node_xyz, node_xyz + (size_t)E * Nf * 3);
     Scratch sc;
     const double* d_X = sc.put(X);
-    const int nlev = (strategy == 1) ? 1 : (int)c->L.size();
+    const int nlev = (strategy == 1) ? 1 : (int)c->L.size();   // 2, 4: every level's operator
     for (int li = 0; li < nlev; ++li) {
       DeviceLevel& L = c->L[li];
       Scratch s2;
@@ -1047,6 +1075,10 @@ int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
         build_p1_matrices(c, li, d_D);
       }
       level_xyz(L, p, X, L.conn_host, L.owner_host, E, false);
+    }
+    if (strategy == 4 && c->L.size() > 1) {  // III: every smoother and the coarse preconditioner too
+      for (size_t li = 0; li + 1 < c->L.size(); ++li) fdm_refresh_vertical(c, (int)li, d_X);
+      coarse_refresh_lines(c);
     }
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
   } catch (const SemError& e) {

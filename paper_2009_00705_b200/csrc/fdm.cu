@@ -182,6 +182,14 @@ __global__ void k_pad_vertical(int E, int nvp, const int32_t* __restrict__ nv, c
   }
 }
 
+void k_pad_vertical_launch(sem_ctx* c, int li) {
+  DeviceLevel& L = c->L[li];
+  const int E = c->E, nvp = 8 * L.f_nvt;
+  k_pad_vertical<<<(E + 127) / 128, 128, 0, c->stream>>>(E, nvp, L.f_nv, L.f_voff, L.f_lvoff, L.f_Sv, L.f_lv, L.f_Svp,
+                                                        L.f_lvp);
+  CUDA_CHECK(cudaGetLastError());
+}
+
 void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cublasHandle_t blas, int verbose) {
   DeviceLevel& L = c->L[li];
   const double t0 = now_ms();
@@ -209,6 +217,19 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
   batched_geneig(c, sol, blas, nv, std::vector<int64_t>(F.voff.begin(), F.voff.end() - 1), F.Kv, F.Mv, lvoff, L.f_Sv,
                  L.f_lv);
   L.f_col = upload(c, F.col);
+  L.f_cfirst = upload(c, F.cfirst);
+  {  // 1D GLL stiffness / mass of the reference layer (per-stage vertical re-formation, stage.cu)
+    const LevelRef R = make_level_ref(F.p);
+    const Rule1D gv = gauss_legendre_rule(F.p + 1);
+    std::vector<double> km(2 * R.n1 * R.n1, 0.0);
+    for (int a = 0; a < R.n1; ++a)
+      for (int b = 0; b < R.n1; ++b)
+        for (int q = 0; q < R.qv; ++q) {
+          km[a * R.n1 + b] += gv.w[q] * R.Dt[q * R.n1 + a] * R.Dt[q * R.n1 + b];
+          km[R.n1 * R.n1 + a * R.n1 + b] += gv.w[q] * R.Bt[q * R.n1 + a] * R.Bt[q * R.n1 + b];
+        }
+    L.f_kmref = upload(c, km);
+  }
   L.f_hoff = upload(c, F.hoff);
   L.f_moff = upload(c, F.moff);
   L.f_nv = upload(c, F.nv);

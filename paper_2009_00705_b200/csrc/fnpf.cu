@@ -175,7 +175,11 @@ __global__ void k_fnpf_rk4(int64_t n, double* __restrict__ x, const double* __re
 // ---------------------------------------------------------------- setup
 void fnpf_init(sem_ctx* c, const double* node_xyz, int strategy) {
   if (c->dist) throw SemError(SEM_EUNSUPPORTED, "FNPF stages: single-domain ctx only");
-  if (strategy != 1 && strategy != 2) throw SemError(SEM_EINVAL, "strategy must be 1 or 2");
+  if (strategy < 1 || strategy > 4) throw SemError(SEM_EINVAL, "strategy must be 1..4");
+  if (strategy >= 3 && c->L.size() > 1 && !c->L[0].fdm)
+    throw SemError(SEM_EUNSUPPORTED, "strategies II / III re-form the smoothers every stage: local_solve = 1 (FDM)");
+  if (strategy == 4 && c->L.size() > 1 && !c->C.iterative)
+    throw SemError(SEM_EUNSUPPORTED, "strategy III re-forms the coarse operator every stage: coarse_solver = 1");
   if (!c->fnpf) c->fnpf = new Fnpf();
   Fnpf& F = *c->fnpf;
   F.strategy = strategy;
@@ -282,20 +286,35 @@ void fnpf_init(sem_ctx* c, const double* node_xyz, int strategy) {
   CUDA_CHECK(cudaMemset(F.phi, 0, n0 * 8));
   F.warm = 0;
   F.geom_t0 = 1;
+  if (strategy == 3 && c->L.size() > 1) {
+    // strategy II (reading O41): the coarse levels' "LIN" operators and smoothers are those of the
+    // still-water geometry (eta = 0), formed once here
+    double* Xf = dalloc<double>(c, X.size());
+    CUDA_CHECK(cudaMemcpy(Xf, F.X0, X.size() * 8, cudaMemcpyDeviceToDevice));
+    double* zero = dalloc<double>(c, F.ns);
+    CUDA_CHECK(cudaMemset(zero, 0, F.ns * 8));
+    const int64_t EN = (int64_t)E * Nf;
+    k_fnpf_z<<<fgrid(EN, 256), 256, 0, c->stream>>>(EN, c->L[0].conn, F.gline, F.gsig, F.zb, zero, Xf);
+    CUDA_CHECK(cudaGetLastError());
+    const int nl = (int)c->L.size();
+    for (int li = 1; li < nl; ++li) refresh_level_operator(c, li, Xf, F.gm[li], F.wq[li]);
+    for (int li = 1; li + 1 < nl; ++li) fdm_refresh_vertical(c, li, Xf);
+    if (c->C.iterative) coarse_refresh_lines(c);
+    else coarse_rebuild_dense(c);
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  }
 }
 
-// operators of the refreshed levels from the nodal map X (strategy 1: finest only)
+// operators (and, strategies 3 / 4, smoothers) of the levels that follow the free surface (stage.cu)
 static void fnpf_geometry(sem_ctx* c, const double* X) {
   Fnpf& F = *c->fnpf;
-  const int nlev = F.strategy == 1 ? 1 : (int)c->L.size();
-  for (int li = 0; li < nlev; ++li) {
-    DeviceLevel& L = c->L[li];
-    if (launch_geometry(c, li, X, F.gm[li], F.Nf, F.wq[li])) throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
-    if (L.Gw) build_g_tiles(c, li);
-    if (L.Ae1) {
-      Scratch s2;
-      build_p1_matrices(c, li, s2.put(L.ref.Dfull));
-    }
+  const int nl = (int)c->L.size(), st = F.strategy;
+  const int nop = (st == 1 || st == 3) ? 1 : nl;
+  for (int li = 0; li < nop; ++li) refresh_level_operator(c, li, X, F.gm[li], F.wq[li]);
+  if (st == 3 && nl > 1) fdm_refresh_vertical(c, 0, X);
+  if (st == 4) {
+    for (int li = 0; li + 1 < nl; ++li) fdm_refresh_vertical(c, li, X);
+    if (nl > 1) coarse_refresh_lines(c);
   }
 }
 

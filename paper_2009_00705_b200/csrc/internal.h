@@ -90,6 +90,8 @@ struct DeviceLevel {
   // FDM local solves (opts.local_solve = 1; fdm.cu, reading O33)
   int fdm = 0, f_nh_max = 0, f_nv_max = 0;
   int32_t* f_col = nullptr;     // [E] column of every element
+  int64_t* f_cfirst = nullptr;  // [ncol+1] first element slot of every column in f_colel
+  double* f_kmref = nullptr;    // [2][n1][n1] 1D GLL stiffness / mass of the reference layer
   int64_t *f_hoff = nullptr, *f_moff = nullptr;   // [ncol+1] patch / S_h offsets
   int32_t* f_nv = nullptr;      // [E] vertical box size
   int64_t *f_voff = nullptr, *f_lvoff = nullptr, *f_ioff = nullptr;   // [E(+1)] S_v / l_v / index offsets
@@ -253,6 +255,11 @@ void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double*
 int64_t coarse_iters(sem_ctx* c, bool reset);
 void coarse_reset_iters(sem_ctx* c);
 void coarse_destroy(sem_ctx* c);
+// stage.cu: per-stage re-formation (strategies of P:350-356)
+void fdm_refresh_vertical(sem_ctx* c, int li, const double* X);
+void coarse_refresh_lines(sem_ctx* c);
+void coarse_rebuild_dense(sem_ctx* c);   // capi.cu: the dense coarse inverse from the current G (setup-time)
+void refresh_level_operator(sem_ctx* c, int li, const double* X, const double* d_gm, const double* d_w);
 // fnpf.cu: FNPF time stage (eq 2.1)
 void fnpf_init(sem_ctx* c, const double* node_xyz, int strategy);
 void fnpf_stage(sem_ctx* c, const double* eta, const double* phis, double* deta, double* dphis, double* w,

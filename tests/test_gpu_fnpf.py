@@ -23,8 +23,8 @@ if not torch.cuda.is_available():
 import paper_2009_00705_b200 as lib  # noqa: E402
 
 
-def _setup(m, strategy=1):
-    s = make_solver(m)
+def _setup(m, strategy=1, **kw):
+    s = make_solver(m, **kw)
     ids = s.fnpf_init(m.node_xyz(lib.reference_nodes(m.p)), strategy=strategy)
     S = fnpf.Surface(m, m.p)
     lib_xy = s.node_xyz(0)[ids]
@@ -42,12 +42,15 @@ def _state(S, seed):
     return eta, phis
 
 
-@pytest.mark.parametrize("strategy", [1, 2])
+@pytest.mark.parametrize("strategy", [1, 2, 3, 4])
 def test_fnpf_rates_parity(strategy):
     """Rates of eq 2.1 at a curved, moving surface (config 2 construction, p = 4):
-    GPU (PCG-p-MG to 1e-13) vs oracle (sparse direct) at every surface node."""
+    GPU (PCG-p-MG to 1e-13) vs oracle (sparse direct) at every surface node, for the
+    paper's strategies I (1), II (3), III (4) and operators-only (2): the strategy
+    changes the preconditioner, never the solution."""
     m = config2(p=4, nx=16, ny=2, nz=2)
-    s, S, perm, _ = _setup(m, strategy)
+    kw = dict(local_solve=1, coarse_solver=1, coarse_rtol=1e-13) if strategy >= 3 else {}
+    s, S, perm, _ = _setup(m, strategy, **kw)
     eta, phis = _state(S, 1)
     de_o, dp_o, w_o = fnpf.surface_rhs(S, eta, phis)
     t = lambda v: torch.from_numpy(np.ascontiguousarray(v[perm])).cuda()
@@ -98,3 +101,35 @@ def test_fnpf_standing_wave_period(linear):
         s.fnpf_erk4_step(te, tp, T / 32, 1e-12, linear=linear)
     assert np.linalg.norm(te.cpu().numpy() - eta0) <= (1e-3 if linear else 3e-2) * np.linalg.norm(eta0)
     s.close()
+
+
+def test_fnpf_strategy_III_smoother_equals_fresh_setup():
+    """Strategy III after one stage: the FDM smoothers re-formed on the device equal a
+    fresh setup on the staged geometry (the oracle's sigma-map nodal map of O37)."""
+    m = config2(p=4, nx=16, ny=2, nz=2)
+    kw = dict(local_solve=1, coarse_solver=1, coarse_rtol=1e-13)
+    s, S, perm, _ = _setup(m, 4, **kw)
+    eta, phis = _state(S, 4)
+    t = lambda v: torch.from_numpy(np.ascontiguousarray(v[perm])).cuda()
+    s.fnpf_rhs(t(eta), t(phis), 1e-10)
+    staged = fnpf.StagedMesh(S, eta)
+    fresh = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=_lib_order_nodes(staged, m.p), **kw)
+    from workloads import random_vector
+    for li in range(s.info["n_levels"] - 1):
+        r = torch.from_numpy(random_vector(s.n_dof(li), 70 + li)).cuda()
+        a, b = s.empty(li), fresh.empty(li)
+        s.schwarz(li, r, a)
+        fresh.schwarz(li, r, b)
+        assert rel(a.cpu().numpy(), b.cpu().numpy()) <= 1e-12
+    s.close()
+    fresh.close()
+
+
+def _lib_order_nodes(staged, p):
+    """The staged nodal map at the LIBRARY's reference nodes (its local order): the
+    oracle's nodes matched by reference coordinates."""
+    rst_lib = lib.reference_nodes(p)
+    rst_orc, _ = fnpf.R.prism_nodes(p)
+    d, idx = cKDTree(rst_orc).query(rst_lib)
+    assert d.max() < 1e-12
+    return staged.node_xyz(rst_orc)[:, idx, :]
