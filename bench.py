@@ -293,6 +293,43 @@ def solve_roofline(s, rep, ms, peak, nu=(3, 3)):
             "note": "algorithmic bytes of every kernel of the solve (byte model of DESIGN.md §7) / solve time"}
 
 
+FNPF_VARIANTS = [("strategy I, exact dense ASM", dict(), 1),
+                 ("strategy III, FDM ASM + line-Jacobi coarse PCG", dict(local_solve=1, coarse_solver=1), 4)]
+
+
+def run_fnpf(args, lib, m, dt=0.05, steps=3):
+    """NEXT-4 / NEXT-1: FNPF time stepping on the headline mesh (eq 2.1, ERK4 with one
+    warm-started Laplace solve per stage to the metric's tol), per-stage PCG iterations
+    (the paper reports ~2 per stage at rtol 1e-7; context only)."""
+    import torch
+    out = []
+    nodes = m.node_xyz(lib.reference_nodes(m.p))
+    for name, kw, strategy in FNPF_VARIANTS:
+        s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=nodes, **kw)
+        ids = s.fnpf_init(nodes, strategy=strategy)
+        xyz = s.node_xyz(0)[ids]
+        eta = torch.from_numpy(xyz[:, 2].copy()).cuda()
+        phis = torch.from_numpy(m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])).cuda()
+        s.fnpf_erk4_step(eta, phis, dt, args.tol)            # warm-up step
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        its = 0
+        e0.record(s.stream)
+        for _ in range(steps):
+            its += s.fnpf_erk4_step(eta, phis, dt, args.tol)
+        e1.record(s.stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out.append({"variant": name, "strategy": strategy, "dt": dt, "steps": steps, "ms_per_step": ms,
+                    "stage_solves_per_s": 4.0 / (ms * 1e-3), "pcg_iters_per_stage": its / (4.0 * steps),
+                    "MDOF_s": s.info["n_free"] * 4.0 / (ms * 1e-3) / 1e6, "tol": args.tol,
+                    "eta_max": float(eta.abs().max().item())})
+        s.close()
+        del s
+        torch.cuda.empty_cache()
+    return out
+
+
 SWEEP = [("dense_o1", "exact dense local inverses, overlap 1 (the paper's smoother, eq 4.4, P:320)",
           dict(local_solve=0, overlap=1)),
          ("fdm_refined", "FDM local solves (O33), refined overlap ceil((P+1)/2) (P:536)",
@@ -479,6 +516,9 @@ def main():
             del s
             torch.cuda.empty_cache()
             variants.append(run_config5(args, lib, peak))
+    fnpf_block = None
+    if world == 1 and args.emulate_ranks <= 1 and not args.no_variants and args.config == "config3":
+        fnpf_block = run_fnpf(args, lib, m)
     if world == 1 and args.emulate_ranks <= 1 and not args.no_sweep and args.config == "config3":
         sweep = run_sweep(args)
     cpu = None
@@ -507,7 +547,7 @@ def main():
             "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "q_mean": rep["q_mean"],
             "work_units": ms_step * 1e3 / us_a,    # solve time / one finest operator apply (O25)
             "roofline": roof, "solve_roofline": sroof, "apply": apply, "variants": variants,
-            "config4_sweep": sweep, "cpu_baseline": cpu, "e2e": e2e,
+            "config4_sweep": sweep, "fnpf": fnpf_block, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
         }
