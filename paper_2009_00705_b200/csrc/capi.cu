@@ -869,6 +869,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   R.t_ms = ms;
   R.wu = c->t_apply_ms > 0 ? ms / c->t_apply_ms : 0.0;
   R.coarse_iters = (int)coarse_iters(c, false);
+  coarse_count_launches(c, R.coarse_iters);
   R.rel_res = nf > 0 ? rn / nf : 0.0;
   if (R.n_hist > 1) {
     const int m = R.n_hist - 1;

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -29,7 +30,7 @@ namespace sem {
 // device scalar slots of the coarse solve (C.cs)
 // (k_line_solve writes z.r and r.r to two consecutive slots: CS_ZR_NEW, CS_RR_DUP)
 enum : int { CS_PQ = 0, CS_RR = 1, CS_ZR_OLD = 2, CS_ZR_NEW = 3, CS_RR_DUP = 4, CS_THR2 = 6, CS_IT = 7,
-             CS_TOTAL = 8, CS_N = 16 };
+             CS_TOTAL = 8, CS_GO = 9, CS_N = 16 };
 static_assert(CS_RR_DUP == CS_ZR_NEW + 1, "line solve output slots");
 
 static int cgrid(int64_t n, int threads) {
@@ -112,7 +113,7 @@ __global__ void k_zero_slots(double* cs, int a, int b, int c2, int d) {
 }
 
 // after the prologue: thr^2 = rtol^2 ||b||^2 (||b||^2 = r.r of the initial residual), loop iff b != 0
-__global__ void k_coarse_start(double* cs, double rtol2, cudaGraphConditionalHandle h) {
+__global__ void k_coarse_start(double* cs, double rtol2, cudaGraphConditionalHandle h, int use_h) {
   cs[CS_THR2] = rtol2 * cs[CS_RR_DUP];
   cs[CS_IT] = 0.0;
   cs[CS_ZR_OLD] = cs[CS_ZR_NEW];
@@ -121,12 +122,13 @@ __global__ void k_coarse_start(double* cs, double rtol2, cudaGraphConditionalHan
   cs[CS_RR] = 0.0;
   cs[CS_ZR_NEW] = 0.0;
   cs[CS_RR_DUP] = 0.0;
-  cudaGraphSetConditional(h, go);
+  cs[CS_GO] = go;
+  if (use_h) cudaGraphSetConditional(h, go);
 }
 
 // end of one CG iteration: beta used, shift z.r, count, stop test ||r||^2 <= thr^2 or maxit,
 // zero the reduction slots of the next iteration
-__global__ void k_coarse_next(double* cs, double maxit, cudaGraphConditionalHandle h) {
+__global__ void k_coarse_next(double* cs, double maxit, cudaGraphConditionalHandle h, int use_h) {
   const double rr = cs[CS_RR];
   cs[CS_ZR_OLD] = cs[CS_ZR_NEW];
   cs[CS_IT] += 1.0;
@@ -236,7 +238,7 @@ __global__ void k_line_axpy_solve(int nlines, const int64_t* __restrict__ loff, 
 // shifts z.r, counts the iteration, zeroes the reduction slots and sets the WHILE condition
 __global__ void k_coarse_update(int64_t n, double* __restrict__ p, const double* __restrict__ z,
                                 double* __restrict__ q, double* cs, unsigned int* done, double maxit,
-                                cudaGraphConditionalHandle h) {
+                                cudaGraphConditionalHandle h, int use_h) {
   const double beta = cs[CS_ZR_NEW] / cs[CS_ZR_OLD];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     p[i] = fma(beta, p[i], z[i]);
@@ -257,7 +259,8 @@ __global__ void k_coarse_update(int64_t n, double* __restrict__ p, const double*
       cs[CS_ZR_NEW] = 0.0;
       cs[CS_RR_DUP] = 0.0;
       *done = 0u;
-      cudaGraphSetConditional(h, go);
+      cs[CS_GO] = go;
+      if (use_h) cudaGraphSetConditional(h, go);
     }
   }
 }
@@ -344,22 +347,61 @@ void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double*
 }
 
 // ---------------------------------------------------------------- solve
-// Enqueue the whole PCG on c->stream, which must be capturing: prologue, then a
-// conditional WHILE node whose body (one CG iteration) is captured through a
-// second stream.  x = A_1^-1 b from x = 0.
-static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
+// prologue: x = 0, r = b (free nodes), z = T^-1 r, p = z; ||b||^2, z.r; the stop threshold and the
+// first loop condition (graph handle h when use_h, and cs[CS_GO] always)
+static void coarse_prologue(sem_ctx* c, const double* b, double* x, cudaGraphConditionalHandle h, int use_h) {
+  const int li = (int)c->L.size() - 1;
+  const DeviceLevel& L = c->L[li];
+  Coarse& C = c->C;
+  double* cs = C.cs;
+  k_zero_slots<<<1, 1, 0, c->stream>>>(cs, CS_ZR_NEW, CS_RR_DUP, -1, -1);
+  launch_init_masked(c, li, nullptr, x, 1);
+  launch_init_masked(c, li, b, C.r, 1);
+  line_solve(c, C.r, C.z, cs + CS_ZR_NEW);  // [ZR_NEW] = z.r, [RR_DUP] = r.r
+  launch_xpby(c, L.n, C.p, C.z, nullptr, nullptr, 1);
+  launch_init_masked(c, li, nullptr, C.q, 1);   // q = 0 (the fused body re-zeroes it every iteration)
+  const double rt = c->opts.coarse_rtol;
+  k_coarse_start<<<1, 1, 0, c->stream>>>(cs, rt * rt, h, use_h);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches += 2;
+}
+
+// one CG iteration; the last kernel sets the loop condition
+static void coarse_body(sem_ctx* c, double* x, cudaGraphConditionalHandle h, int use_h) {
   const int li = (int)c->L.size() - 1;
   const DeviceLevel& L = c->L[li];
   Coarse& C = c->C;
   const int64_t n = L.n;
   double* cs = C.cs;
-  // prologue: x = 0, r = b (free nodes), z = T^-1 r, p = z; ||b||^2, z.r
-  k_zero_slots<<<1, 1, 0, c->stream>>>(cs, CS_ZR_NEW, CS_RR_DUP, -1, -1);
-  launch_init_masked(c, li, nullptr, x, 1);
-  launch_init_masked(c, li, b, C.r, 1);
-  line_solve(c, C.r, C.z, cs + CS_ZR_NEW);  // [ZR_NEW] = z.r, [RR_DUP] = r.r
-  launch_xpby(c, n, C.p, C.z, nullptr, nullptr, 1);
-  launch_init_masked(c, li, nullptr, C.q, 1);   // q = 0 (the fused body re-zeroes it every iteration)
+  const double maxit = (double)c->opts.coarse_maxit;
+  if (L.Ae1 && !c->det.on && L.N == 6) {
+    // fused: [q = A p, p.q] -> [x, r update, z = T^-1 r, ||r||^2, z.r] -> [p = z + beta p, q = 0, stop test]
+    const int E = c->E;
+    k_coarse_apply_pq<<<(E + 127) / 128, 128, 0, c->stream>>>(E, L.conn, L.Ae1, C.p, C.q, cs + CS_PQ);
+    k_line_axpy_solve<<<cgrid(C.nlines, 128), 128, 0, c->stream>>>(C.nlines, C.loff, C.lnode, C.ta, C.tinv, C.tc,
+                                                                   x, C.r, C.p, C.q, C.z, cs);
+    k_coarse_update<<<cgrid(n, 256), 256, 0, c->stream>>>(n, C.p, C.z, C.q, cs, C.done, maxit, h, use_h);
+    CUDA_CHECK(cudaGetLastError());
+    c->launches += 3;
+    return;
+  }
+  // q = A p; p.q; x += alpha p, r -= alpha q (||r||^2); z = T^-1 r (z.r); p = z + beta p; stop test
+  launch_init_masked(c, li, nullptr, C.q, 1);
+  launch_apply(c, li, C.p, C.q, 0);
+  launch_dot2(c, n, C.p, C.q, nullptr, nullptr, nullptr, cs + CS_PQ, false);
+  launch_axpy_pcg(c, n, x, C.r, C.p, C.q, cs + CS_ZR_OLD, cs + CS_PQ, cs + CS_RR, nullptr, false);
+  line_solve(c, C.r, C.z, cs + CS_ZR_NEW);
+  launch_xpby(c, n, C.p, C.z, cs + CS_ZR_NEW, cs + CS_ZR_OLD, 0);
+  k_coarse_next<<<1, 1, 0, c->stream>>>(cs, maxit, h, use_h);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+}
+
+// Enqueue the whole PCG on c->stream, which must be capturing: prologue, then a conditional
+// WHILE node whose body (one CG iteration) is captured through a second stream.  x = A_1^-1 b
+// from x = 0.  The body's kernels are counted per executed iteration (coarse_count_launches).
+static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
+  Coarse& C = c->C;
   cudaStreamCaptureStatus st;
   cudaGraph_t graph = nullptr;
   const cudaGraphNode_t* deps = nullptr;
@@ -368,9 +410,7 @@ static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
   if (st != cudaStreamCaptureStatusActive) throw SemError(SEM_ECUDA, "coarse PCG emitted outside a capture");
   cudaGraphConditionalHandle h;
   CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
-  const double rt = c->opts.coarse_rtol;
-  k_coarse_start<<<1, 1, 0, c->stream>>>(cs, rt * rt, h);
-  c->launches += 2;
+  coarse_prologue(c, b, x, h, 1);
   CUDA_CHECK(cudaStreamGetCaptureInfo(c->stream, &st, nullptr, &graph, &deps, &ndeps));
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
@@ -387,32 +427,7 @@ static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
   c->stream = C.body_stream;
   const int64_t l0 = c->launches;
   try {
-    if (L.Ae1 && !c->det.on && L.N == 6) {
-      // fused: [q = A p, p.q] -> [x, r update, z = T^-1 r, ||r||^2, z.r] -> [p = z + beta p, q = 0, stop test]
-      const int E = c->E;
-      k_coarse_apply_pq<<<(E + 127) / 128, 128, 0, c->stream>>>(E, L.conn, L.Ae1, C.p, C.q, cs + CS_PQ);
-      k_line_axpy_solve<<<cgrid(C.nlines, 128), 128, 0, c->stream>>>(C.nlines, C.loff, C.lnode, C.ta, C.tinv, C.tc,
-                                                                     x, C.r, C.p, C.q, C.z, cs);
-      const int gu = cgrid(n, 256);
-      k_coarse_update<<<gu, 256, 0, c->stream>>>(n, C.p, C.z, C.q, cs, C.done, (double)c->opts.coarse_maxit, h);
-      CUDA_CHECK(cudaGetLastError());
-      c->launches += 3;
-      C.body_launches = c->launches - l0;
-      c->stream = keep;
-      cudaGraph_t g2 = nullptr;
-      CUDA_CHECK(cudaStreamEndCapture(C.body_stream, &g2));
-      return;
-    }
-    // q = A p; p.q; x += alpha p, r -= alpha q (||r||^2); z = T^-1 r (z.r); p = z + beta p; stop test
-    launch_init_masked(c, li, nullptr, C.q, 1);
-    launch_apply(c, li, C.p, C.q, 0);
-    launch_dot2(c, n, C.p, C.q, nullptr, nullptr, nullptr, cs + CS_PQ, false);
-    launch_axpy_pcg(c, n, x, C.r, C.p, C.q, cs + CS_ZR_OLD, cs + CS_PQ, cs + CS_RR, nullptr, false);
-    line_solve(c, C.r, C.z, cs + CS_ZR_NEW);
-    launch_xpby(c, n, C.p, C.z, cs + CS_ZR_NEW, cs + CS_ZR_OLD, 0);
-    k_coarse_next<<<1, 1, 0, c->stream>>>(cs, (double)c->opts.coarse_maxit, h);
-    CUDA_CHECK(cudaGetLastError());
-    c->launches++;
+    coarse_body(c, x, h, 1);
   } catch (...) {
     c->stream = keep;
     cudaGraph_t g2;
@@ -420,9 +435,18 @@ static void emit_coarse_pcg(sem_ctx* c, const double* b, double* x) {
     throw;
   }
   C.body_launches = c->launches - l0;
+  c->launches = l0;
   c->stream = keep;
   cudaGraph_t g2 = nullptr;
   CUDA_CHECK(cudaStreamEndCapture(C.body_stream, &g2));
+}
+
+static bool no_graphs() {
+  static const int off = [] {
+    const char* e = getenv("SEM_NO_GRAPHS");
+    return (e && atoi(e)) ? 1 : 0;
+  }();
+  return off != 0;
 }
 
 void coarse_pcg(sem_ctx* c, const double* b, double* x) {
@@ -431,6 +455,17 @@ void coarse_pcg(sem_ctx* c, const double* b, double* x) {
   CUDA_CHECK(cudaStreamIsCapturing(c->stream, &st));
   if (st == cudaStreamCaptureStatusActive) {
     emit_coarse_pcg(c, b, x);
+    return;
+  }
+  if (no_graphs()) {  // SEM_NO_GRAPHS=1 (profiling): host-driven loop, one condition read per iteration
+    coarse_prologue(c, b, x, 0, 0);
+    for (;;) {
+      double go = 0.0;
+      CUDA_CHECK(cudaMemcpyAsync(&go, C.cs + CS_GO, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      if (go == 0.0) break;
+      coarse_body(c, x, 0, 0);
+    }
     return;
   }
   // eager: replay the solve's own graph on the coarsest level's buffers
@@ -463,6 +498,11 @@ void coarse_pcg(sem_ctx* c, const double* b, double* x) {
   CUDA_CHECK(cudaGraphLaunch(C.exec, c->stream));
   c->launches += C.exec_launches;
   if (x != L.u) CUDA_CHECK(cudaMemcpyAsync(x, L.u, L.n * 8, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// graph-replayed WHILE bodies: add the kernels of the `iters` executed iterations to the count
+void coarse_count_launches(sem_ctx* c, int64_t iters) {
+  if (c->C.iterative && !no_graphs()) c->launches += iters * c->C.body_launches;
 }
 
 // total inner iterations since the last reset (synchronises the stream)

@@ -414,6 +414,7 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
   CUDA_CHECK(cudaEventElapsedTime(&ms, c0->ev0, c0->ev1));
   R.t_ms = ms;
   R.coarse_iters = (int)coarse_iters(D.coarse, false);
+  coarse_count_launches(D.coarse, R.coarse_iters);
   R.rel_res = nf > 0 ? rn / nf : 0.0;
   if (R.n_hist > 1) R.q_mean = std::pow(R.res_hist[R.n_hist - 1] / R.res_hist[0], 1.0 / (R.n_hist - 1));
   if (status == SEM_OK && !R.converged) status = SEM_ENOTCONV;

@@ -254,6 +254,7 @@ void setup_coarse_lines(sem_ctx* c, const std::vector<int32_t>& conn, const std:
 void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double* Ae, double* off);
 int64_t coarse_iters(sem_ctx* c, bool reset);
 void coarse_reset_iters(sem_ctx* c);
+void coarse_count_launches(sem_ctx* c, int64_t iters);
 void coarse_destroy(sem_ctx* c);
 // stage.cu: per-stage re-formation (strategies of P:350-356)
 void fdm_refresh_vertical(sem_ctx* c, int li, const double* X);
