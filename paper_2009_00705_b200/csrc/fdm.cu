@@ -1007,16 +1007,30 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   // 3. Ys = S_h Zs -> B2 over the stacked columns
   fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, soff[cnt], warp, lane);
   __syncthreads();
-  // 4. every column node of the unit: sum of the boxes holding it, scatter (x W for S^-1)
+  // 4. every column node of the unit: sum of the boxes holding it, scatter (x W for S^-1).
+  // The boxes are ordered by layer and their z ranges increase with j: the boxes holding z form
+  // a contiguous run [jlo, jhi], found per z from the unit's box table (fixed summation order j)
+  __shared__ short zj[2 * 8 * 16 + 2][2];
+  for (int z = tid; z < nzu; z += 256) {
+    int jlo = cnt, jhi = -1;
+    for (int j = 0; j < cnt; ++j) {
+      const int zz = z - (ez0[j] - zlo);
+      if (zz >= 0 && zz < env[j]) {
+        jlo = min(jlo, j);
+        jhi = max(jhi, j);
+      }
+    }
+    zj[z][0] = (short)jlo;
+    zj[z][1] = (short)jhi;
+  }
+  __syncthreads();
   for (int t = tid; t < nh * nzu; t += 256) {
     const int h = t / nzu, z = t - h * nzu;
     const int g = __ldg(ci + h * nz + zlo + z);
     if (g < 0) continue;
     double acc = 0.0;
-    for (int j = 0; j < cnt; ++j) {
-      const int zz = z - (ez0[j] - zlo);
-      if (!sk[j] && zz >= 0 && zz < env[j]) acc += B2[h * ldb + soff[j] + zz];
-    }
+    for (int j = zj[z][0]; j <= zj[z][1]; ++j)
+      if (!sk[j]) acc += B2[h * ldb + soff[j] + z - (ez0[j] - zlo)];
     if (!transpose) acc *= __ldg(W + g);
     atomicAdd(u + g, acc);
   }
