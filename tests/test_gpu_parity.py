@@ -6,6 +6,8 @@ rel. residual <= 1e-12.  Step bars (transfers, smoother, coarse solve, V-cycle)
 use the same 1e-12 bound: they are linear maps evaluated in FP64 whose only
 difference from the oracle is the summation order (DESIGN.md §"Tolerances").
 """
+import functools
+
 import numpy as np
 import pytest
 
@@ -229,21 +231,27 @@ def test_config4_construction_every_order(p, apply_kernel):
     kernels (0 = warp-per-element DMMA, 1 = FMA, 2 = batched DMMA, 3 = four elements per warp): apply and solve parity; p = 1 is the
     single-level coarse solve (O26).  3x3 (p <= 5) or 2x2 quads x 2 layers = 36 / 16
     prisms: several element batches with a ragged last batch for every p."""
-    from workloads.configs import basin
-    n = 2 if p >= 6 else 3
-    m = basin(f"c4r_p{p}", p, 32.0 * n / 56, n, 2, seed=4)
+    m, lev, phiD, phi_direct = _c4_oracle(p)      # the oracle side, shared by the four kernel variants
     s = make_solver(m, apply_kernel=apply_kernel)
-    lev = sem.build_system(m, p)
     perm = lib_to_oracle(s.node_xyz(0), lev.xyz)
     u = random_vector(lev.n, seed=p)
     y = s.apply(torch.from_numpy(u[perm]).cuda())
     out = np.zeros(lev.n)
     out[perm] = y.cpu().numpy()
     assert rel(out, lev.A @ u) <= APPLY_TOL
-    phiD = m.phi(*lev.xyz.T)
     phi, rep = s.solve(torch.from_numpy(phiD[perm]).cuda(), tol=1e-13)
     out[perm] = phi.cpu().numpy()
-    assert rel(out, sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+    assert rel(out, phi_direct) <= SOLVE_TOL
+
+
+@functools.lru_cache(maxsize=None)
+def _c4_oracle(p):
+    from workloads.configs import basin
+    n = 2 if p >= 6 else 3
+    m = basin(f"c4r_p{p}", p, 32.0 * n / 56, n, 2, seed=4)
+    lev = sem.build_system(m, p)
+    phiD = m.phi(*lev.xyz.T)
+    return m, lev, phiD, sem.solve_direct(lev, phiD)
 
 
 def test_solve_host_matches_device(c2):
