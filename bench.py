@@ -133,6 +133,14 @@ def oracle_sample(tol, budget_s=20.0):
             break
     t = statistics.median(times)
     nfree = len(lev.free)
+    # one fine-level SpMV of the assembled operator (the paper's work unit), single thread
+    import numpy as np
+    u = np.random.default_rng(0).uniform(-1, 1, lev.n)
+    t0, k = time.perf_counter(), 0
+    while time.perf_counter() - t0 < 1.0:
+        lev.A @ u
+        k += 1
+    t_spmv = (time.perf_counter() - t0) / k
     try:
         from threadpoolctl import threadpool_info
         thr = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
@@ -143,7 +151,7 @@ def oracle_sample(tol, budget_s=20.0):
                        f"patch: 8x8 quads x 2 layers = {m.n_elem} prisms, p=5, {nfree} free DOF; median of "
                        f"{len(times)} solves ({info['iters']} iterations); host cores available "
                        f"{len(os.sched_getaffinity(0))}",
-                t_solve_s=t, n_free=nfree, iters=info["iters"])
+                t_solve_s=t, n_free=nfree, iters=info["iters"], apply_spmv_MDOF_s=lev.n / t_spmv / 1e6)
 
 
 def run_reference(args, rank, world):
@@ -524,7 +532,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = oracle_sample(args.tol)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "apply_spmv_MDOF_s")}
     rep = reps[-1]
     if rank == 0:
         out = {

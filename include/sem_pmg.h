@@ -69,6 +69,10 @@ typedef struct {
   const uint8_t *face_tag;    /* [n_prism][5] faces (bot, top, q01, q12, q20), SEM_FACE_*            */
   const double *node_xyz;     /* [n_prism][N(p)][3] curvilinear nodes of the finest order in the local
                                  order above (the nodal element map), or NULL = straight-sided */
+  const int32_t *part;        /* optional [n_prism] owning rank of every prism for partitioned solves
+                                 (opts.nranks > 1), or NULL = the library's column partition (RCB of the
+                                 column centroids).  FDM local solves need whole columns per rank
+                                 (SEM_EUNSUPPORTED otherwise); ignored when nranks == 1. */
 } sem_mesh;
 
 typedef struct {

@@ -18,7 +18,7 @@ _dp = C.POINTER(C.c_double)
 class SemMesh(C.Structure):
     _fields_ = [("n_vert", C.c_int32), ("xyz", _dp), ("n_prism", C.c_int32),
                 ("prism", C.POINTER(C.c_int32)), ("face_tag", C.POINTER(C.c_uint8)),
-                ("node_xyz", _dp)]
+                ("node_xyz", _dp), ("part", C.POINTER(C.c_int32))]
 
 
 class SemOpts(C.Structure):
@@ -234,7 +234,7 @@ class Solver:
     """sem_setup(mesh, p) + the compute calls of include/sem_pmg.h."""
 
     def __init__(self, vertices, prisms, face_tag, p: int, node_xyz=None, *, levels=None, stream=None,
-                 nccl_id: bytes | None = None, **opts):
+                 nccl_id: bytes | None = None, part=None, **opts):
         import torch
         self._torch = torch
         o = SemOpts()
@@ -270,6 +270,10 @@ class Solver:
             nx = np.ascontiguousarray(node_xyz, dtype=np.float64)
             self._keep.append(nx)
             m.node_xyz = nx.ctypes.data_as(_dp)
+        if part is not None:
+            pa = np.ascontiguousarray(part, dtype=np.int32)
+            self._keep.append(pa)
+            m.part = pa.ctypes.data_as(C.POINTER(C.c_int32))
         self._ctx = C.c_void_p()
         _check(_lib.sem_setup(C.byref(m), p, C.byref(o), C.byref(self._ctx)), "sem_setup")
         self._keep = None

@@ -367,6 +367,12 @@ void prepare_global(const sem_mesh* mesh, int p, const sem_opts& o, GlobalModel&
   if (mesh->xyz) hm.xyz.assign(mesh->xyz, mesh->xyz + (size_t)hm.nv * 3);
   gm.P = p;
   gm.sched = schedule_for(p, o);
+  gm.user_part.clear();
+  if (mesh->part && o.nranks > 1) {
+    gm.user_part.assign(mesh->part, mesh->part + E);
+    for (int r : gm.user_part)
+      if (r < 0 || r >= o.nranks) throw SemError(SEM_EINVAL, "sem_mesh.part: rank out of range");
+  }
   if (gm.sched.size() > 16) throw SemError(SEM_EINVAL, "too many levels");
   const int Nf = n_prism(p);
   gm.X.resize((size_t)E * Nf * 3);

@@ -470,7 +470,7 @@ void compute_partition(const GlobalModel& gm, const sem_opts& o, std::vector<int
       cy[e] = sy / Nf;
     }
   }
-  epart = partition_columns(cx, cy, o.nranks);
+  epart = gm.user_part.empty() ? partition_columns(cx, cy, o.nranks) : gm.user_part;
   sch.assign(nl - 1, SchwarzTopo());
   const int nth = std::min(32, std::max(1, omp_get_max_threads()));
   for (int l = 0; l + 1 < nl; ++l) {

@@ -66,6 +66,7 @@ struct GlobalModel {
   std::vector<int> sched;
   std::vector<double> X;          // [E][N(P)][3] finest nodal map
   std::vector<LevelTopo> topo;    // global numbering per level
+  std::vector<int> user_part;     // sem_mesh.part (empty = the library's column partition)
 };
 
 void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lids, const LocalPart* part,

@@ -109,3 +109,24 @@ def test_partitioned_fdm_matches_single_domain(name, nranks):
     assert rel(pd.cpu().numpy(), p1.cpu().numpy()) <= 1e-10
     sd.close()
     s1.close()
+
+
+@pytest.mark.parametrize("local_solve", [0, 1])
+def test_user_partition_sem_mesh_part(local_solve):
+    """sem_mesh.part: a caller-given partition -- here three strips of
+    whole columns by the x of the column's triangle, a different cut from the
+    library's recursive bisection -- gives the single-domain solution."""
+    m = basin("c3s_part", 5, 32.0 * 6 / 64, 6, 3, seed=3)
+    cx = m.vert2d[m.tri].mean(axis=1)[:, 0]                   # per triangle (column)
+    col = np.arange(m.n_elem) // m.nz                           # element -> column (column-major order)
+    part = np.minimum(2, (3 * cx[col] / cx.max()).astype(np.int32))
+    s1 = mk(m, local_solve=local_solve)
+    sd = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)),
+                    nranks=3, part=part, local_solve=local_solve)
+    xyz = s1.node_xyz(0)
+    phiD = torch.from_numpy(m.phi(*xyz.T)).cuda()
+    a, _ = s1.solve(phiD, 1e-12)
+    b, _ = sd.solve(phiD, 1e-12)
+    assert rel(b.cpu().numpy(), a.cpu().numpy()) <= 1e-10
+    u = torch.from_numpy(random_vector(s1.n_dof(0), 9)).cuda()
+    assert rel(sd.apply(u).cpu().numpy(), s1.apply(u).cpu().numpy()) <= 1e-13
