@@ -66,7 +66,11 @@ struct AQ {
   static constexpr int TSE = TSE0 + 8;          // slot stride per element: = 8 mod 16 (bank spread of the 4 elements)
   static constexpr int TS = 4 * TSE;            // doubles of one slot (four elements)
   static constexpr int NYL = aq::cdiv(N1, 2);   // vertical output nodes scattered per lane
-  static constexpr int SMEM = (BM + BMT + BT + W * R * TS) * 8 + W * R * 8;
+  // next quad's gather staged in shared memory by cp.async: u [4][UST] (UST = 4 mod 16: the four
+  // elements' rows in distinct banks) and the connectivity [4 N]
+  static constexpr int UST = (N + 11) / 16 * 16 + 4;
+  static constexpr int SU = 4 * UST, SC = 4 * N;
+  static constexpr int SMEM = (BMT + BT + W * R * TS + W * SU) * 8 + W * SC * 4 + W * R * 8;
   static_assert(TSE % 16 == 8 && LDA % 16 == 8, "bank layout");
   static_assert(SMEM <= 227 * 1024, "apply_quad shared memory");
 };
@@ -112,15 +116,16 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
                  const double* __restrict__ mats, const double* __restrict__ u, double* __restrict__ y, int flags) {
   using D = AQ<P>;
   extern __shared__ __align__(128) double sm[];
-  double* Bm = sm;                        // [3][ROWSA][LDM]
-  double* BmT = sm + D::BM;               // [3][8 NM][LDA]
+  double* BmT = sm;                       // [3][8 NM][LDA]  B_c[a][m] at [m][a] (both triangle stages)
   double* sBt = BmT + D::BMT;             // [QV][N1]
   double* sDt = sBt + D::QV * D::N1;
-  double* ringall = sm + D::BM + D::BMT + D::BT;   // [W][R][4][TSE]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(ringall + D::W * D::R * D::TS);
+  double* ringall = sBt + D::BT;          // [W][R][4][TSE]
+  double* suall = ringall + D::W * D::R * D::TS;      // [W][4][UST]
+  int32_t* scall = reinterpret_cast<int32_t*>(suall + D::W * D::SU);   // [W][4 N]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(scall + D::W * D::SC);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r4 = lane >> 2, c4 = lane & 3, el = r4 & 3, h = r4 >> 2;
-  for (int i = tid; i < D::BM + D::BMT + D::BT; i += 32 * D::W) sm[i] = __ldg(mats + i);
+  for (int i = tid; i < D::BMT + D::BT; i += 32 * D::W) sm[i] = __ldg(mats + D::BM + i);
   if (lane == 0) {
     for (int b = 0; b < D::R; ++b)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(aq_smem(mbar + D::R * warp + b)));
@@ -148,8 +153,40 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
           "l"(Gw + (size_t)(4 * qd + k) * 6 * D::Q + (size_t)ma * 48 * D::QV), "r"(one), "r"(mb)
           : "memory");
   };
-  if (q0 < nquad)
+  double* su = suall + warp * D::SU;
+  int32_t* scn = scall + warp * D::SC;
+  // gather staging of quad qd: (1) its connectivity, 16-byte cp.async; (2) u through it, 8-byte
+  // cp.async (zero-filled where absent / Dirichlet); consumed after cp.async.wait_group 0
+  auto stage_conn = [&](int qd) {
+    const int64_t base = (int64_t)4 * qd * D::N;
+    const int nval = min(4, E - 4 * qd) * D::N;   // ints of the quad's existing elements
+    for (int i = lane; i < D::SC / 4; i += 32) {
+      const int cnt = min(4, max(0, nval - 4 * i));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(aq_smem(scn + 4 * i)),
+                   "l"(conn + base + 4 * i), "r"(4 * cnt)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto stage_u = [&](int qd) {
+    const int nval = min(4, E - 4 * qd) * D::N;
+    for (int i = lane; i < D::SC; i += 32) {
+      const int g = i < nval ? scn[i] : INT_MIN;
+      const bool take = g >= 0 || (g != INT_MIN && (flags & AP_GATHER_ALL));
+      const double* src = u + (take ? (g >= 0 ? g : ~g) : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(aq_smem(su + (i / D::N) * D::UST + i % D::N)),
+                   "l"(src), "r"(take ? 8 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (q0 < nquad) {
     for (int t = 0; t < D::R; ++t) issue(t);
+    stage_conn(q0);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    stage_u(q0);
+  }
   int tk = 0;
   for (int qd = q0; qd < nquad; qd += qstride, tk += D::MTA) {
     const int e = 4 * qd + el;
@@ -157,6 +194,8 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
     const int32_t* ce = conn + (size_t)(ev ? e : 0) * D::N;
     // ---- stage A (FMA): lane's A fragments of stage B, m = 4 ks + c4, q = 2 mt + h
     double Ua[D::MTQ][D::KM], Ud[D::MTQ][D::KM];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");   // this quad's u (staged during the previous one)
+    __syncwarp();
     {
       double uu[D::KM][D::N1];
 #pragma unroll
@@ -164,13 +203,7 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
 #pragma unroll
         for (int l = 0; l < D::N1; ++l) {
           const int m = 4 * ks + c4;
-          double v = 0.0;
-          if (ev && m < D::NT) {
-            const int g = __ldg(ce + m + D::NT * l);
-            if (g >= 0) v = __ldg(u + g);
-            else if (flags & AP_GATHER_ALL) v = __ldg(u + ~g);
-          }
-          uu[ks][l] = v;
+          uu[ks][l] = (ev && m < D::NT) ? su[el * D::UST + m + D::NT * l] : 0.0;
         }
 #pragma unroll
       for (int mt = 0; mt < D::MTQ; ++mt) {
@@ -195,28 +228,20 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
     for (int mt = 0; mt < D::MTQ; ++mt)
 #pragma unroll
       for (int nm = 0; nm < D::NM; ++nm) Vt[mt][nm][0] = Vt[mt][nm][1] = Vd[mt][nm][0] = Vd[mt][nm][1] = 0.0;
-    // next quad's gather, prefetched into L1 during this quad (only 2 warps per scheduler: the
-    // connectivity -> u dependent loads of a quad start would otherwise stall the warp)
-    constexpr int NPF = (4 * D::N + 31) / 32;
+    // next quad's gather staged in shared memory during this quad (only 2 warps per scheduler:
+    // the connectivity -> u dependent loads of a quad start would otherwise stall the warp)
     const int qn = qd + qstride;
-    int pf[NPF];
 #pragma unroll 1
     for (int na = 0; na < D::MTA; ++na) {
       const int t = tk + na;
       if (na == 0 && qn < nquad) {
-#pragma unroll
-        for (int k = 0; k < NPF; ++k) {
-          const int i = lane + 32 * k;
-          pf[k] = (i < 4 * D::N && 4 * qn + i / D::N < E) ? __ldg(conn + (size_t)4 * qn * D::N + i) : INT_MIN;
-        }
+        __syncwarp();   // every lane has read this quad's u from su
+        stage_conn(qn);
       }
       if (na == 1 && qn < nquad) {
-#pragma unroll
-        for (int k = 0; k < NPF; ++k)
-          if (pf[k] != INT_MIN) {
-            const double* a = u + (pf[k] >= 0 ? pf[k] : ~pf[k]);
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-          }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        stage_u(qn);
       }
       {  // wait for copy t
         const uint32_t mb = aq_smem(mbar + D::R * warp + t % D::R);
@@ -237,8 +262,8 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
         for (int mt = 0; mt < D::MTQ; ++mt) g[c][mt][0] = g[c][mt][1] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < D::KM; ++ks) {
-        const int off = (8 * na + r4) * D::LDM + 4 * ks + c4;
-        const double br = Bm[off], bs = Bm[D::ROWSA * D::LDM + off], b0 = Bm[2 * D::ROWSA * D::LDM + off];
+        const int off = (4 * ks + c4) * D::LDA + 8 * na + r4;    // B_c[a = 8 na + r4][m = 4 ks + c4]
+        const double br = BmT[off], bs = BmT[8 * D::NM * D::LDA + off], b0 = BmT[16 * D::NM * D::LDA + off];
 #pragma unroll
         for (int mt = 0; mt < D::MTQ; ++mt) {
           aq_dmma(g[0][mt][0], g[0][mt][1], Ua[mt][ks], br);
