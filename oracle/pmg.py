@@ -32,8 +32,8 @@ from . import sem
 
 def prolongation(fine: sem.Level, coarse: sem.Level) -> sp.csr_matrix:
     """P[j][i] = N_i^c(x_j^f) assembled from one element containing x_j^f."""
-    rst_f, _ = R.prism_nodes(fine.p)
-    I, _ = R.prism_basis(coarse.p, rst_f)               # [Nf][Nc]
+    rst_f, _ = R.prism_nodes(fine.p, fine.q)
+    I, _ = R.prism_basis(coarse.p, rst_f, coarse.q)     # [Nf][Nc]
     E, Nf = fine.conn.shape
     owner_e = np.full(fine.n, -1, dtype=np.int64)
     owner_l = np.full(fine.n, -1, dtype=np.int64)
@@ -54,7 +54,7 @@ def lattice_adjacency(level: sem.Level) -> sp.csr_matrix:
     holds both with |dl| <= 1 and triangular-lattice offset in {0, +-(1,-1,0),
     +-(1,0,-1), +-(0,1,-1)} of the barycentric indices (i, j, k=p-i-j)."""
     p = level.p
-    _, ijl = R.prism_nodes(p)
+    _, ijl = R.prism_nodes(p, level.q)
     i, j, l = ijl[:, 0], ijl[:, 1], ijl[:, 2]
     k = p - i - j
     di = i[:, None] - i[None, :]
@@ -169,7 +169,9 @@ class PMG:
         self.nu1, self.nu2, self.literal = nu1, nu2, literal
         self.levels = []
         for pl in self.schedule:
-            lev = sem.build_system(mesh, pl, p_geo=mesh.p)
+            # a level is an order p, or a pair (P_xy, P_z)
+            pp, qq = (pl, None) if np.isscalar(pl) else (int(pl[0]), int(pl[1]))
+            lev = sem.build_system(mesh, pp, q=qq if qq != pp else None)
             F = lev.free
             AFF = lev.A[F][:, F].tocsr()
             self.levels.append(MGLevel(level=lev, A=AFF))

@@ -154,21 +154,25 @@ def n_tri(p):
     return (p + 1) * (p + 2) // 2
 
 
-def n_prism(p):
-    return n_tri(p) * (p + 1)
+def n_prism(p, q=None):
+    """Nodes of P_p(triangle) x P_q(t) (q = p: the isotropic space of reading O2)."""
+    return n_tri(p) * ((p if q is None else q) + 1)
 
 
 @functools.lru_cache(maxsize=None)
-def prism_nodes(p: int):
+def prism_nodes(p: int, q: int | None = None):
     """Reference coordinates [N][3] of local prism nodes n = m + Nt*l and the
-    lattice coordinates [N][3] = (i, j, l)."""
+    lattice coordinates [N][3] = (i, j, l).  Horizontal order p (triangle nodes),
+    vertical order q (LGL(q) in t; default q = p).  SURVEY NEXT-2: the paper's
+    (P_xy, P_z) pairs (P:450)."""
+    q = p if q is None else q
     r, s = tri_nodes(p)
-    t, _ = lgl(p)
+    t, _ = lgl(q)
     lat = tri_lattice(p)
     Nt = n_tri(p)
-    rst = np.zeros((Nt * (p + 1), 3))
-    ijl = np.zeros((Nt * (p + 1), 3), dtype=np.int64)
-    for l in range(p + 1):
+    rst = np.zeros((Nt * (q + 1), 3))
+    ijl = np.zeros((Nt * (q + 1), 3), dtype=np.int64)
+    for l in range(q + 1):
         for m in range(Nt):
             n = m + Nt * l
             rst[n] = (r[m], s[m], t[l])
@@ -176,17 +180,18 @@ def prism_nodes(p: int):
     return rst, ijl
 
 
-def prism_basis(p: int, pts: np.ndarray):
-    """Prism cardinal basis of order p at points [np][3]:
-    values [np][N] and gradient [3][np][N] (d/dr, d/ds, d/dt)."""
+def prism_basis(p: int, pts: np.ndarray, q: int | None = None):
+    """Prism cardinal basis of P_p(triangle) x P_q(t) (default q = p) at points
+    [np][3]: values [np][N] and gradient [3][np][N] (d/dr, d/ds, d/dt)."""
+    q = p if q is None else q
     pts = np.atleast_2d(pts)
     Lt, Lr, Ls = tri_lagrange(p, pts[:, 0], pts[:, 1])
-    h, dh = lagrange1d(lgl(p)[0], pts[:, 2])
+    h, dh = lagrange1d(lgl(q)[0], pts[:, 2])
     Nt = n_tri(p)
     npt = pts.shape[0]
-    val = np.zeros((npt, Nt * (p + 1)))
-    grad = np.zeros((3, npt, Nt * (p + 1)))
-    for l in range(p + 1):
+    val = np.zeros((npt, Nt * (q + 1)))
+    grad = np.zeros((3, npt, Nt * (q + 1)))
+    for l in range(q + 1):
         sl = slice(Nt * l, Nt * (l + 1))
         val[:, sl] = Lt * h[:, l:l + 1]
         grad[0][:, sl] = Lr * h[:, l:l + 1]
@@ -210,14 +215,16 @@ def tri_cubature(p: int):
 
 
 @functools.lru_cache(maxsize=None)
-def prism_cubature(p: int):
-    """Cubature points [Q][3] and weights [Q], point q = ta + Qt*qv."""
+def prism_cubature(p: int, q: int | None = None):
+    """Cubature points [Q][3] and weights [Q], point q = ta + Qt*qv: the collapsed
+    triangle rule of order p times GL(q+1) in t (default q = p; reading O6)."""
+    q = p if q is None else q
     r, s, wt = tri_cubature(p)
-    t, wv = gauss_legendre(p + 1)
+    t, wv = gauss_legendre(q + 1)
     Qt = len(r)
-    pts = np.zeros((Qt * (p + 1), 3))
-    w = np.zeros(Qt * (p + 1))
-    for qv in range(p + 1):
+    pts = np.zeros((Qt * (q + 1), 3))
+    w = np.zeros(Qt * (q + 1))
+    for qv in range(q + 1):
         for ta in range(Qt):
             q = ta + Qt * qv
             pts[q] = (r[ta], s[ta], t[qv])
@@ -225,12 +232,28 @@ def prism_cubature(p: int):
     return pts, w
 
 
-def face_nodes(p: int):
+def face_nodes(p: int, q: int | None = None):
     """Local node lists of the 5 prism faces (bot, top, q01, q12, q20)."""
-    _, ijl = prism_nodes(p)
+    q = p if q is None else q
+    _, ijl = prism_nodes(p, q)
     i, j, l = ijl[:, 0], ijl[:, 1], ijl[:, 2]
-    return [np.nonzero(l == 0)[0], np.nonzero(l == p)[0], np.nonzero(j == 0)[0],
+    return [np.nonzero(l == 0)[0], np.nonzero(l == q)[0], np.nonzero(j == 0)[0],
             np.nonzero(i + j == p)[0], np.nonzero(i == 0)[0]]
+
+
+def level_schedule_pq(p: int, q: int):
+    """Coarsening of (P_xy, P_z) (reading O19): semi-coarsen the larger
+    order first, to max(smaller, ceil((larger+1)/2)), until the orders are equal
+    ("until polynomial orders in all directions are equal"), then the
+    isotropic rule of level_schedule."""
+    out = [(p, q)]
+    while out[-1][0] != out[-1][1]:
+        a, b = out[-1]
+        if a > b:
+            out.append((max(b, math.ceil((a + 1) / 2) if math.ceil((a + 1) / 2) < a else a - 1), b))
+        else:
+            out.append((a, max(a, math.ceil((b + 1) / 2) if math.ceil((b + 1) / 2) < b else b - 1)))
+    return out + [(c, c) for c in level_schedule(out[-1][0])[1:]]
 
 
 def level_schedule(p: int):

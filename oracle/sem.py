@@ -31,6 +31,11 @@ class Level:
     dirichlet: np.ndarray     # [n] bool
     G: np.ndarray | None = None   # [E][Q][3][3]
     A: sp.csr_matrix | None = None
+    q: int | None = None      # vertical order (None = p, the isotropic space)
+
+    @property
+    def pz(self):
+        return self.p if self.q is None else self.q
 
     @property
     def n(self):
@@ -64,26 +69,31 @@ def number_nodes(pts: np.ndarray, tol: float = 1e-9):
     return conn, rep[perm]
 
 
-def build_level(mesh, p: int) -> Level:
-    rst, _ = R.prism_nodes(p)
+def mesh_pz(mesh):
+    """Vertical order of the mesh's finest nodal map (default its p)."""
+    return getattr(mesh, "pz", None) or mesh.p
+
+
+def build_level(mesh, p: int, q: int | None = None) -> Level:
+    rst, _ = R.prism_nodes(p, q)
     pts = mesh.node_xyz(rst)
     conn, xyz = number_nodes(pts)
     dirichlet = np.zeros(xyz.shape[0], dtype=bool)
-    fn = R.face_nodes(p)
+    fn = R.face_nodes(p, q)
     for f in range(5):
         tagged = np.nonzero(mesh.face_tag[:, f] == 1)[0]
         if len(tagged):
             dirichlet[conn[np.ix_(tagged, fn[f])].ravel()] = True
-    return Level(p=p, conn=conn, xyz=xyz, dirichlet=dirichlet)
+    return Level(p=p, conn=conn, xyz=xyz, dirichlet=dirichlet, q=q)
 
 
-def geometry(mesh, p_geo: int, p: int, elems=None):
-    """G = w detJ J^{-1} J^{-T} [e][Q][3][3] at order-p cubature from the order
-    p_geo nodal map (O-5).  Raises on detJ <= 0."""
-    rst_geo, _ = R.prism_nodes(p_geo)
+def geometry(mesh, p_geo: int, p: int, elems=None, q_geo: int | None = None, q: int | None = None):
+    """G = w detJ J^{-1} J^{-T} [e][Q][3][3] at the order-(p, q) cubature from the
+    order-(p_geo, q_geo) nodal map (O-5).  Raises on detJ <= 0."""
+    rst_geo, _ = R.prism_nodes(p_geo, q_geo)
     X = mesh.node_xyz(rst_geo, elems)                   # [e][Ng][3]
-    pts, w = R.prism_cubature(p)
-    _, dgeo = R.prism_basis(p_geo, pts)                 # [3][Q][Ng]
+    pts, w = R.prism_cubature(p, q)
+    _, dgeo = R.prism_basis(p_geo, pts, q_geo)          # [3][Q][Ng]
     # J[e][q][i][c] = sum_n X[e][n][i] * dgeo[c][q][n]
     # (optimize=True only lets numpy contract through BLAS: same formula, summation order only)
     J = np.einsum("eni,cqn->eqic", X, dgeo, optimize=True)
@@ -95,10 +105,10 @@ def geometry(mesh, p_geo: int, p: int, elems=None):
     return G
 
 
-def element_matrices(G: np.ndarray, p: int):
+def element_matrices(G: np.ndarray, p: int, q: int | None = None):
     """A_e[i][j] = sum_q sum_cd dl_i^c(q) G_q[c][d] dl_j^d(q)   [e][N][N]."""
-    pts, _ = R.prism_cubature(p)
-    _, D = R.prism_basis(p, pts)                        # [3][Q][N]
+    pts, _ = R.prism_cubature(p, q)
+    _, D = R.prism_basis(p, pts, q)                     # [3][Q][N]
     return np.einsum("cqi,eqcd,dqj->eij", D, G, D)
 
 
@@ -109,12 +119,14 @@ def assemble(level: Level, Ae: np.ndarray) -> sp.csr_matrix:
     return sp.coo_matrix((Ae.ravel(), (rows, cols)), shape=(level.n, level.n)).tocsr()
 
 
-def build_system(mesh, p: int, p_geo: int | None = None) -> Level:
-    """Assembled Neumann stiffness A (= -L) of order p with geometry from the
-    order-p_geo map (default: mesh.p, the finest order)."""
-    lev = build_level(mesh, p)
-    lev.G = geometry(mesh, p_geo or mesh.p, p)
-    lev.A = assemble(lev, element_matrices(lev.G, p))
+def build_system(mesh, p: int, p_geo: int | None = None, q: int | None = None, q_geo: int | None = None) -> Level:
+    """Assembled Neumann stiffness A (= -L) of order (p, q) with geometry from
+    the order-(p_geo, q_geo) map (default: the mesh's finest orders)."""
+    if p_geo is None:
+        p_geo, q_geo = mesh.p, mesh_pz(mesh)
+    lev = build_level(mesh, p, q)
+    lev.G = geometry(mesh, p_geo, p, q_geo=q_geo, q=q)
+    lev.A = assemble(lev, element_matrices(lev.G, p, q))
     return lev
 
 
