@@ -129,6 +129,16 @@ typedef struct {
                                  subdomains, reductions sum per-block partials in a fixed order, the dense
                                  coarse solve is a row-wise GEMV of the full inverse, FDM levels use the
                                  generic k_fdm.  Slower; single-domain ctx only (SEM_EUNSUPPORTED otherwise). */
+  int pz;                     /* vertical polynomial order of the finest level, 0 (default) = p: the element
+                                 space P_p(triangle) x P_pz(t) -- the paper's (P_xy, P_z) pairs (
+                                 SURVEY NEXT-2).  Anisotropic levels run the generic operator kernel
+                                 (k_apply_pq) with dense local solves on a single domain
+                                 (SEM_EUNSUPPORTED otherwise).  node_xyz then has N = (p+1)(p+2)/2 (pz+1)
+                                 nodes per prism, local node m + Nt l with l = 0..pz (LGL of order pz). */
+  const int *levels_z;        /* with levels: the vertical order of every level (Table 5.4:
+                                 levels = {5, 3, 1}, levels_z = {3, 3, 1}); NULL = levels (isotropic), or,
+                                 without levels, semi-coarsening of the larger order first until the
+                                 orders agree, then P -> ceil((P+1)/2) (reading O19)                   */
 } sem_opts;
 
 typedef struct {
@@ -164,6 +174,7 @@ typedef struct {
   int smoother_kernel[16];    /* sweep kernel of each level's smoother (SEM_SMOOTHER_*; 0 on the
                                  coarsest level)                                                     */
   int smoother_mt[16];        /* FDM levels: 8-row tiles of the largest horizontal patch, ceil(n_h/8) */
+  int level_pz[16];           /* vertical polynomial order of each level (= level_p when isotropic)   */
 } sem_info;
 
 /* sem_info.smoother_kernel */
@@ -182,6 +193,9 @@ void sem_default_opts(sem_opts *opts);
  * library's local order (see the conventions above).  rst: host, caller-owned,
  * 3*N(p) doubles, N(p) = (p+1)^2 (p+2)/2.  Returns SEM_EINVAL for p<1 or p>8. */
 int sem_reference_nodes(int p, double *rst);
+/* The same for P_p(triangle) x P_pz(t): [Nt(p) (pz+1)][3], local node m + Nt l,
+ * l = 0..pz on the LGL points of order pz.  SEM_EINVAL outside 1..8. */
+int sem_reference_nodes_pq(int p, int pz, double *rst);
 
 /* Build the solver for order p (1..8) on `mesh` (all level
  * operators, smoothers and the coarse factor are formed once here and reused).

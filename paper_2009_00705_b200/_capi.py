@@ -28,7 +28,8 @@ class SemOpts(C.Structure):
                 ("verbose", C.c_int), ("apply_kernel", C.c_int), ("coarse_solver", C.c_int),
                 ("coarse_rtol", C.c_double), ("coarse_maxit", C.c_int), ("nranks", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("local_solve", C.c_int),
-                ("mixed_precision", C.c_int), ("deterministic", C.c_int)]
+                ("mixed_precision", C.c_int), ("deterministic", C.c_int), ("pz", C.c_int),
+                ("levels_z", C.POINTER(C.c_int))]
 
 
 class SemReport(C.Structure):
@@ -50,7 +51,8 @@ class SemInfo(C.Structure):
                 ("level_p", C.c_int * 16), ("level_n_dof", C.c_int64 * 16), ("level_n_free", C.c_int64 * 16),
                 ("schwarz_bytes", C.c_int64 * 16), ("schwarz_nk_sum", C.c_int64 * 16),
                 ("schwarz_packed", C.c_int64 * 16), ("coarse_n", C.c_int64), ("device_bytes", C.c_int64),
-                ("setup_ms", C.c_double), ("smoother_kernel", C.c_int * 16), ("smoother_mt", C.c_int * 16)]
+                ("setup_ms", C.c_double), ("smoother_kernel", C.c_int * 16), ("smoother_mt", C.c_int * 16),
+                ("level_pz", C.c_int * 16)]
 
 
 SMOOTHER_KERNELS = {0: "coarse", 1: "k_schwarz", 2: "k_fdm_warp<MT,1>", 3: "k_fdm_warp<MT,2>", 4: "k_fdm_cta<MT>",
@@ -60,6 +62,7 @@ SMOOTHER_KERNELS = {0: "coarse", 1: "k_schwarz", 2: "k_fdm_warp<MT,1>", 3: "k_fd
 _vp = C.c_void_p
 _lib.sem_default_opts.argtypes = [C.POINTER(SemOpts)]
 _lib.sem_reference_nodes.argtypes = [C.c_int, _dp]
+_lib.sem_reference_nodes_pq.argtypes = [C.c_int, C.c_int, _dp]
 _lib.sem_setup.argtypes = [C.POINTER(SemMesh), C.c_int, C.POINTER(SemOpts), C.POINTER(_vp)]
 _lib.sem_get_info.argtypes = [_vp, C.POINTER(SemInfo)]
 _lib.sem_node_xyz.argtypes = [_vp, C.c_int, _vp, C.c_int]
@@ -95,7 +98,7 @@ _lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.sem_host_partition.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp]
 
-EXPORTS = ["sem_fnpf_init", "sem_fnpf_surface_nodes", "fnpf_rhs", "fnpf_erk4_step", "laplace_solve_guess", "sem_update_geometry", "sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+EXPORTS = ["sem_reference_nodes_pq", "sem_fnpf_init", "sem_fnpf_surface_nodes", "fnpf_rhs", "fnpf_erk4_step", "laplace_solve_guess", "sem_update_geometry", "sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
            "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
            "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
            "sem_destroy", "sem_strerror", "sem_last_error"]
@@ -117,13 +120,18 @@ def _check(code, where):
 def default_opts() -> dict:
     o = SemOpts()
     _lib.sem_default_opts(C.byref(o))
-    return {k: getattr(o, k) for k, _ in SemOpts._fields_ if k not in ("levels", "stream")}
+    return {k: getattr(o, k) for k, _ in SemOpts._fields_ if k not in ("levels", "stream", "levels_z")}
 
 
-def reference_nodes(p: int) -> np.ndarray:
-    n = (p + 1) ** 2 * (p + 2) // 2
+def reference_nodes(p: int, pz: int | None = None) -> np.ndarray:
+    """Reference coordinates of the library's local nodes of P_p(triangle) x P_pz(t)."""
+    q = p if pz is None else pz
+    n = (p + 1) * (p + 2) // 2 * (q + 1)
     out = np.zeros((n, 3))
-    _check(_lib.sem_reference_nodes(p, out.ctypes.data_as(_dp)), "sem_reference_nodes")
+    if q == p:
+        _check(_lib.sem_reference_nodes(p, out.ctypes.data_as(_dp)), "sem_reference_nodes")
+    else:
+        _check(_lib.sem_reference_nodes_pq(p, q, out.ctypes.data_as(_dp)), "sem_reference_nodes_pq")
     return out
 
 
@@ -245,9 +253,14 @@ class Solver:
             setattr(o, k, v)
         self._levels = None
         if levels is not None:
-            self._levels = (C.c_int * len(levels))(*levels)
+            # orders, or (P_xy, P_z) pairs
+            pairs = [tuple(x) if not np.isscalar(x) else (int(x), int(x)) for x in levels]
+            self._levels = (C.c_int * len(pairs))(*[a for a, _ in pairs])
             o.levels = self._levels
-            o.n_levels = len(levels)
+            o.n_levels = len(pairs)
+            if any(not np.isscalar(x) for x in levels):
+                self._levels_z = (C.c_int * len(pairs))(*[b for _, b in pairs])
+                o.levels_z = self._levels_z
         self._nccl = None
         if nccl_id is not None:
             self._nccl = C.create_string_buffer(bytes(nccl_id), 128)
@@ -282,6 +295,7 @@ class Solver:
         _check(_lib.sem_get_info(self._ctx, C.byref(inf)), "sem_get_info")
         self.info = dict(n_dof=inf.n_dof, n_free=inf.n_free, n_elem=inf.n_elem, n_levels=inf.n_levels,
                          level_p=list(inf.level_p[: inf.n_levels]),
+                         level_pz=list(inf.level_pz[: inf.n_levels]),
                          level_n_dof=list(inf.level_n_dof[: inf.n_levels]),
                          level_n_free=list(inf.level_n_free[: inf.n_levels]),
                          schwarz_bytes=list(inf.schwarz_bytes[: inf.n_levels]),

@@ -41,8 +41,10 @@ std::vector<int> schedule_for(int p, const sem_opts& o) {
   if (o.levels && o.n_levels > 0) {
     for (int i = 0; i < o.n_levels; ++i) s.push_back(o.levels[i]);
     if (s[0] != p) throw SemError(SEM_EINVAL, "levels[0] must equal p");
+    const bool aniso = o.levels_z != nullptr;
     for (size_t i = 1; i < s.size(); ++i)
-      if (s[i] >= s[i - 1] || s[i] < 1) throw SemError(SEM_EINVAL, "levels must strictly decrease to >= 1");
+      if ((aniso ? s[i] > s[i - 1] : s[i] >= s[i - 1]) || s[i] < 1)
+        throw SemError(SEM_EINVAL, "levels must decrease to >= 1");
     if (s.back() != 1) throw SemError(SEM_EINVAL, "the coarsest level must be P=1 (P:222-223)");
     return s;
   }
@@ -53,6 +55,47 @@ std::vector<int> schedule_for(int p, const sem_opts& o) {
     s.push_back(c);
   }
   return s;
+}
+
+// (P_xy, P_z) schedules (reading O19): explicit (opts.levels + opts.levels_z), or
+// semi-coarsening of the larger order first -- to max(smaller, ceil((larger+1)/2)) with the
+// strict-decrease guard -- until the orders agree, then the isotropic rule
+void schedule_pq(int p, int pz, const sem_opts& o, std::vector<int>& sp, std::vector<int>& sq) {
+  sp.clear();
+  sq.clear();
+  if (o.levels && o.n_levels > 0) {
+    sp = schedule_for(p, o);
+    if (o.levels_z) {
+      sq.assign(o.levels_z, o.levels_z + o.n_levels);
+      if (sq[0] != pz) throw SemError(SEM_EINVAL, "levels_z[0] must equal pz");
+      for (size_t i = 1; i < sq.size(); ++i)
+        if (sq[i] > sq[i - 1] || sq[i] < 1 || (sq[i] == sq[i - 1] && sp[i] == sp[i - 1]))
+          throw SemError(SEM_EINVAL, "every level must coarsen at least one direction");
+      if (sq.back() != 1) throw SemError(SEM_EINVAL, "the coarsest level must be (1,1)");
+    } else {
+      if (pz != p) throw SemError(SEM_EINVAL, "an anisotropic finest level needs levels_z");
+      sq = sp;
+    }
+    return;
+  }
+  auto next = [](int a) {
+    int c = (a + 2) / 2;
+    return c >= a ? a - 1 : c;
+  };
+  int a = p, b = pz;
+  sp.push_back(a);
+  sq.push_back(b);
+  while (a != b) {
+    if (a > b) a = std::max(b, next(a));
+    else b = std::max(a, next(b));
+    sp.push_back(a);
+    sq.push_back(b);
+  }
+  while (a > 1) {
+    a = next(a);
+    sp.push_back(a);
+    sq.push_back(a);
+  }
 }
 
 double now_ms() {
@@ -232,6 +275,7 @@ void setup_schwarz(sem_ctx* c, int li, const SchwarzTopo& S, cublasHandle_t blas
 // ------------------------------------------------------------------ coarse setup
 void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, const double* d_D) {
   DeviceLevel& L = c->L.back();
+  if (L.p != 1 || L.q != 1) throw SemError(SEM_EINVAL, "the coarsest level must be P=1 in both directions");
   const int E = c->E;
   std::vector<int32_t> cmap(topo.n, -1), fidx;
   for (int64_t i = 0; i < topo.n; ++i)
@@ -346,6 +390,7 @@ void check_opts(const sem_opts& o) {
   if (o.local_solve < 0 || o.local_solve > 1) throw SemError(SEM_EINVAL, "bad options: local_solve");
   if (o.mixed_precision < 0 || o.mixed_precision > 1) throw SemError(SEM_EINVAL, "bad options: mixed_precision");
   if (o.deterministic < 0 || o.deterministic > 1) throw SemError(SEM_EINVAL, "bad options: deterministic");
+  if (o.pz < 0 || o.pz > 8) throw SemError(SEM_EINVAL, "bad options: pz");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
       o.apply_kernel > 3 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
       o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
@@ -366,7 +411,13 @@ void prepare_global(const sem_mesh* mesh, int p, const sem_opts& o, GlobalModel&
     if (v < 0 || v >= hm.nv) throw SemError(SEM_EINVAL, "prism vertex index out of range");
   if (mesh->xyz) hm.xyz.assign(mesh->xyz, mesh->xyz + (size_t)hm.nv * 3);
   gm.P = p;
-  gm.sched = schedule_for(p, o);
+  gm.PZ = o.pz > 0 ? o.pz : p;
+  if (gm.PZ > 8) throw SemError(SEM_EINVAL, "vertical order pz must be in 1..8");
+  schedule_pq(p, gm.PZ, o, gm.sched, gm.schedz);
+  if (gm.PZ != p || gm.sched != gm.schedz) {
+    if (o.nranks > 1 || o.local_solve != 0)
+      throw SemError(SEM_EUNSUPPORTED, "anisotropic (P_xy, P_z) levels: single domain, dense local solves only");
+  }
   gm.user_part.clear();
   if (mesh->part && o.nranks > 1) {
     gm.user_part.assign(mesh->part, mesh->part + E);
@@ -374,13 +425,13 @@ void prepare_global(const sem_mesh* mesh, int p, const sem_opts& o, GlobalModel&
       if (r < 0 || r >= o.nranks) throw SemError(SEM_EINVAL, "sem_mesh.part: rank out of range");
   }
   if (gm.sched.size() > 16) throw SemError(SEM_EINVAL, "too many levels");
-  const int Nf = n_prism(p);
+  const int Nf = n_prism(p, gm.PZ);
   gm.X.resize((size_t)E * Nf * 3);
   std::vector<double>& X = gm.X;
   if (mesh->node_xyz) {
     std::copy(mesh->node_xyz, mesh->node_xyz + X.size(), X.begin());
   } else {  // straight-sided: linear wedge map from the 6 vertices
-    std::vector<double> rst = reference_nodes(p);
+    std::vector<double> rst = reference_nodes(p, gm.PZ);
 #pragma omp parallel for
     for (int e = 0; e < E; ++e)
       for (int n = 0; n < Nf; ++n) {
@@ -398,22 +449,23 @@ void prepare_global(const sem_mesh* mesh, int p, const sem_opts& o, GlobalModel&
   }
   double tm = now_ms();
   Entities ent;
-  if (gm.sched[0] >= 2) ent = build_entities(hm);
+  if (gm.sched[0] >= 2 || gm.schedz[0] >= 2) ent = build_entities(hm);
   gm.topo.resize(gm.sched.size());
-  for (size_t li = 0; li < gm.sched.size(); ++li) gm.topo[li] = number_level(hm, ent, gm.sched[li]);
+  for (size_t li = 0; li < gm.sched.size(); ++li) gm.topo[li] = number_level(hm, ent, gm.sched[li], gm.schedz[li]);
   if (o.verbose) fprintf(stderr, "[sem] numbering %.0f ms\n", now_ms() - tm);
 }
 
 // host coordinates of a level's nodes: the finest nodal map X (order pf) evaluated at the
 // level's reference nodes; in the global build the owner element's value is kept
 void level_xyz(DeviceLevel& L, int pf, const std::vector<double>& X, const std::vector<int32_t>& conn,
-               const std::vector<uint8_t>& own, int E, bool all_elements) {
+               const std::vector<uint8_t>& own, int E, bool all_elements, int qf) {
+  if (qf < 0) qf = pf;
   const LevelRef& R = L.ref;
-  const int Nf = n_prism(pf);
+  const int Nf = n_prism(pf, qf);
   L.xyz.assign((size_t)L.n * 3, 0.0);
   std::vector<double> It, I1;
-  transfer_matrices(L.p, pf, It, I1);  // order-pf basis at this level's nodes
-  const int ntl = R.nt, n1l = R.n1, ntf = n_tri(pf), n1f = pf + 1;
+  transfer_matrices(L.p, pf, It, I1, R.q, qf);  // order-(pf, qf) basis at this level's nodes
+  const int ntl = R.nt, n1l = R.n1, ntf = n_tri(pf), n1f = qf + 1;
 #pragma omp parallel for
   for (int e = 0; e < E; ++e)
     for (int l = 0; l < n1l; ++l)
@@ -443,9 +495,10 @@ void level_xyz(DeviceLevel& L, int pf, const std::vector<double>& X, const std::
 void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lids, const LocalPart* part,
                   const std::vector<SchwarzTopo>* gsch) {
   const sem_opts& o = c->opts;
-  const int p = gm.P;
-  const int Nf = n_prism(p);
+  const int p = gm.P, pz = gm.PZ;
+  const int Nf = n_prism(p, pz);
   const int nl = (int)lids.size();
+  c->PZ = pz;
   const int E = part ? (int)part->elems.size() : gm.hm.E;
   c->E = E;
   c->E_own = part ? part->E_own : E;
@@ -487,7 +540,8 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
     const std::vector<uint8_t>& dir = part ? part->L[lid].dir : GT.dir;
     const std::vector<uint8_t>& own = part ? part->L[lid].owner : GT.owner;
     L.p = gm.sched[lid];
-    L.ref = make_level_ref(L.p);
+    L.q = gm.schedz[lid];
+    L.ref = make_level_ref(L.p, L.q);
     L.N = L.ref.N;
     L.Q = L.ref.Q;
     L.n = part ? part->L[lid].n : GT.n;
@@ -523,27 +577,29 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
       mats[(size_t)3 * R.qt * ntp + R.n1 * R.n1 + i] = R.Dt[i];
     }
     L.mats = upload(c, mats);
-    L.frag = upload(c, dmma_fragments(R));
-    if (L.p <= 6) L.wmats = upload(c, warp_apply_mats(R));
-    if (L.p >= 3 && L.p <= 5) L.qmats = upload(c, quad_apply_mats(R));
+    if (L.p == L.q) {  // the tensor-core kernels are isotropic; (P_xy, P_z) levels use k_apply_pq
+      L.frag = upload(c, dmma_fragments(R));
+      if (L.p <= 6) L.wmats = upload(c, warp_apply_mats(R));
+      if (L.p >= 3 && L.p <= 5) L.qmats = upload(c, quad_apply_mats(R));
+    }
     // geometric factors from the finest nodal map (all held elements)
     L.G = dalloc<double>(c, (size_t)E * 6 * L.Q);
     {
       Scratch s2;
-      double* d_gm = s2.put(geometry_matrix(p, L.p));
+      double* d_gm = s2.put(geometry_matrix(p, L.p, pz, L.q));
       double* d_w = s2.put(R.wq);
       if (launch_geometry(c, li, d_X, d_gm, Nf, d_w)) throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
       build_g_tiles(c, li);
     }
     // node coordinates of this level (fine map evaluated at the level's nodes)
-    level_xyz(L, p, X, conn, own, E, part != nullptr);
+    level_xyz(L, p, X, conn, own, E, part != nullptr, pz);
     if (!part) {  // kept for sem_update_geometry (single domain)
       L.conn_host = conn;
       L.owner_host = own;
     }
     if (li + 1 < nl) {
       std::vector<double> It, I1;
-      transfer_matrices(L.p, gm.sched[lids[li + 1]], It, I1);
+      transfer_matrices(L.p, gm.sched[lids[li + 1]], It, I1, L.q, gm.schedz[lids[li + 1]]);
       L.Itri = upload(c, It);
       L.I1 = upload(c, I1);
     }
@@ -558,7 +614,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
     Scratch s2;
     double* d_D = s2.put(c->L[li].ref.Dfull);
     const int lid = lids[li];
-    if (o.apply_kernel == 0 || o.apply_kernel == 3) build_p1_matrices(c, li, d_D);
+    if ((o.apply_kernel == 0 || o.apply_kernel == 3) && c->L[li].p == c->L[li].q) build_p1_matrices(c, li, d_D);
     if (li + 1 < nl) {
       double t0 = now_ms();
       if (part && o.local_solve == 1) {  // partitioned FDM / exact-dense hybrid (O33, O35)
@@ -917,11 +973,20 @@ void sem_default_opts(sem_opts* o) {
   o->nranks = 1;
   o->rank = 0;
   o->nccl_id = nullptr;
+  o->pz = 0;
+  o->levels_z = nullptr;
 }
 
 int sem_reference_nodes(int p, double* rst) {
   if (p < 1 || p > 8 || !rst) return SEM_EINVAL;
   std::vector<double> v = reference_nodes(p);
+  std::copy(v.begin(), v.end(), rst);
+  return SEM_OK;
+}
+
+int sem_reference_nodes_pq(int p, int pz, double* rst) {
+  if (p < 1 || p > 8 || pz < 1 || pz > 8 || !rst) return SEM_EINVAL;
+  std::vector<double> v = reference_nodes(p, pz);
   std::copy(v.begin(), v.end(), rst);
   return SEM_OK;
 }
@@ -966,6 +1031,7 @@ int sem_get_info(const sem_ctx* c, sem_info* info) {
   info->n_levels = (int)c->L.size();
   for (size_t i = 0; i < c->L.size(); ++i) {
     info->level_p[i] = c->L[i].p;
+    info->level_pz[i] = c->L[i].q;
     info->level_n_dof[i] = c->L[i].n;
     info->level_n_free[i] = c->L[i].nfree;
     info->schwarz_bytes[i] = c->L[i].schwarz_bytes;
@@ -1065,7 +1131,7 @@ int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
     if (strategy == 4 && c->L.size() > 1 && (!c->L[0].fdm || !c->C.iterative))
       throw SemError(SEM_EUNSUPPORTED, "strategy III (4) re-forms smoothers and coarse preconditioner every stage: "
                                        "needs local_solve = 1 and coarse_solver = 1");
-    const int p = c->P, Nf = n_prism(p), E = c->E;
+    const int p = c->P, Nf = n_prism(p, c->PZ), E = c->E;
     std::vector<double> X(node_xyz, node_xyz + (size_t)E * Nf * 3);
     Scratch sc;
     const double* d_X = sc.put(X);
@@ -1073,7 +1139,7 @@ int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
     for (int li = 0; li < nlev; ++li) {
       DeviceLevel& L = c->L[li];
       Scratch s2;
-      const double* d_gm = s2.put(geometry_matrix(p, L.p));
+      const double* d_gm = s2.put(geometry_matrix(p, L.p, c->PZ, L.q));
       const double* d_w = s2.put(L.ref.wq);
       if (launch_geometry(c, li, d_X, d_gm, Nf, d_w)) throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
       if (L.Gw) build_g_tiles(c, li);
@@ -1081,7 +1147,7 @@ int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
         const double* d_D = s2.put(L.ref.Dfull);
         build_p1_matrices(c, li, d_D);
       }
-      level_xyz(L, p, X, L.conn_host, L.owner_host, E, false);
+      level_xyz(L, p, X, L.conn_host, L.owner_host, E, false, c->PZ);
     }
     if (strategy == 4 && c->L.size() > 1) {  // III: every smoother and the coarse preconditioner too
       for (size_t li = 0; li + 1 < c->L.size(); ++li) fdm_refresh_vertical(c, (int)li, d_X);

@@ -175,6 +175,7 @@ __global__ void k_fnpf_rk4(int64_t n, double* __restrict__ x, const double* __re
 // ---------------------------------------------------------------- setup
 void fnpf_init(sem_ctx* c, const double* node_xyz, int strategy) {
   if (c->dist) throw SemError(SEM_EUNSUPPORTED, "FNPF stages: single-domain ctx only");
+  if (c->PZ != c->P) throw SemError(SEM_EUNSUPPORTED, "FNPF stages: isotropic orders only");
   if (strategy < 1 || strategy > 4) throw SemError(SEM_EINVAL, "strategy must be 1..4");
   if (strategy >= 3 && c->L.size() > 1 && !c->L[0].fdm)
     throw SemError(SEM_EUNSUPPORTED, "strategies II / III re-form the smoothers every stage: local_solve = 1 (FDM)");

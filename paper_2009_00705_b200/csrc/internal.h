@@ -67,7 +67,7 @@ enum : int {
 };
 
 struct DeviceLevel {
-  int p = 0, N = 0, Q = 0;
+  int p = 0, q = 0, N = 0, Q = 0;   // horizontal / vertical order (q = p isotropic)
   int64_t n = 0, nfree = 0;
   LevelRef ref;                 // host copy
   int32_t* conn = nullptr;      // [E][N], Dirichlet nodes stored as ~gid
@@ -199,7 +199,7 @@ struct sem_ctx {
   int E_global = 0;             // elements of the whole mesh
   int E = 0;                    // elements held (owned + halo in a partition)
   int E_own = 0;                // elements owned (applied); the first E_own of the E
-  int P = 0;
+  int P = 0, PZ = 0;            // finest horizontal / vertical order
   std::vector<sem::DeviceLevel> L;
   sem::Coarse C;
   double* scal = nullptr;       // device scalars [32]

@@ -207,6 +207,112 @@ static void apply_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y
   CUDA_CHECK(cudaGetLastError());
 }
 
+// Operator of an anisotropic level P_p(triangle) x P_q(t), any orders at run
+// time: one CTA per element, the same sum factorisation as k_apply<P> (eq 3.8) with the vertical
+// stages over q + 1 nodes / Gauss points.  Shared memory: the reference matrices, u_e, Ut/Udt,
+// the three cubature-point fields and Vt/Vdt.  elist: deterministic colour batches.
+__global__ void __launch_bounds__(128) k_apply_pq(int E, int nt, int n1, int qt, const int32_t* __restrict__ conn,
+                                                  const double* __restrict__ G, const double* __restrict__ mats,
+                                                  const double* __restrict__ u, double* __restrict__ y, int flags,
+                                                  const int32_t* __restrict__ elist) {
+  extern __shared__ double sm[];
+  const int ntp = nt | 1, N = nt * n1, qv = n1, Q = qt * qv;
+  const int e = elist ? elist[blockIdx.x] : blockIdx.x;
+  if (blockIdx.x >= E) return;
+  const double* B0 = mats;                 // [qt][ntp]
+  const double* Br = B0 + qt * ntp;
+  const double* Bs = Br + qt * ntp;
+  const double* Bt = Bs + qt * ntp;        // [qv][n1]
+  const double* Dt = Bt + n1 * n1;
+  double* ue = sm;                         // [N]
+  double* Ut = ue + N;                     // [nt][qv]
+  double* Ud = Ut + nt * qv;
+  double* g = Ud + nt * qv;                // [3][Q]
+  double* Vt = g + 3 * Q;                  // [nt][qv]
+  double* Vd = Vt + nt * qv;
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int32_t* ce = conn + (size_t)e * N;
+  for (int i = tid; i < N; i += T) {
+    const int c = __ldg(ce + i);
+    ue[i] = c >= 0 ? u[c] : ((flags & AP_GATHER_ALL) ? u[~c] : 0.0);
+  }
+  __syncthreads();
+  // A: Ut[m][z] = sum_l u[m + nt l] Bt[z][l], Ud with Dt
+  for (int i = tid; i < nt * qv; i += T) {
+    const int m = i / qv, z = i % qv;
+    double a = 0.0, b = 0.0;
+    for (int l = 0; l < n1; ++l) {
+      const double v = ue[m + nt * l];
+      a = fma(v, __ldg(Bt + z * n1 + l), a);
+      b = fma(v, __ldg(Dt + z * n1 + l), b);
+    }
+    Ut[i] = a;
+    Ud[i] = b;
+  }
+  __syncthreads();
+  // B and G: at every point (a, z): (g_r, g_s, g_0) = (Br Ut, Bs Ut, B0 Ud), w = G g
+  for (int pt = tid; pt < Q; pt += T) {
+    const int a = pt % qt, z = pt / qt;
+    double gr = 0.0, gs = 0.0, g0 = 0.0;
+    for (int m = 0; m < nt; ++m) {
+      const double ut = Ut[m * qv + z], ud = Ud[m * qv + z];
+      gr = fma(__ldg(Br + a * ntp + m), ut, gr);
+      gs = fma(__ldg(Bs + a * ntp + m), ut, gs);
+      g0 = fma(__ldg(B0 + a * ntp + m), ud, g0);
+    }
+    const double* Gp = G + (size_t)e * 6 * Q + pt;
+    const double xx = __ldg(Gp), xy = __ldg(Gp + Q), xz = __ldg(Gp + 2 * Q), yy = __ldg(Gp + 3 * Q),
+                 yz = __ldg(Gp + 4 * Q), zz = __ldg(Gp + 5 * Q);
+    g[pt] = xx * gr + xy * gs + xz * g0;
+    g[Q + pt] = xy * gr + yy * gs + yz * g0;
+    g[2 * Q + pt] = xz * gr + yz * gs + zz * g0;
+  }
+  __syncthreads();
+  // B^T: Vt[m][z] = sum_a Br[a][m] w_r + Bs[a][m] w_s, Vd[m][z] = sum_a B0[a][m] w_0
+  for (int i = tid; i < nt * qv; i += T) {
+    const int m = i / qv, z = i % qv;
+    double a1 = 0.0, a2 = 0.0;
+    for (int a = 0; a < qt; ++a) {
+      const int pt = a + qt * z;
+      a1 = fma(__ldg(Br + a * ntp + m), g[pt], fma(__ldg(Bs + a * ntp + m), g[Q + pt], a1));
+      a2 = fma(__ldg(B0 + a * ntp + m), g[2 * Q + pt], a2);
+    }
+    Vt[i] = a1;
+    Vd[i] = a2;
+  }
+  __syncthreads();
+  // A^T + scatter: y[m + nt l] (+/-)= sum_z Vt[m][z] Bt[z][l] + Vd[m][z] Dt[z][l]
+  const double sgn = (flags & AP_NEGATE) ? -1.0 : 1.0;
+  for (int i = tid; i < N; i += T) {
+    const int m = i % nt, l = i / nt;
+    double acc = 0.0;
+    for (int z = 0; z < qv; ++z)
+      acc = fma(Vt[m * qv + z], __ldg(Bt + z * n1 + l), fma(Vd[m * qv + z], __ldg(Dt + z * n1 + l), acc));
+    const int c = __ldg(ce + i);
+    if (c >= 0) atomicAdd(y + c, sgn * acc);
+    else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~c, sgn * acc);
+  }
+}
+
+static void apply_pq(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags) {
+  const LevelRef& R = L.ref;
+  const int smem = (R.N + 4 * R.nt * R.qv + 3 * R.Q) * (int)sizeof(double);
+  static int attr[kMaxDev] = {0};
+  if (smem > 48 * 1024) smem_opt_in(k_apply_pq, smem, attr);
+  if (c->E_own == 0) return;
+  if (c->det.on) {
+    for (size_t k = 0; k + 1 < c->det.ecol_off.size(); ++k) {
+      const int cnt = (int)(c->det.ecol_off[k + 1] - c->det.ecol_off[k]);
+      k_apply_pq<<<cnt, 128, smem, c->stream>>>(cnt, R.nt, R.n1, R.qt, L.conn, L.G, L.mats, u, y, flags,
+                                                c->det.ecol + c->det.ecol_off[k]);
+    }
+  } else {
+    k_apply_pq<<<c->E_own, 128, smem, c->stream>>>(c->E_own, R.nt, R.n1, R.qt, L.conn, L.G, L.mats, u, y, flags,
+                                                   nullptr);
+  }
+  CUDA_CHECK(cudaGetLastError());
+}
+
 // P <= 2 operators: one thread per element, y_e = A_e u_e with the element matrix
 // precomputed at setup (N(N+1)/2 packed entries, structure-of-arrays for coalescing).
 // P = 1: 168 B per element instead of G's 384 B; P = 2: 1368 B vs 1296 B, but no
@@ -276,6 +382,11 @@ void build_p1_matrices(sem_ctx* c, int level, const double* d_D) {
 }
 
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
+  if (c->L[level].p != c->L[level].q) {  // anisotropic level
+    apply_pq(c, c->L[level], u, y, flags);
+    c->launches++;
+    return;
+  }
   if (!c->det.on) {
     const DeviceLevel& L = c->L[level];
     if (L.p <= 2 && L.Ae1 && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3)) {

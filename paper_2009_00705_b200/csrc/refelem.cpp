@@ -251,19 +251,22 @@ static TriCub tri_cubature(int p) {
   return c;
 }
 
-LevelRef make_level_ref(int p) {
+LevelRef make_level_ref(int p, int qz) {
+  // P_p(triangle) x P_q(t): horizontal order p, vertical order q (q = p isotropic)
+  const int qo = qz < 0 ? p : qz;
   LevelRef L;
   L.p = p;
-  L.n1 = p + 1;
+  L.q = qo;
+  L.n1 = qo + 1;
   L.nt = n_tri(p);
   L.N = L.nt * L.n1;
   L.qt = (p + 1) * (p + 1);
-  L.qv = p + 1;
+  L.qv = qo + 1;
   L.Q = L.qt * L.qv;
   TriBasis tb(p);
   TriCub tc = tri_cubature(p);
-  Rule1D gv = gauss_legendre_rule(p + 1);
-  Lagrange1D h(lgl_rule(p).x);
+  Rule1D gv = gauss_legendre_rule(qo + 1);
+  Lagrange1D h(lgl_rule(qo).x);
   L.B0.resize(L.qt * L.nt);
   L.Br.resize(L.qt * L.nt);
   L.Bs.resize(L.qt * L.nt);
@@ -293,13 +296,15 @@ LevelRef make_level_ref(int p) {
   return L;
 }
 
-std::vector<double> geometry_matrix(int pg, int p) {
-  // d/dr, d/ds, d/dt of the order-pg nodal basis at the order-p cubature
+std::vector<double> geometry_matrix(int pg, int p, int qg, int q) {
+  // d/dr, d/ds, d/dt of the order-(pg, qg) nodal basis at the order-(p, q) cubature
+  if (qg < 0) qg = pg;
+  if (q < 0) q = p;
   TriBasis tb(pg);
   TriCub tc = tri_cubature(p);
-  Rule1D gv = gauss_legendre_rule(p + 1);
-  Lagrange1D h(lgl_rule(pg).x);
-  int ntg = n_tri(pg), n1g = pg + 1, Ng = ntg * n1g, qt = (p + 1) * (p + 1), qv = p + 1, Q = qt * qv;
+  Rule1D gv = gauss_legendre_rule(q + 1);
+  Lagrange1D h(lgl_rule(qg).x);
+  int ntg = n_tri(pg), n1g = qg + 1, Ng = ntg * n1g, qt = (p + 1) * (p + 1), qv = q + 1, Q = qt * qv;
   std::vector<double> out(3 * (size_t)Ng * Q);
   std::vector<double> L(ntg), Lr(ntg), Ls(ntg), hv(n1g), dh(n1g);
   for (int a = 0; a < qt; ++a) {
@@ -319,23 +324,26 @@ std::vector<double> geometry_matrix(int pg, int p) {
   return out;
 }
 
-void transfer_matrices(int pf, int pc, std::vector<double>& Itri, std::vector<double>& I1) {
+void transfer_matrices(int pf, int pc, std::vector<double>& Itri, std::vector<double>& I1, int qf, int qc) {
+  if (qf < 0) qf = pf;
+  if (qc < 0) qc = pc;
   TriBasis tf(pf), tc(pc);
   int ntf = n_tri(pf), ntc = n_tri(pc);
   Itri.assign((size_t)ntf * ntc, 0.0);
   for (int m = 0; m < ntf; ++m) tc.eval(tf.r[m], tf.s[m], &Itri[(size_t)m * ntc], nullptr, nullptr);
-  Rule1D gf = lgl_rule(pf);
-  Lagrange1D hc(lgl_rule(pc).x);
-  I1.assign((size_t)(pf + 1) * (pc + 1), 0.0);
-  for (int l = 0; l <= pf; ++l) hc.eval(gf.x[l], &I1[(size_t)l * (pc + 1)], nullptr);
+  Rule1D gf = lgl_rule(qf);
+  Lagrange1D hc(lgl_rule(qc).x);
+  I1.assign((size_t)(qf + 1) * (qc + 1), 0.0);
+  for (int l = 0; l <= qf; ++l) hc.eval(gf.x[l], &I1[(size_t)l * (qc + 1)], nullptr);
 }
 
-std::vector<double> reference_nodes(int p) {
+std::vector<double> reference_nodes(int p, int q) {
+  if (q < 0) q = p;
   TriBasis tb(p);
-  Rule1D g = lgl_rule(p);
+  Rule1D g = lgl_rule(q);
   int nt = n_tri(p);
-  std::vector<double> rst(3 * (size_t)nt * (p + 1));
-  for (int l = 0; l <= p; ++l)
+  std::vector<double> rst(3 * (size_t)nt * (q + 1));
+  for (int l = 0; l <= q; ++l)
     for (int m = 0; m < nt; ++m) {
       size_t n = m + (size_t)nt * l;
       rst[3 * n + 0] = tb.r[m];

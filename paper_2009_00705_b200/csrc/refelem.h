@@ -35,28 +35,30 @@ struct TriBasis {
 };
 
 inline int n_tri(int p) { return (p + 1) * (p + 2) / 2; }
-inline int n_prism(int p) { return n_tri(p) * (p + 1); }
+inline int n_prism(int p, int q = -1) { return n_tri(p) * ((q < 0 ? p : q) + 1); }
 
 // Reference data of one multigrid level of order p.
 struct LevelRef {
-  int p, n1, nt, N, qt, qv, Q;
+  int p, q, n1, nt, N, qt, qv, Q;   // q: vertical order (n1 = qv = q + 1); q = p isotropic
   std::vector<double> B0, Br, Bs;   // [qt][nt]
   std::vector<double> Bt, Dt;       // [qv][n1]
   std::vector<double> wq;           // [Q] cubature weights, q = a + qt*qv
   std::vector<double> Dfull;        // [3][Q][N] full reference gradients (setup only)
   std::vector<int> li, lj, ll;      // lattice coords of local nodes [N]
 };
-LevelRef make_level_ref(int p);
+// P_p(triangle) x P_q(t) (the paper's (P_xy, P_z)); q < 0: q = p
+LevelRef make_level_ref(int p, int q = -1);
 
-// Derivatives of the order-pg nodal basis at the cubature of order p:
+// Derivatives of the order-(pg, qg) nodal basis at the cubature of order (p, q):
 // layout [n][c][Q] (n = geometry node, c = r,s,t) for the geometry kernel.
-std::vector<double> geometry_matrix(int pg, int p);
+std::vector<double> geometry_matrix(int pg, int p, int qg = -1, int q = -1);
 
-// Transfer (prolongation) factors from order pc to order pf:
+// Transfer (prolongation) factors from order (pc, qc) to order (pf, qf):
 // Itri[mf][mc] = L^c_mc(node mf of pf), I1[lf][lc] = h^c_lc(t_lf).
-void transfer_matrices(int pf, int pc, std::vector<double>& Itri, std::vector<double>& I1);
+void transfer_matrices(int pf, int pc, std::vector<double>& Itri, std::vector<double>& I1, int qf = -1,
+                       int qc = -1);
 
 // Reference node coordinates [N][3] in the documented local order.
-std::vector<double> reference_nodes(int p);
+std::vector<double> reference_nodes(int p, int q = -1);
 
 }  // namespace sem

@@ -62,8 +62,9 @@ struct Scratch {
 
 struct GlobalModel {
   HostMesh hm;
-  int P = 0;
-  std::vector<int> sched;
+  int P = 0, PZ = 0;              // finest horizontal / vertical order (PZ = P isotropic)
+  std::vector<int> sched;         // horizontal order of every level, finest first
+  std::vector<int> schedz;        // vertical order of every level
   std::vector<double> X;          // [E][N(P)][3] finest nodal map
   std::vector<LevelTopo> topo;    // global numbering per level
   std::vector<int> user_part;     // sem_mesh.part (empty = the library's column partition)

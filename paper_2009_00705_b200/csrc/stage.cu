@@ -234,7 +234,8 @@ void coarse_refresh_lines(sem_ctx* c) {
 // Operator of level li (G, the a-tile copy, the P <= 2 element matrices) from the finest nodal map X
 void refresh_level_operator(sem_ctx* c, int li, const double* X, const double* d_gm, const double* d_w) {
   DeviceLevel& L = c->L[li];
-  if (launch_geometry(c, li, X, d_gm, n_prism(c->P), d_w)) throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
+  if (launch_geometry(c, li, X, d_gm, n_prism(c->P, c->PZ), d_w))
+    throw SemError(SEM_EBADELEM, "detJ <= 0 at a cubature point");
   if (L.Gw) build_g_tiles(c, li);
   if (L.Ae1) {
     Scratch s2;

@@ -88,17 +88,21 @@ Entities build_entities(const HostMesh& m) {
   return ent;
 }
 
-LevelTopo number_level(const HostMesh& m, const Entities& ent, int p) {
+LevelTopo number_level(const HostMesh& m, const Entities& ent, int p, int qz) {
+  // P_p(triangle) x P_q(t): p - 1 nodes per triangle edge, q - 1 per vertical
+  // edge, (p - 1)(q - 1) per lateral quad face, nti (q - 1) per element interior
+  const int q = qz < 0 ? p : qz;
   LevelTopo L;
   L.p = p;
-  const int nt = (p + 1) * (p + 2) / 2, n1 = p + 1, N = nt * n1;
+  L.q = q;
+  const int nt = (p + 1) * (p + 2) / 2, n1 = q + 1, N = nt * n1;
   L.N = N;
   const int E = m.E;
   L.conn.resize((size_t)E * N);
   L.owner.assign((size_t)E * N, 0);
   // entity bases (first touch); -1 = unassigned
   std::vector<int64_t> vbase(m.nv, -1), ebase(ent.n_edge, -1), tbase(ent.n_tface, -1), qbase(ent.n_qface, -1);
-  const int ne = p - 1, nti = (p - 1) * (p - 2) / 2, nq = (p - 1) * (p - 1);
+  const int ne = p - 1, nev = q - 1, nti = (p - 1) * (p - 2) / 2, nq = (p - 1) * (q - 1);
   int64_t next = 0;
   auto take = [&](std::vector<int64_t>& base, int32_t id, int cnt) {
     if (base[id] < 0) { base[id] = next; next += cnt; }
@@ -130,7 +134,7 @@ LevelTopo number_level(const HostMesh& m, const Entities& ent, int p) {
     for (int n = 0; n < N; ++n) {
       const int i = li[n], j = lj[n], l = ll[n], k = p - i - j;
       const int zeros = (i == 0) + (j == 0) + (k == 0);
-      const int vert = (l == 0) ? 0 : (l == p ? 1 : 2);  // bottom, top, middle
+      const int vert = (l == 0) ? 0 : (l == q ? 1 : 2);  // bottom, top, middle
       int64_t gid;
       if (zeros == 2) {  // triangle vertex t
         const int t = (k == p) ? 0 : (i == p ? 1 : 2);
@@ -138,8 +142,8 @@ LevelTopo number_level(const HostMesh& m, const Entities& ent, int p) {
           gid = take(vbase, v[3 * vert + t], 1);
         } else {  // vertical edge, position l from the bottom vertex
           int32_t a = v[t], b = v[3 + t];
-          int s = (a < b) ? l : p - l;
-          gid = take(ebase, ent.edge[(size_t)e * 9 + 6 + t], ne) + (s - 1);
+          int s = (a < b) ? l : q - l;
+          gid = take(ebase, ent.edge[(size_t)e * 9 + 6 + t], nev) + (s - 1);
         }
       } else if (zeros == 1) {  // triangle edge
         int te, s;  // edge index (01, 12, 20) and position from its first vertex
@@ -155,8 +159,8 @@ LevelTopo number_level(const HostMesh& m, const Entities& ent, int p) {
           int32_t c00 = v[ta], cp0 = v[tb], c0p = v[3 + ta], cpp = v[3 + tb];
           int32_t mn = std::min(std::min(c00, cp0), std::min(c0p, cpp));
           int ss = (mn == cp0 || mn == cpp) ? p - s : s;
-          int lv = (mn == c0p || mn == cpp) ? p - l : l;
-          gid = take(qbase, ent.qface[(size_t)e * 3 + te], nq) + (int64_t)(ss - 1) * (p - 1) + (lv - 1);
+          int lv = (mn == c0p || mn == cpp) ? q - l : l;
+          gid = take(qbase, ent.qface[(size_t)e * 3 + te], nq) + (int64_t)(ss - 1) * (q - 1) + (lv - 1);
         }
       } else {  // triangle interior
         if (vert < 2) {
@@ -171,9 +175,9 @@ LevelTopo number_level(const HostMesh& m, const Entities& ent, int p) {
           gid = take(tbase, ent.tface[(size_t)e * 2 + vert], nti) + off;
         } else {
           // element interior: one block per element, taken at the first interior node met
-          if (int_e != e) { int_e = e; int_base = next; next += (int64_t)nti * (p - 1); }
+          if (int_e != e) { int_e = e; int_base = next; next += (int64_t)nti * (q - 1); }
           int64_t base = int_base;
-          gid = base + (int64_t)tri_int[j * (p + 1) + i] * (p - 1) + (l - 1);
+          gid = base + (int64_t)tri_int[j * (p + 1) + i] * (q - 1) + (l - 1);
         }
       }
       if (gid >= (int64_t)INT32_MAX) throw std::runtime_error("node count exceeds int32");
@@ -192,7 +196,7 @@ LevelTopo number_level(const HostMesh& m, const Entities& ent, int p) {
       if (tg[f] != 1) continue;
       for (int n = 0; n < N; ++n) {
         const int i = li[n], j = lj[n], l = ll[n], k = p - i - j;
-        bool on = (f == 0 && l == 0) || (f == 1 && l == p) || (f == 2 && j == 0) || (f == 3 && k == 0) ||
+        bool on = (f == 0 && l == 0) || (f == 1 && l == q) || (f == 2 && j == 0) || (f == 3 && k == 0) ||
                   (f == 4 && i == 0);
         if (on) L.dir[L.conn[(size_t)e * N + n]] = 1;
       }
@@ -206,14 +210,14 @@ LevelTopo number_level(const HostMesh& m, const Entities& ent, int p) {
 
 SchwarzTopo schwarz_topology(const LevelTopo& L, int E, int overlap, int nthreads) {
   SchwarzTopo S;
-  const int p = L.p, N = L.N;
+  const int p = L.p, q = L.q > 0 ? L.q : L.p, N = L.N;
   const int64_t n = L.n;
   // lattice pattern of reading O15: |dl| <= 1 and horizontal offset 0 or one
   // triangular-lattice step (barycentric offsets +-(1,-1,0) and permutations)
   std::vector<int> li(N), lj(N), ll(N);
   {
     int c = 0;
-    for (int l = 0; l <= p; ++l)
+    for (int l = 0; l <= q; ++l)
       for (int j = 0; j <= p; ++j)
         for (int i = 0; i <= p - j; ++i) { li[c] = i; lj[c] = j; ll[c] = l; ++c; }
   }

@@ -25,14 +25,14 @@ struct Entities {
 Entities build_entities(const HostMesh& m);
 
 struct LevelTopo {
-  int p = 0, N = 0;
+  int p = 0, q = 0, N = 0;          // horizontal / vertical order (q = p isotropic)
   int64_t n = 0, nfree = 0;
   std::vector<int32_t> conn;      // [E][N] global ids (unsigned)
   std::vector<uint8_t> dir;       // [n] 1 = Dirichlet
   std::vector<uint8_t> owner;     // [E][N] 1 = first occurrence of the node in element order
 };
 // throws std::runtime_error on bad input
-LevelTopo number_level(const HostMesh& m, const Entities& ent, int p);
+LevelTopo number_level(const HostMesh& m, const Entities& ent, int p, int q = -1);
 
 struct SchwarzTopo {
   std::vector<int64_t> off;       // [E+1] into idx (unpadded)
