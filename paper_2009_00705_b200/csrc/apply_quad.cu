@@ -320,23 +320,28 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
       __syncwarp();  // every lane is done with this slot before it is refilled
       issue(t + D::R);
       // ---- stage B^T: V^T[(q,e)][m] += w^T[(q,e)][a] B_c[a][m]; k-step i <-> a = 8 na + 2 c4 + i
+      // B^T operands of both k-steps (a = 8 na + 2 c4 + {0, 1}) in one 16-byte load per component;
+      // the DMMAs then sweep all (mt, nm) accumulators per operand, so that two updates of one
+      // accumulator are MTQ x NM instructions apart (no back-to-back dependent DMMA)
+      double2 bo[3][D::NM];
 #pragma unroll
       for (int nm = 0; nm < D::NM; ++nm) {
-        // B^T operands of both k-steps (a = 8 na + 2 c4 + {0, 1}) in one 16-byte load per component
         const int off = (8 * nm + r4) * D::LDA + 8 * na + 2 * c4;
-        const double2 br = *reinterpret_cast<const double2*>(BmT + off);
-        const double2 bs = *reinterpret_cast<const double2*>(BmT + 8 * D::NM * D::LDA + off);
-        const double2 b0 = *reinterpret_cast<const double2*>(BmT + 16 * D::NM * D::LDA + off);
 #pragma unroll
-        for (int mt = 0; mt < D::MTQ; ++mt) {
-          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[0][mt][0], br.x);
-          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[1][mt][0], bs.x);
-          aq_dmma(Vd[mt][nm][0], Vd[mt][nm][1], g[2][mt][0], b0.x);
-          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[0][mt][1], br.y);
-          aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[1][mt][1], bs.y);
-          aq_dmma(Vd[mt][nm][0], Vd[mt][nm][1], g[2][mt][1], b0.y);
-        }
+        for (int c = 0; c < 3; ++c) bo[c][nm] = *reinterpret_cast<const double2*>(BmT + 8 * c * D::NM * D::LDA + off);
       }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int mt = 0; mt < D::MTQ; ++mt)
+#pragma unroll
+            for (int nm = 0; nm < D::NM; ++nm) {
+              const double b = i ? bo[c][nm].y : bo[c][nm].x;
+              if (c < 2) aq_dmma(Vt[mt][nm][0], Vt[mt][nm][1], g[c][mt][i], b);
+              else aq_dmma(Vd[mt][nm][0], Vd[mt][nm][1], g[2][mt][i], b);
+            }
     }
     // ---- stage A^T (FMA): y[m][l] over the lane's q = 2 mt + h, partner lane (h ^ 1) adds the rest
     double yp[D::NM][2][D::N1];
