@@ -183,6 +183,10 @@ VARIANTS = [
      dict(local_solve=1, overlap=1)),
     ("mixed", "exact dense local inverses and coarse inverse STORED in FP32, FP64 arithmetic (P:35)",
      dict(local_solve=0, overlap=1, mixed_precision=1)),
+    ("condensed", "statically condensed system (element-interior nodes eliminated, P:630-663, reading O43), "
+     "exact dense local inverses, overlap 1", dict(local_solve=0, overlap=1, condensed=True)),
+    ("fdm_condensed", "statically condensed system (P:630-663, O43), FDM local solves, overlap 1",
+     dict(local_solve=1, overlap=1, condensed=True)),
 ]
 
 
@@ -193,30 +197,38 @@ def run_variants(args, lib, m, phiD_h, peak, base_kw):
     out = []
     for name, desc, extra in VARIANTS:
         kw = dict(base_kw)
+        extra = dict(extra)
+        cond = extra.pop("condensed", False)
         kw.update(extra)
-        if kw == base_kw:
+        if kw == base_kw and not cond:
             continue
         t0 = time.perf_counter()
         s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)), **kw)
+        if cond:
+            s.condensed_info()   # forms the interior factors (setup)
         setup_s = time.perf_counter() - t0
         phiD = torch.from_numpy(phiD_h).cuda()
         phi = s.empty(0)
+        solve = (lambda: s.solve_condensed(phiD, args.tol, out=phi)) if cond else (
+            lambda: s.solve(phiD, args.tol, out=phi))
         for _ in range(args.warmup):
-            s.solve(phiD, args.tol, out=phi)
+            solve()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s.stream)
         for _ in range(args.steps):
-            _, rep = s.solve(phiD, args.tol, out=phi)
+            _, rep = solve()
         e1.record(s.stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
         us, b = s.bench_kernel("schwarz", 0, 20)
         ach = b / (us * 1e-6) / 1e9
-        out.append({"name": name, "smoother": desc, "value": s.info["n_free"] / (ms * 1e-3) / 1e6,
+        out.append({"name": name, "smoother": desc, "solve": "laplace_solve_condensed" if cond else "laplace_solve",
+                    "value": s.info["n_free"] / (ms * 1e-3) / 1e6,
                     "unit": "MDOF/s", "ms_per_step": ms, "iters": rep["iters"], "vcycles": rep["vcycles"],
                     "rel_res": rep["rel_res"], "setup_s": setup_s,
-                    "smoother_kernel": {"kernel": "k_fdm_warp" if extra.get("local_solve") else "k_schwarz<float>",
+                    "smoother_kernel": {"kernel": "k_fdm_warp" if extra.get("local_solve") else (
+                                        "k_schwarz<float>" if extra.get("mixed_precision") else "k_schwarz<double>"),
                                         "us": us, "alg_bytes_per_launch": b, "achieved_GBs": ach,
                                         "frac_hbm": ach / peak}})
         s.close()
@@ -380,7 +392,32 @@ def sweep_one(args, p, variant):
            "MDOF_s": i["n_free"] / (ms * 1e-3) / 1e6, "setup_s": setup_s, "device_GB": i["device_bytes"] / 1e9,
            "smoother_kernels": i["smoother_kernel"],
            "solve_roofline": solve_roofline(s, rep, ms, peak) if p > 1 else None}
+    if p >= 3:  # the same solve on the statically condensed system (NEXT-3): same ctx, same stop test
+        out["condensed"] = timed_condensed(args, s, phiD, phi)
     print("SWEEP " + json.dumps(out), flush=True)
+
+
+def timed_condensed(args, s, phiD, phi):
+    """laplace_solve_condensed timed like the plain solve (warm-ups, then args.steps solves
+    between CUDA events on the ctx's stream); the one-off interior factorisation is setup."""
+    import torch
+    t0 = time.perf_counter()
+    ni, nb, by = s.condensed_info()
+    cond_setup_s = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        s.solve_condensed(phiD, args.tol, out=phi, check=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s.stream)
+    for _ in range(args.steps):
+        _, rep = s.solve_condensed(phiD, args.tol, out=phi, check=False)
+    e1.record(s.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    return {"MDOF_s": s.info["n_free"] / (ms * 1e-3) / 1e6, "ms_per_step": ms, "iters": rep["iters"],
+            "vcycles": rep["vcycles"], "q_mean": rep["q_mean"], "rel_res": rep["rel_res"],
+            "converged": rep["converged"], "interior_per_elem": ni, "skeleton_per_elem": nb,
+            "factor_GB": by / 1e9, "factor_setup_s": cond_setup_s}
 
 
 def run_sweep(args):

@@ -245,6 +245,32 @@ int laplace_solve(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
 int laplace_solve_guess(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
                         double tol, double *phi, sem_report *rep);
 
+/* laplace_solve on the statically condensed system (the
+ * supplement's "Static Condensation", eq (laplacecondensed)
+ * P:655-657; reading O43):
+ *   S phi_b = b_b - A_bi A_ii^-1 b_i,  S = A_bb - A_bi A_ii^-1 A_ib,
+ *   A_ii phi_i = b_i - A_ib phi_b,
+ * with i = the element-interior nodes of the finest level (triangle lattice
+ * i, j, k >= 1 and 0 < l < q: one element each, so A_ii is block diagonal) and
+ * b = every other free node.  The outer iteration opts.outer runs on S with the
+ * preconditioner phi_b <- (V(r))_b (the skeleton block of the full-system
+ * V-cycle, which approximates (A^-1)_bb = S^-1); iterates keep their interior
+ * values as the exact interior solve of their skeleton values, so phi (output,
+ * including Dirichlet values) is the full solution and the residual tested
+ * against tol*||b_F - A_FD phi_D|| + atol is the full system's.
+ * guess != 0: phi is read on free skeleton nodes as the initial phi_b.
+ * The per-element factors (A_ii^-1 A_ib and A_ii^-1, FP64, E*ni*(nb+ni)*8
+ * bytes) are formed on the device on the first call and after every
+ * sem_update_geometry (SEM_ENOMEM if they do not fit).  Element orders with
+ * no interior nodes (p < 3 or q < 2) reduce to laplace_solve.  Single-domain
+ * ctx only (SEM_EUNSUPPORTED otherwise).  rhs, dirichlet_phi, phi: device. */
+int laplace_solve_condensed(sem_ctx *ctx, const double *rhs, const double *dirichlet_phi,
+                            double tol, double *phi, int guess, sem_report *rep);
+
+/* Sizes of the condensation (forms the factors if not yet formed): interior
+ * and skeleton nodes per element and the device bytes of the factors. */
+int sem_condensed_info(sem_ctx *ctx, int *n_interior, int *n_skeleton, int64_t *bytes);
+
 /* New element geometry for the next time stage (Fig 5.1;
  * readings O41, O42): node_xyz is the nodal map in sem_mesh.node_xyz's layout (host,
  * copied), with the same mesh topology.

@@ -72,6 +72,8 @@ _lib.pmg_vcycle.argtypes = [_vp, _vp, _vp]
 _lib.laplace_solve.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
 _lib.laplace_solve_host.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
 _lib.laplace_solve_guess.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(SemReport)]
+_lib.laplace_solve_condensed.argtypes = [_vp, _vp, _vp, C.c_double, _vp, C.c_int, C.POINTER(SemReport)]
+_lib.sem_condensed_info.argtypes = [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64)]
 _lib.sem_update_geometry.argtypes = [_vp, _dp, C.c_int]
 _lib.sem_prolong.argtypes = [_vp, C.c_int, _vp, _vp]
 _lib.sem_restrict.argtypes = [_vp, C.c_int, _vp, _vp]
@@ -98,7 +100,7 @@ _lib.sem_host_reference.argtypes = [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.sem_host_partition.argtypes = [C.POINTER(SemMesh), C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp]
 
-EXPORTS = ["sem_reference_nodes_pq", "sem_fnpf_init", "sem_fnpf_surface_nodes", "fnpf_rhs", "fnpf_erk4_step", "laplace_solve_guess", "sem_update_geometry", "sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
+EXPORTS = ["laplace_solve_condensed", "sem_condensed_info", "sem_reference_nodes_pq", "sem_fnpf_init", "sem_fnpf_surface_nodes", "fnpf_rhs", "fnpf_erk4_step", "laplace_solve_guess", "sem_update_geometry", "sem_host_fdm", "sem_bench_kernel", "sem_host_partition", "sem_nccl_unique_id", "sem_host_numbering", "sem_host_schwarz", "sem_host_reference", "sem_default_opts", "sem_reference_nodes", "sem_setup", "sem_get_info", "sem_node_xyz",
            "sem_dirichlet_mask", "sem_apply_laplace", "pmg_vcycle", "laplace_solve", "laplace_solve_host",
            "sem_prolong", "sem_restrict", "sem_schwarz", "sem_coarse_solve", "sem_launch_count",
            "sem_destroy", "sem_strerror", "sem_last_error"]
@@ -350,6 +352,23 @@ class Solver:
         if check and code != 0:
             raise SemError(code, "laplace_solve_guess")
         return phi, rep.as_dict()
+
+    def solve_condensed(self, dirichlet_phi, tol, rhs=None, out=None, guess=False, check=True):
+        """laplace_solve_condensed (static condensation, NEXT-3): with guess=True `out` holds the
+        initial guess (read on free skeleton nodes)."""
+        phi = self.empty(0) if out is None else out
+        rep = SemReport()
+        code = _lib.laplace_solve_condensed(self._ctx, None if rhs is None else _ptr(rhs), _ptr(dirichlet_phi), tol,
+                                            _ptr(phi), int(bool(guess)), C.byref(rep))
+        if check and code != 0:
+            raise SemError(code, "laplace_solve_condensed")
+        return phi, rep.as_dict()
+
+    def condensed_info(self):
+        """sem_condensed_info: (interior, skeleton) nodes per element and the factor bytes."""
+        ni, nb, by = C.c_int(), C.c_int(), C.c_int64()
+        _check(_lib.sem_condensed_info(self._ctx, C.byref(ni), C.byref(nb), C.byref(by)), "sem_condensed_info")
+        return ni.value, nb.value, by.value
 
     def update_geometry(self, node_xyz, strategy=1):
         """sem_update_geometry: new nodal map [n_prism][N(p)][3] (same topology)."""

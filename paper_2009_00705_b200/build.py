@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = ["csrc/refelem.cpp", "csrc/topology.cpp", "csrc/partition.cpp", "csrc/kernels.cu", "csrc/apply_dmma.cu", "csrc/apply_warp.cu", "csrc/apply_quad.cu",
-       "csrc/capi.cu", "csrc/coarse.cu", "csrc/fnpf.cu", "csrc/stage.cu", "csrc/dist.cu", "csrc/fdm.cpp", "csrc/fdm.cu"]
+       "csrc/capi.cu", "csrc/coarse.cu", "csrc/fnpf.cu", "csrc/stage.cu", "csrc/condense.cu", "csrc/dist.cu", "csrc/fdm.cpp", "csrc/fdm.cu"]
 LIB = os.path.join(HERE, "libsem_pmg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -822,7 +822,7 @@ void read_scalars(sem_ctx* c, int n) {
 
 // ------------------------------------------------------------------ solve
 int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep,
-             int guess = 0) {
+             int guess = 0, int cond = 0) {
   if (!phiD || !phi) throw SemError(SEM_EINVAL, "dirichlet_phi and phi are required");
   if (!(tol >= 0.0)) throw SemError(SEM_EINVAL, "tol must be >= 0");
   DeviceLevel& L = c->L[0];
@@ -851,7 +851,20 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
   R.norm_f = nf;
   const double thresh = tol * nf + o.atol;
   double rn = nf;
-  if (guess) {  // warm start (NEXT-1, the paper's per-stage solves): u_F = phi_F, r = b_F - A_FF u_F
+  if (cond) {
+    // static condensation (NEXT-3; condense.cu): u = E u_b + [0; A_ii^-1 b_i] with
+    // u_b = phi_b (warm start) or 0, r = b_F - A_FF u (zero on the interior nodes)
+    if (guess) {
+      launch_init_masked(c, 0, phi, u, 1);
+      cond_extend(c, u);
+    }
+    cond_interior(c, r, u);
+    launch_apply(c, 0, u, r, AP_NEGATE);
+    cond_zero(c, r);
+    launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 6);
+    read_scalars(c, 7);
+    rn = std::sqrt(c->hscal[6]);
+  } else if (guess) {  // warm start (NEXT-1, the paper's per-stage solves): u_F = phi_F, r = b_F - A_FF u_F
     launch_init_masked(c, 0, phi, u, 1);
     launch_apply(c, 0, u, r, AP_NEGATE);
     launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 6);
@@ -867,6 +880,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
     // preconditioner is not exactly linear: flexible CG (Polak-Ribiere beta)
     const bool flex = c->C.iterative != 0;
     vcycle_pcg(c, r, p);
+    if (cond) cond_extend(c, p);   // condensed preconditioner E (V r)_b
     R.vcycles++;
     int dcur = 8, dnew = 10;  // [d] = z^T r, [d+1] = z^T r_old
     launch_dot2(c, n, p, r, nullptr, nullptr, nullptr, sc + dcur);
@@ -874,6 +888,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
       // q = A p (masked: p is 0 on Dirichlet nodes)
       CUDA_CHECK(cudaMemsetAsync(q, 0, sizeof(double) * n, c->stream));
       launch_apply(c, 0, p, q, 0);
+      if (cond) cond_zero(c, q);     // (A E p_b)_i = 0: q = [S p_b; 0]
       launch_dot2(c, n, p, q, nullptr, nullptr, nullptr, sc + 1);
       if (flex) CUDA_CHECK(cudaMemcpyAsync(c->rw_old, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
       // alpha = delta / p^T q; u += alpha p; r -= alpha q; ||r||^2
@@ -892,6 +907,7 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
       }
       // z = V(r); beta = z^T r / delta (flexible: z^T (r - r_old) / delta); p = z + beta p
       vcycle_pcg(c, r, z);
+      if (cond) cond_extend(c, z);
       R.vcycles++;
       if (flex) {
         launch_dot2(c, n, z, r, z, c->rw_old, nullptr, sc + dnew);
@@ -907,11 +923,13 @@ int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, doub
     const double* bF = c->rw_old;  // b_F of the lift (kept below)
     while (R.iters < o.imax) {
       vcycle(c, 0, r, z);
+      if (cond) cond_extend(c, z);
       R.vcycles++;
       launch_axpy(c, n, 1.0, z, u);
       // r = b_F - A_FF u (one operator apply per iteration)
       CUDA_CHECK(cudaMemcpyAsync(r, bF, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
       launch_apply(c, 0, u, r, AP_NEGATE);
+      if (cond) cond_zero(c, r);
       R.iters++;
       launch_dot2(c, n, r, r, nullptr, nullptr, nullptr, sc + 3);
       read_scalars(c, 4);
@@ -1123,6 +1141,47 @@ int laplace_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol,
   }
 }
 
+int laplace_solve_condensed(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, int guess,
+                            sem_report* rep) {
+  if (!c) return SEM_EINVAL;
+  if (c->dist) return SEM_EUNSUPPORTED;
+  DeviceGuard guard(c->device);
+  try {
+    if (!phiD || !phi) throw SemError(SEM_EINVAL, "dirichlet_phi and phi are required");
+    if (!c->cond) {
+      try {
+        condense_setup(c);
+      } catch (...) {
+        condense_destroy(c);
+        throw;
+      }
+    }
+    return do_solve(c, rhs, phiD, tol, phi, rep, guess ? 1 : 0, 1);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+}
+
+int sem_condensed_info(sem_ctx* c, int* n_interior, int* n_skeleton, int64_t* bytes) {
+  if (!c || !n_interior || !n_skeleton || !bytes) return SEM_EINVAL;
+  if (c->dist) return SEM_EUNSUPPORTED;
+  DeviceGuard guard(c->device);
+  try {
+    if (!c->cond) {
+      try {
+        condense_setup(c);
+      } catch (...) {
+        condense_destroy(c);
+        throw;
+      }
+    }
+    cond_sizes(c, n_interior, n_skeleton, bytes);
+  } catch (const SemError& e) {
+    return fail(e);
+  }
+  return SEM_OK;
+}
+
 int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
   if (!c || !node_xyz || (strategy != 1 && strategy != 2 && strategy != 4)) return SEM_EINVAL;
   if (c->dist) return SEM_EUNSUPPORTED;
@@ -1131,6 +1190,7 @@ int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
     if (strategy == 4 && c->L.size() > 1 && (!c->L[0].fdm || !c->C.iterative))
       throw SemError(SEM_EUNSUPPORTED, "strategy III (4) re-forms smoothers and coarse preconditioner every stage: "
                                        "needs local_solve = 1 and coarse_solver = 1");
+    condense_destroy(c);   // the interior factorisations follow the geometry (re-formed on the next condensed solve)
     const int p = c->P, Nf = n_prism(p, c->PZ), E = c->E;
     std::vector<double> X(node_xyz, node_xyz + (size_t)E * Nf * 3);
     Scratch sc;
@@ -1362,6 +1422,7 @@ void sem_destroy(sem_ctx* c) {
     if (c->vc_graph[i]) cudaGraphExecDestroy(c->vc_graph[i]);
   coarse_destroy(c);
   fnpf_destroy(c);
+  condense_destroy(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hscal) cudaFreeHost(c->hscal);

@@ -30,7 +30,8 @@
 
 namespace sem {
 
-int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep, int guess);
+int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep, int guess,
+             int cond);
 
 struct Fnpf {
   int64_t ns = 0;                 // free-surface nodes
@@ -336,7 +337,7 @@ void fnpf_stage(sem_ctx* c, const double* eta, const double* phis, double* deta,
   k_fnpf_scatter<<<fgrid(F.ns, 256), 256, 0, c->stream>>>(F.ns, F.snode, phis, F.phiD);
   CUDA_CHECK(cudaGetLastError());
   c->launches++;
-  int st = do_solve(c, nullptr, F.phiD, tol, F.phi, rep, F.warm);
+  int st = do_solve(c, nullptr, F.phiD, tol, F.phi, rep, F.warm, 0);
   if (st != SEM_OK && st != SEM_ENOTCONV) throw SemError(st, "FNPF stage solve failed");
   F.warm = 1;
   CUDA_CHECK(cudaMemsetAsync(F.acc, 0, 5 * F.ns * sizeof(double), c->stream));

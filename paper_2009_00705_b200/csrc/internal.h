@@ -153,6 +153,7 @@ void det_finalize(sem_ctx* c, int nb, double* out0, double* out1);
 
 struct Dist;  // dist.cu
 struct Fnpf;  // fnpf.cu
+struct Condense;  // condense.cu
 
 struct Coarse {
   int64_t nc = 0;               // free coarse nodes
@@ -211,6 +212,8 @@ struct sem_ctx {
   sem::Det det;                 // deterministic mode (opts.deterministic)
   // ---- FNPF time stages (fnpf.cu)
   sem::Fnpf* fnpf = nullptr;
+  // ---- static condensation of element-interior nodes (condense.cu)
+  sem::Condense* cond = nullptr;
   int64_t launches = 0;
   int64_t device_bytes = 0;
   double setup_ms = 0.0;
@@ -268,6 +271,13 @@ void fnpf_stage(sem_ctx* c, const double* eta, const double* phis, double* deta,
 void fnpf_erk4(sem_ctx* c, double* eta, double* phis, double dt, double tol, int linear, int* iters);
 int64_t fnpf_surface(const sem_ctx* c, int32_t* ids);
 void fnpf_destroy(sem_ctx* c);
+// condense.cu: static condensation
+void condense_setup(sem_ctx* c);
+void condense_destroy(sem_ctx* c);
+void cond_extend(sem_ctx* c, double* v);
+void cond_interior(sem_ctx* c, const double* src, double* dst);
+void cond_zero(sem_ctx* c, double* v);
+void cond_sizes(const sem_ctx* c, int* ni, int* nb, int64_t* bytes);
 void launch_xpby(sem_ctx* c, int64_t n, double* p, const double* z, const double* num, const double* den, int mode);
 void launch_combine_phi(sem_ctx* c, int level, const double* uF, const double* phiD, double* phi);
 void launch_axpy(sem_ctx* c, int64_t n, double a, const double* x, double* y);
