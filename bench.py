@@ -276,6 +276,10 @@ def run_config5(args, lib, peak):
            "smoother_kernel": {"kernel": "k_fdm_cta<8> + k_schwarz<double> (O35 subset)", "us": us,
                                "alg_bytes_per_launch": b, "achieved_GBs": b / us / 1e3, "frac_hbm": b / us / 1e3 / peak},
            "apply": {"kernel": "k_apply_warp<6>", "us": ua, "achieved_GBs": ba / ua / 1e3, "frac": ba / ua / 1e3 / peak}}
+    try:  # the same solve on the statically condensed system (NEXT-3), same ctx and stop test
+        out["condensed"] = timed_condensed(args, s, phiD, phi)
+    except lib.SemError as e:
+        out["condensed"] = {"error": str(e)}
     s.close()
     del s
     torch.cuda.empty_cache()
