@@ -139,6 +139,14 @@ typedef struct {
                                  levels = {5, 3, 1}, levels_z = {3, 3, 1}); NULL = levels (isotropic), or,
                                  without levels, semi-coarsening of the larger order first until the
                                  orders agree, then P -> ceil((P+1)/2) (reading O19)                   */
+  int coarse_agg;             /* iterative coarse solve (reading O9): aggregates of the two-level
+                                 correction added to its vertical-line preconditioner,
+                                 z = T^-1 r + P_a A_a^-1 P_a^T r (P_a piecewise constant on groups of
+                                 whole lines, A_a = P_a^T A P_a, dense inverse formed at setup;
+                                 reading O44).  -1 (default) auto: min(1024, lines / 32) when there are
+                                 >= 4096 lines, else off; 0 off; > 0 that many (at most the line
+                                 count).  Off in deterministic mode.  Under strategy III the lines are
+                                 re-formed every stage and A_a^-1 stays that of setup.              */
 } sem_opts;
 
 typedef struct {
@@ -175,6 +183,7 @@ typedef struct {
                                  coarsest level)                                                     */
   int smoother_mt[16];        /* FDM levels: 8-row tiles of the largest horizontal patch, ceil(n_h/8) */
   int level_pz[16];           /* vertical polynomial order of each level (= level_p when isotropic)   */
+  int coarse_agg;             /* aggregates of the iterative coarse solve's two-level correction (0: none) */
 } sem_info;
 
 /* sem_info.smoother_kernel */

@@ -29,7 +29,7 @@ class SemOpts(C.Structure):
                 ("coarse_rtol", C.c_double), ("coarse_maxit", C.c_int), ("nranks", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("local_solve", C.c_int),
                 ("mixed_precision", C.c_int), ("deterministic", C.c_int), ("pz", C.c_int),
-                ("levels_z", C.POINTER(C.c_int))]
+                ("levels_z", C.POINTER(C.c_int)), ("coarse_agg", C.c_int)]
 
 
 class SemReport(C.Structure):
@@ -52,7 +52,7 @@ class SemInfo(C.Structure):
                 ("schwarz_bytes", C.c_int64 * 16), ("schwarz_nk_sum", C.c_int64 * 16),
                 ("schwarz_packed", C.c_int64 * 16), ("coarse_n", C.c_int64), ("device_bytes", C.c_int64),
                 ("setup_ms", C.c_double), ("smoother_kernel", C.c_int * 16), ("smoother_mt", C.c_int * 16),
-                ("level_pz", C.c_int * 16)]
+                ("level_pz", C.c_int * 16), ("coarse_agg", C.c_int)]
 
 
 SMOOTHER_KERNELS = {0: "coarse", 1: "k_schwarz", 2: "k_fdm_warp<MT,1>", 3: "k_fdm_warp<MT,2>", 4: "k_fdm_cta<MT>",
@@ -297,7 +297,7 @@ class Solver:
         _check(_lib.sem_get_info(self._ctx, C.byref(inf)), "sem_get_info")
         self.info = dict(n_dof=inf.n_dof, n_free=inf.n_free, n_elem=inf.n_elem, n_levels=inf.n_levels,
                          level_p=list(inf.level_p[: inf.n_levels]),
-                         level_pz=list(inf.level_pz[: inf.n_levels]),
+                         level_pz=list(inf.level_pz[: inf.n_levels]), coarse_agg=inf.coarse_agg,
                          level_n_dof=list(inf.level_n_dof[: inf.n_levels]),
                          level_n_free=list(inf.level_n_free[: inf.n_levels]),
                          schwarz_bytes=list(inf.schwarz_bytes[: inf.n_levels]),

@@ -311,6 +311,7 @@ void setup_coarse(sem_ctx* c, const LevelTopo& topo, cusolverDnHandle_t sol, con
     }
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
     setup_coarse_lines(c, topo.conn, topo.dir, c->C.dinv, off);
+    setup_coarse_agg(c, d_D, (void*)sol);
     return;
   }
   c->C.nc = nc;
@@ -391,6 +392,7 @@ void check_opts(const sem_opts& o) {
   if (o.mixed_precision < 0 || o.mixed_precision > 1) throw SemError(SEM_EINVAL, "bad options: mixed_precision");
   if (o.deterministic < 0 || o.deterministic > 1) throw SemError(SEM_EINVAL, "bad options: deterministic");
   if (o.pz < 0 || o.pz > 8) throw SemError(SEM_EINVAL, "bad options: pz");
+  if (o.coarse_agg < -1 || o.coarse_agg > 8192) throw SemError(SEM_EINVAL, "bad options: coarse_agg (-1..8192)");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
       o.apply_kernel > 3 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
       o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
@@ -993,6 +995,7 @@ void sem_default_opts(sem_opts* o) {
   o->nccl_id = nullptr;
   o->pz = 0;
   o->levels_z = nullptr;
+  o->coarse_agg = -1;
 }
 
 int sem_reference_nodes(int p, double* rst) {
@@ -1047,6 +1050,7 @@ int sem_get_info(const sem_ctx* c, sem_info* info) {
   info->n_free = c->L[0].nfree;
   info->n_elem = c->E;
   info->n_levels = (int)c->L.size();
+  info->coarse_agg = c->C.nagg;
   for (size_t i = 0; i < c->L.size(); ++i) {
     info->level_p[i] = c->L[i].p;
     info->level_pz[i] = c->L[i].q;

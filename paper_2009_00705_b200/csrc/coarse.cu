@@ -10,12 +10,21 @@
 // exactly by the Thomas algorithm with factors precomputed at setup; on meshes whose
 // prisms do not stack consistently every line is a single node (point Jacobi).
 //
+// Two-level correction (reading O44): the line solves leave the smooth horizontal error, so
+// the preconditioner adds an exact solve on a coarse space of piecewise constants over
+// aggregates of whole lines (recursive coordinate bisection of the lines' (x, y)):
+//   z = T^-1 r + P_a A_a^-1 P_a^T r,   A_a = P_a^T A P_a (dense inverse, formed at setup).
+// Both terms are SPD, so CG stays CG.  Restriction P_a^T r is fused into the line kernel
+// (one atomic per line), A_a^-1 is one small dense GEMV, and the prolongation is folded into
+// the search-direction update p = (T^-1 r + P_a z_a) + beta p.
+//
 // The whole solve runs on the device: the stop test is a CUDA-graph WHILE node whose
 // condition a one-thread kernel sets after every iteration, so no host round trip
 // happens inside the solve and the V-cycle that contains it can itself be captured
 // and replayed from a CUDA graph (capi.cu vcycle_pcg).  Outside a capture the solve
 // is replayed from a cached graph of its own.
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -23,6 +32,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "partition.h"
 #include "setup_util.h"
 
 namespace sem {
@@ -191,21 +201,23 @@ __global__ void k_line_axpy_solve(int nlines, const int64_t* __restrict__ loff, 
                                   const double* __restrict__ ta, const double* __restrict__ tinv,
                                   const double* __restrict__ tc, double* __restrict__ x, double* __restrict__ r,
                                   const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ z,
-                                  double* cs) {
+                                  double* cs, const int32_t* __restrict__ aggl, double* __restrict__ rc) {
   const double alpha = cs[CS_ZR_OLD] / cs[CS_PQ];
   double s0 = 0.0, s1 = 0.0;
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlines; l += gridDim.x * blockDim.x) {
     const int64_t b = loff[l], e = loff[l + 1];
-    double d = 0.0;
+    double d = 0.0, rsum = 0.0;
     for (int64_t t = b; t < e; ++t) {
       const int32_t g = lnode[t];
       x[g] = fma(alpha, p[g], x[g]);
       const double rg = fma(-alpha, q[g], r[g]);
       r[g] = rg;
       s1 = fma(rg, rg, s1);
+      rsum += rg;
       d = (rg - ta[t] * d) * tinv[t];
       z[g] = d;
     }
+    if (aggl) atomicAdd(rc + aggl[l], rsum);   // P_a^T r
     double xx = 0.0;
     for (int64_t t = e - 1; t >= b; --t) {
       const int32_t g = lnode[t];
@@ -238,10 +250,17 @@ __global__ void k_line_axpy_solve(int nlines, const int64_t* __restrict__ loff, 
 // shifts z.r, counts the iteration, zeroes the reduction slots and sets the WHILE condition
 __global__ void k_coarse_update(int64_t n, double* __restrict__ p, const double* __restrict__ z,
                                 double* __restrict__ q, double* cs, unsigned int* done, double maxit,
-                                cudaGraphConditionalHandle h, int use_h) {
+                                cudaGraphConditionalHandle h, int use_h, const int32_t* __restrict__ aggn,
+                                const double* __restrict__ zc, double* __restrict__ rc, int nagg) {
   const double beta = cs[CS_ZR_NEW] / cs[CS_ZR_OLD];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    p[i] = fma(beta, p[i], z[i]);
+    double zi = z[i];
+    if (aggn) {   // z = T^-1 r + P_a z_a
+      const int32_t a = aggn[i];
+      if (a >= 0) zi += zc[a];
+      if (i < nagg) rc[i] = 0.0;   // the next iteration's restriction accumulates from 0
+    }
+    p[i] = fma(beta, p[i], zi);
     q[i] = 0.0;
   }
   __syncthreads();
@@ -263,6 +282,65 @@ __global__ void k_coarse_update(int64_t n, double* __restrict__ p, const double*
       if (use_h) cudaGraphSetConditional(h, go);
     }
   }
+}
+
+// ---- two-level correction kernels
+// rc[aggn[i]] += r[i] (free nodes)
+__global__ void k_agg_restrict(int64_t n, const int32_t* __restrict__ aggn, const double* __restrict__ r,
+                               double* __restrict__ rc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = aggn[i];
+    if (a >= 0) atomicAdd(rc + a, r[i]);
+  }
+}
+
+// zc = A_a^-1 rc (one warp per row of the symmetric inverse); zr += zc . rc
+__global__ void k_agg_solve(int na, const double* __restrict__ Ainv, const double* __restrict__ rc,
+                            double* __restrict__ zc, double* zr) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= na) return;
+  const double* a = Ainv + (int64_t)row * na;
+  double s = 0.0;
+  for (int j = lane; j < na; j += 32) s = fma(a[j], rc[j], s);
+  s = cw_sum(s);
+  if (lane == 0) {
+    zc[row] = s;
+    atomicAdd(zr, s * rc[row]);
+  }
+}
+
+// z[i] += zc[aggn[i]]
+__global__ void k_agg_prolong_add(int64_t n, const int32_t* __restrict__ aggn, const double* __restrict__ zc,
+                                  double* __restrict__ z) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = aggn[i];
+    if (a >= 0) z[i] += zc[a];
+  }
+}
+
+// A_a[aggn[i]][aggn[j]] += A_e[i][j] for the free nodes of P = 1 elements e0 .. e0+ne (setup)
+__global__ void k_agg_assemble(int ne, const int32_t* __restrict__ conn, const double* __restrict__ Ae,
+                               const int32_t* __restrict__ aggn, int na, double* __restrict__ Aa) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)ne * 36) return;
+  const int64_t e = idx / 36;
+  const int i = (int)(idx % 36) / 6, j = (int)(idx % 6);
+  const int32_t gi = conn[e * 6 + i], gj = conn[e * 6 + j];
+  if (gi < 0 || gj < 0) return;
+  atomicAdd(Aa + (int64_t)aggn[gi] * na + aggn[gj], Ae[idx]);
+}
+
+// z += P_a A_a^-1 P_a^T r and zr += (P_a^T r) . (A_a^-1 P_a^T r); leaves rc = 0
+static void agg_correct(sem_ctx* c, const double* r, double* z, double* zr) {
+  Coarse& C = c->C;
+  const int64_t n = c->L.back().n;
+  k_agg_restrict<<<cgrid(n, 256), 256, 0, c->stream>>>(n, C.aggn, r, C.rc);
+  k_agg_solve<<<(C.nagg + 7) / 8, 256, 0, c->stream>>>(C.nagg, C.Aagg_inv, C.rc, C.zc, zr);
+  k_agg_prolong_add<<<cgrid(n, 256), 256, 0, c->stream>>>(n, C.aggn, C.zc, z);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaMemsetAsync(C.rc, 0, sizeof(double) * C.nagg, c->stream));
+  c->launches += 3;
 }
 
 static void line_solve(sem_ctx* c, const double* r, double* z, double* out2) {
@@ -333,11 +411,83 @@ void setup_coarse_lines(sem_ctx* c, const std::vector<int32_t>& conn, const std:
   C.ta = upload(c, ta);
   C.tinv = upload(c, tinv);
   C.tc = upload(c, tc);
+  // aggregates of the two-level correction (reading O44): RCB of the lines' (x, y)
+  C.nagg = 0;
+  const int want = c->opts.coarse_agg < 0 ? (C.nlines >= 4096 ? std::min(1024, C.nlines / 32) : 0)
+                                          : std::min(c->opts.coarse_agg, C.nlines);
+  const std::vector<double>& xyz = c->L.back().xyz;
+  if (want > 0 && !c->opts.deterministic && (int64_t)xyz.size() == 3 * n) {
+    std::vector<double> lx(C.nlines), ly(C.nlines);
+    for (int l = 0; l < C.nlines; ++l) {
+      const int32_t g = lnode[loff[l]];
+      lx[l] = xyz[3 * (size_t)g];
+      ly[l] = xyz[3 * (size_t)g + 1];
+    }
+    std::vector<int> al = partition_columns(lx, ly, want);   // equal-(x, y) lines stay together
+    std::vector<int> used(want, -1);
+    int na = 0;
+    for (int& a : al) {   // compact (an RCB part can be empty when lines share (x, y))
+      if (used[a] < 0) used[a] = na++;
+      a = used[a];
+    }
+    std::vector<int32_t> aggl(al.begin(), al.end()), aggn(n, -1);
+    for (int l = 0; l < C.nlines; ++l)
+      for (int64_t t = loff[l]; t < loff[l + 1]; ++t) aggn[lnode[t]] = aggl[l];
+    C.nagg = na;
+    C.aggl = upload(c, aggl);
+    C.aggn = upload(c, aggn);
+    C.rc = dalloc<double>(c, na);
+    C.zc = dalloc<double>(c, na);
+    CUDA_CHECK(cudaMemset(C.rc, 0, na * sizeof(double)));
+  }
   C.cs = dalloc<double>(c, CS_N);
   CUDA_CHECK(cudaMemset(C.cs, 0, CS_N * sizeof(double)));
   C.done = dalloc<unsigned int>(c, 1);
   CUDA_CHECK(cudaMemset(C.done, 0, sizeof(unsigned int)));
   CUDA_CHECK(cudaMemset(C.z, 0, n * sizeof(double)));
+}
+
+int coarse_agg_count(const sem_ctx* c) { return c->C.nagg; }
+
+// A_a = P_a^T A P_a from the P = 1 element matrices and its dense inverse (cuSOLVER, setup only)
+void setup_coarse_agg(sem_ctx* c, const double* d_D, void* cusolver_handle) {
+  Coarse& C = c->C;
+  if (!C.nagg) return;
+  cusolverDnHandle_t sol = (cusolverDnHandle_t)cusolver_handle;
+  const int li = (int)c->L.size() - 1;
+  DeviceLevel& L = c->L[li];
+  const int na = C.nagg, E = c->E;
+  C.Aagg_inv = dalloc<double>(c, (size_t)na * na);
+  CUDA_CHECK(cudaMemsetAsync(C.Aagg_inv, 0, (size_t)na * na * 8, c->stream));
+  Scratch sc;
+  const int64_t chunk = std::min<int64_t>(E, 1 << 20);
+  double* Ae = sc.get<double>((size_t)chunk * 36);
+  for (int64_t e0 = 0; e0 < E; e0 += chunk) {
+    const int ne = (int)std::min<int64_t>(chunk, E - e0);
+    launch_elem_matrices(c, li, d_D, Ae, (int)e0, ne);
+    k_agg_assemble<<<(int)((ne * 36 + 255) / 256), 256, 0, c->stream>>>(ne, L.conn + (size_t)e0 * 6, Ae, C.aggn, na,
+                                                                          C.Aagg_inv);
+    CUDA_CHECK(cudaGetLastError());
+  }
+  int lwork = 0, lwork2 = 0;
+  if (cusolverDnDpotrf_bufferSize(sol, CUBLAS_FILL_MODE_LOWER, na, C.Aagg_inv, na, &lwork) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDpotri_bufferSize(sol, CUBLAS_FILL_MODE_LOWER, na, C.Aagg_inv, na, &lwork2) != CUSOLVER_STATUS_SUCCESS)
+    throw SemError(SEM_ECUDA, "cusolverDn buffer size (aggregate coarse space)");
+  double* work = sc.get<double>(std::max(lwork, lwork2));
+  int* dinfo = sc.get<int>(1);
+  int hinfo = 0;
+  if (cusolverDnDpotrf(sol, CUBLAS_FILL_MODE_LOWER, na, C.Aagg_inv, na, work, lwork, dinfo) != CUSOLVER_STATUS_SUCCESS)
+    throw SemError(SEM_ECUDA, "cusolverDnDpotrf (aggregate coarse space)");
+  CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (hinfo != 0) throw SemError(SEM_ESINGULAR, "aggregate coarse matrix is not SPD (info " + std::to_string(hinfo) + ")");
+  if (cusolverDnDpotri(sol, CUBLAS_FILL_MODE_LOWER, na, C.Aagg_inv, na, work, lwork2, dinfo) != CUSOLVER_STATUS_SUCCESS)
+    throw SemError(SEM_ECUDA, "cusolverDnDpotri (aggregate coarse space)");
+  CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (hinfo != 0) throw SemError(SEM_ESINGULAR, "aggregate coarse inverse failed (info " + std::to_string(hinfo) + ")");
+  launch_symmetrize(c, C.Aagg_inv, na);
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }
 
 void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double* Ae, double* off) {
@@ -358,6 +508,7 @@ static void coarse_prologue(sem_ctx* c, const double* b, double* x, cudaGraphCon
   launch_init_masked(c, li, nullptr, x, 1);
   launch_init_masked(c, li, b, C.r, 1);
   line_solve(c, C.r, C.z, cs + CS_ZR_NEW);  // [ZR_NEW] = z.r, [RR_DUP] = r.r
+  if (C.nagg) agg_correct(c, C.r, C.z, cs + CS_ZR_NEW);
   launch_xpby(c, L.n, C.p, C.z, nullptr, nullptr, 1);
   launch_init_masked(c, li, nullptr, C.q, 1);   // q = 0 (the fused body re-zeroes it every iteration)
   const double rt = c->opts.coarse_rtol;
@@ -379,10 +530,13 @@ static void coarse_body(sem_ctx* c, double* x, cudaGraphConditionalHandle h, int
     const int E = c->E;
     k_coarse_apply_pq<<<(E + 127) / 128, 128, 0, c->stream>>>(E, L.conn, L.Ae1, C.p, C.q, cs + CS_PQ);
     k_line_axpy_solve<<<cgrid(C.nlines, 128), 128, 0, c->stream>>>(C.nlines, C.loff, C.lnode, C.ta, C.tinv, C.tc,
-                                                                   x, C.r, C.p, C.q, C.z, cs);
-    k_coarse_update<<<cgrid(n, 256), 256, 0, c->stream>>>(n, C.p, C.z, C.q, cs, C.done, maxit, h, use_h);
+                                                                   x, C.r, C.p, C.q, C.z, cs, C.aggl, C.rc);
+    if (C.nagg)   // z_a = A_a^-1 P_a^T r (rc accumulated by the line kernel), z.r += z_a . rc
+      k_agg_solve<<<(C.nagg + 7) / 8, 256, 0, c->stream>>>(C.nagg, C.Aagg_inv, C.rc, C.zc, cs + CS_ZR_NEW);
+    k_coarse_update<<<cgrid(n, 256), 256, 0, c->stream>>>(n, C.p, C.z, C.q, cs, C.done, maxit, h, use_h, C.aggn,
+                                                          C.zc, C.rc, C.nagg);
     CUDA_CHECK(cudaGetLastError());
-    c->launches += 3;
+    c->launches += C.nagg ? 4 : 3;
     return;
   }
   // q = A p; p.q; x += alpha p, r -= alpha q (||r||^2); z = T^-1 r (z.r); p = z + beta p; stop test
@@ -391,6 +545,7 @@ static void coarse_body(sem_ctx* c, double* x, cudaGraphConditionalHandle h, int
   launch_dot2(c, n, C.p, C.q, nullptr, nullptr, nullptr, cs + CS_PQ, false);
   launch_axpy_pcg(c, n, x, C.r, C.p, C.q, cs + CS_ZR_OLD, cs + CS_PQ, cs + CS_RR, nullptr, false);
   line_solve(c, C.r, C.z, cs + CS_ZR_NEW);
+  if (C.nagg) agg_correct(c, C.r, C.z, cs + CS_ZR_NEW);
   launch_xpby(c, n, C.p, C.z, cs + CS_ZR_NEW, cs + CS_ZR_OLD, 0);
   k_coarse_next<<<1, 1, 0, c->stream>>>(cs, maxit, h, use_h);
   CUDA_CHECK(cudaGetLastError());

@@ -700,6 +700,7 @@ void dist_info(const sem_ctx* c, sem_info* info) {
     }
   }
   info->coarse_n = D.coarse->C.nc;
+  info->coarse_agg = D.coarse->C.nagg;
   info->device_bytes = c->device_bytes + D.coarse->device_bytes;
   for (auto* pc : D.parts) info->device_bytes += pc->device_bytes;
 }

@@ -174,6 +174,13 @@ struct Coarse {
   double *ta = nullptr, *tinv = nullptr, *tc = nullptr;   // Thomas factors per line position
   double* cs = nullptr;         // device scalars of the solve (coarse.cu CS_*)
   unsigned int* done = nullptr; // block-completion counter of k_coarse_update
+  // two-level correction of the line preconditioner (coarse.cu): z = T^-1 r + P_a A_a^-1 P_a^T r with
+  // P_a piecewise constant on nagg aggregates of whole lines (RCB of the lines' (x, y)), A_a = P_a^T A P_a
+  int nagg = 0;
+  int32_t* aggn = nullptr;      // [n] aggregate of every free node (-1: Dirichlet)
+  int32_t* aggl = nullptr;      // [nlines] aggregate of every line
+  double* Aagg_inv = nullptr;   // [nagg][nagg] symmetric inverse of A_a
+  double *rc = nullptr, *zc = nullptr;   // [nagg] restricted residual / aggregate correction
   cudaGraphExec_t exec = nullptr;                 // standalone graph of the solve (coarsest L.f -> L.u)
   cudaStream_t cap_stream = nullptr, body_stream = nullptr;
   int64_t exec_launches = 0, body_launches = 0;
@@ -254,6 +261,8 @@ void launch_axpy_pcg(sem_ctx* c, int64_t n, double* u, double* r, const double* 
 void coarse_pcg(sem_ctx* c, const double* b, double* x);
 void setup_coarse_lines(sem_ctx* c, const std::vector<int32_t>& conn, const std::vector<uint8_t>& dir,
                         const double* d_diag, const double* d_off);
+int coarse_agg_count(const sem_ctx* c);   // aggregates the line preconditioner's correction will use
+void setup_coarse_agg(sem_ctx* c, const double* d_D, void* cusolver_handle);
 void launch_offdiag_accum(sem_ctx* c, const int32_t* conn, int ne, const double* Ae, double* off);
 int64_t coarse_iters(sem_ctx* c, bool reset);
 void coarse_reset_iters(sem_ctx* c);

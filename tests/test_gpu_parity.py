@@ -294,12 +294,15 @@ def test_not_converged_flag(c1):
     assert not rep["converged"] and rep["iters"] == 1
 
 
-def test_iterative_coarse_solver(c2):
-    """Reading O9 for large P=1 problems: Jacobi-PCG coarse solve (coarse_solver=1)
-    agrees with the exact coarse solve to its tolerance, and the flexible outer
-    PCG still reaches the sparse-direct solution to 1e-10."""
+@pytest.mark.parametrize("agg", [0, 4, 16])
+def test_iterative_coarse_solver(c2, agg):
+    """Reading O9 for large P=1 problems: line-Jacobi PCG coarse solve (coarse_solver=1),
+    with and without the two-level aggregate correction (reading O44, coarse_agg
+    aggregates), agrees with the exact coarse solve to its tolerance, and the flexible
+    outer PCG still reaches the sparse-direct solution to 1e-10."""
     m = c2.m
-    s = make_solver(m, coarse_solver=1, coarse_rtol=1e-12)
+    s = make_solver(m, coarse_solver=1, coarse_rtol=1e-12, coarse_agg=agg)
+    assert s.info["coarse_agg"] == agg
     last = c2.mg.levels[-1]
     li = c2.nl - 1
     r = random_vector(last.A.shape[0], seed=12)
@@ -310,6 +313,7 @@ def test_iterative_coarse_solver(c2):
     phi, rep = s.solve(c2.to_lib(0, phiD), tol=1e-13)
     assert rep["converged"] and rep["coarse_iters"] > 0
     assert rel(c2.to_orc(0, phi), sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+    s.close()
 
 
 def test_mixed_precision_storage(c2):
