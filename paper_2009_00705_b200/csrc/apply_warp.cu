@@ -126,7 +126,9 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
                                                                  const double* __restrict__ G,
                                                                  const double* __restrict__ mats,
                                                                  const double* __restrict__ u, double* __restrict__ y,
-                                                                 int flags) {
+                                                                 int flags, const int32_t* __restrict__ elist) {
+  // E = element slots; slot s is element elist[s] (a subset, e.g. the interface elements of a
+  // partition, dist.cu) or s itself when elist is null
   using D = AW<P>;
   extern __shared__ __align__(128) double sm[];
   double* Bm = sm;                          // [3][ROWSA][LDM]
@@ -171,9 +173,11 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
   double* ring = Gs + warp * D::R * D::TS;
   // copy t of this warp's stream: element e0 + (t / TPE) stride, a-tile ma = t % TPE (or the whole
   // element), slot t % R
+  auto eid = [&](int sl) { return elist ? __ldg(elist + sl) : sl; };
   auto issue_tile = [&](int t) {
-    const int el = e0 + (t / D::TPE) * stride, ma = t % D::TPE;
-    if (el >= E || lane != 0) return;
+    const int sl = e0 + (t / D::TPE) * stride, ma = t % D::TPE;
+    if (sl >= E || lane != 0) return;
+    const int el = eid(sl);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
     const uint32_t bytes =
         D::WHOLE ? (uint32_t)D::GSZ * 8u : (uint32_t)(6 * D::QV * (ma < D::MTA - 1 ? 8 : D::NALAST)) * 8u;
@@ -209,13 +213,13 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
   double ua[D::MTM][D::KL];
   if (e < E) {
     for (int t = 0; t < D::R; ++t) issue_tile(t);
-    load_conn_a(e, cA);
+    load_conn_a(eid(e), cA);
     gather_u(cA, ua);
   }
   int tk = 0;  // first copy index of the current element
   while (e < E) {
     const int en = e + stride;
-    const int32_t* ce = conn + (size_t)e * D::N;
+    const int32_t* ce = conn + (size_t)eid(e) * D::N;
     // connectivity of this element's output positions (m = 8 mm + r4, l = 8 nl + 2 c4 + i), used at the end
     int cY[D::MTM][D::NL][2];
 #pragma unroll
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(32 * AW<P>::W, 1) k_apply_warp(int E, const in
           const int m = mm * 8 + r4, l = nl * 8 + 2 * c4 + i;
           cY[mm][nl][i] = (m < D::NT && l < D::N1) ? __ldg(ce + m + D::NT * l) : INT_MIN;
         }
-    if (en < E) load_conn_a(en, cA);   // next element's gather positions (in flight during stage A)
+    if (en < E) load_conn_a(eid(en), cA);   // next element's gather positions (in flight during stage A)
     // ---- stage A: Ut, Udt [m][q]
     double Ut[D::MTM][D::NQ][2], Udt[D::MTM][D::NQ][2];
 #pragma unroll
@@ -403,7 +407,8 @@ void build_g_tiles(sem_ctx* c, int level) {
 }
 
 template <int P>
-static void apply_warp_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags) {
+static void apply_warp_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags,
+                         const int32_t* elist, int ne) {
   using D = AW<P>;
   static int grid_maxes[kMaxDev] = {0};
   const int dev = cur_device();
@@ -415,23 +420,24 @@ static void apply_warp_P(sem_ctx* c, const DeviceLevel& L, const double* u, doub
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_warp<P>, 32 * D::W, D::SMEM));
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
-  if (c->E_own == 0) return;
-  const int need = (c->E_own + D::W - 1) / D::W;
+  const int E = elist ? ne : c->E_own;
+  if (E == 0) return;
+  const int need = (E + D::W - 1) / D::W;
   const int grid = need < grid_max ? need : grid_max;
-  k_apply_warp<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(c->E_own, L.conn, L.Gw, L.wmats, u, y, flags);
+  k_apply_warp<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(E, L.conn, L.Gw, L.wmats, u, y, flags, elist);
   CUDA_CHECK(cudaGetLastError());
 }
 
-bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags) {
+bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne) {
   const DeviceLevel& L = c->L[level];
   if (!L.wmats || !L.Gw) return false;
   switch (L.p) {
-    case 1: apply_warp_P<1>(c, L, u, y, flags); break;
-    case 2: apply_warp_P<2>(c, L, u, y, flags); break;
-    case 3: apply_warp_P<3>(c, L, u, y, flags); break;
-    case 4: apply_warp_P<4>(c, L, u, y, flags); break;
-    case 5: apply_warp_P<5>(c, L, u, y, flags); break;
-    case 6: apply_warp_P<6>(c, L, u, y, flags); break;
+    case 1: apply_warp_P<1>(c, L, u, y, flags, elist, ne); break;
+    case 2: apply_warp_P<2>(c, L, u, y, flags, elist, ne); break;
+    case 3: apply_warp_P<3>(c, L, u, y, flags, elist, ne); break;
+    case 4: apply_warp_P<4>(c, L, u, y, flags, elist, ne); break;
+    case 5: apply_warp_P<5>(c, L, u, y, flags, elist, ne); break;
+    case 6: apply_warp_P<6>(c, L, u, y, flags, elist, ne); break;
     default: return false;
   }
   c->launches++;

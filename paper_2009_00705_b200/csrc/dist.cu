@@ -18,6 +18,12 @@
 //   emulated  all R ranks in one process on one device, exchanges as device
 //             copies between the ranks' buffers -- used to test the partitioned
 //             algorithm against the single-domain one on a single GPU.
+//
+// Operator applies overlap their exchange with compute (apply_exchange): the owned
+// elements touching an exchanged node (interface) are applied first, their partial
+// sums packed and sent on a communication stream, and the interior elements -- which
+// touch no exchanged node -- are applied on the compute stream while the transfer is
+// in flight; the received sums are added after both.  SEM_DIST_OVERLAP=0 turns it off.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -25,6 +31,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "setup_util.h"
@@ -122,10 +129,19 @@ struct Dist {
   double* gbuf3 = nullptr;       // [gn[0]]
   double *cx = nullptr, *cz = nullptr;  // global coarse rhs / solution [gn.back()]
   double* hsum = nullptr;        // pinned host [32] (emulated all-reduce)
+  // overlap of operator applies with their exchange (apply_exchange)
+  bool overlap = true;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_xfer = nullptr;
 };
 
-// one exchange: complete the partial sums of v (one pointer per part) on level li
-static void exchange(Dist& D, int li, const std::vector<double*>& v) {
+template <class F>
+static void each(Dist& D, F f) {
+  for (size_t r = 0; r < D.parts.size(); ++r) f(D.parts[r], (int)r);
+}
+
+// exchange = pack (compute stream) -> transfer (stream st) -> unpack-add (compute stream)
+static void pack_all(Dist& D, int li, const std::vector<double*>& v) {
   const int R = (int)D.parts.size();
   for (int r = 0; r < R; ++r) {
     sem_ctx* c = D.parts[r];
@@ -133,6 +149,20 @@ static void exchange(Dist& D, int li, const std::vector<double*>& v) {
     const int64_t n = L.xoff.back();
     if (n) k_pack<<<gsz(n), 256, 0, c->stream>>>(n, L.xidx, v[r], L.sendbuf), c->launches++;
   }
+}
+
+static void unpack_all(Dist& D, int li, const std::vector<double*>& v) {
+  const int R = (int)D.parts.size();
+  for (int r = 0; r < R; ++r) {
+    sem_ctx* c = D.parts[r];
+    DeviceLevel& L = c->L[li];
+    const int64_t n = L.xoff.back();
+    if (n) k_unpack_add<<<gsz(n), 256, 0, c->stream>>>(n, L.xidx, L.recvbuf, v[r]), c->launches++;
+  }
+}
+
+static void transfer(Dist& D, int li, cudaStream_t st) {
+  const int R = (int)D.parts.size();
   if (D.emulated) {
     for (int r = 0; r < R; ++r) {
       DeviceLevel& L = D.parts[r]->L[li];
@@ -145,7 +175,7 @@ static void exchange(Dist& D, int li, const std::vector<double*>& v) {
         if (jq == Q.nbr.size() || Q.xoff[jq + 1] - Q.xoff[jq] != cnt)
           throw SemError(SEM_ENCCL, "inconsistent exchange lists");
         CUDA_CHECK(cudaMemcpyAsync(L.recvbuf + L.xoff[j], Q.sendbuf + Q.xoff[jq], cnt * 8, cudaMemcpyDeviceToDevice,
-                                   D.parts[r]->stream));
+                                   st));
       }
     }
   } else {
@@ -154,17 +184,52 @@ static void exchange(Dist& D, int li, const std::vector<double*>& v) {
     NCCL_CHECK(nccl().GroupStart());
     for (size_t j = 0; j < L.nbr.size(); ++j) {
       const size_t cnt = (size_t)(L.xoff[j + 1] - L.xoff[j]);
-      NCCL_CHECK(nccl().Send(L.sendbuf + L.xoff[j], cnt, ncclFloat64, L.nbr[j], D.comm, c->stream));
-      NCCL_CHECK(nccl().Recv(L.recvbuf + L.xoff[j], cnt, ncclFloat64, L.nbr[j], D.comm, c->stream));
+      NCCL_CHECK(nccl().Send(L.sendbuf + L.xoff[j], cnt, ncclFloat64, L.nbr[j], D.comm, st));
+      NCCL_CHECK(nccl().Recv(L.recvbuf + L.xoff[j], cnt, ncclFloat64, L.nbr[j], D.comm, st));
     }
     NCCL_CHECK(nccl().GroupEnd());
   }
-  for (int r = 0; r < R; ++r) {
-    sem_ctx* c = D.parts[r];
-    DeviceLevel& L = c->L[li];
-    const int64_t n = L.xoff.back();
-    if (n) k_unpack_add<<<gsz(n), 256, 0, c->stream>>>(n, L.xidx, L.recvbuf, v[r]), c->launches++;
+}
+
+// one exchange: complete the partial sums of v (one pointer per part) on level li
+static void exchange(Dist& D, int li, const std::vector<double*>& v) {
+  pack_all(D, li, v);
+  transfer(D, li, D.parts[0]->stream);
+  unpack_all(D, li, v);
+}
+
+// y (+)= A u on level li (each part's owned elements), then the exchange that completes y.
+// Overlapped when every part can apply element subsets (k_apply_warp, p <= 6): interface
+// elements -> pack -> [transfer on the comm stream || interior elements] -> unpack-add.
+// Correct because interior elements write no exchanged node, so the packed partial sums
+// are final once the interface elements are done.
+static void apply_exchange(Dist& D, int li, const std::vector<double*>& u, const std::vector<double*>& y, int flags) {
+  bool ov = D.overlap;
+  for (auto* c : D.parts) ov = ov && c->L[li].e_if && c->L[li].wmats && c->L[li].Gw && !c->det.on &&
+                               (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3);
+  if (!ov) {
+    each(D, [&](sem_ctx* c, int i) { launch_apply(c, li, u[i], y[i], flags); });
+    exchange(D, li, y);
+    return;
   }
+  sem_ctx* c0 = D.parts[0];
+  each(D, [&](sem_ctx* c, int i) {
+    DeviceLevel& L = c->L[li];
+    if (L.n_if && !launch_apply_warp(c, li, u[i], y[i], flags, L.e_if, L.n_if))
+      throw SemError(SEM_ECUDA, "interface apply");
+  });
+  pack_all(D, li, y);
+  CUDA_CHECK(cudaEventRecord(D.ev_pack, c0->stream));
+  CUDA_CHECK(cudaStreamWaitEvent(D.comm_stream, D.ev_pack, 0));
+  transfer(D, li, D.comm_stream);
+  CUDA_CHECK(cudaEventRecord(D.ev_xfer, D.comm_stream));
+  each(D, [&](sem_ctx* c, int i) {
+    DeviceLevel& L = c->L[li];
+    if (L.n_in && !launch_apply_warp(c, li, u[i], y[i], flags, L.e_in, L.n_in))
+      throw SemError(SEM_ECUDA, "interior apply");
+  });
+  CUDA_CHECK(cudaStreamWaitEvent(c0->stream, D.ev_xfer, 0));
+  unpack_all(D, li, y);
 }
 
 // sum slots [s, s+k) of every part's scalar array over all ranks (in place)
@@ -200,10 +265,6 @@ static void allreduce_vec(Dist& D, double* g, int64_t n) {
 }
 
 // ------------------------------------------------------------------ steps
-template <class F>
-static void each(Dist& D, F f) {
-  for (size_t r = 0; r < D.parts.size(); ++r) f(D.parts[r], (int)r);
-}
 
 using Vecs = std::vector<double*>;
 
@@ -215,11 +276,8 @@ static Vecs lvec(Dist& D, int li, double* DeviceLevel::*m) {
 
 // r = f - A u on level li (complete on every rank's nodes)
 static void residual(Dist& D, int li, const Vecs& f, const Vecs& u, const Vecs& r) {
-  each(D, [&](sem_ctx* c, int i) {
-    launch_init_masked(c, li, f[i], r[i], 2);
-    launch_apply(c, li, u[i], r[i], AP_NEGATE);
-  });
-  exchange(D, li, r);
+  each(D, [&](sem_ctx* c, int i) { launch_init_masked(c, li, f[i], r[i], 2); });
+  apply_exchange(D, li, u, r, AP_NEGATE);
 }
 
 // u += S^-1 r (transpose = 0) or u += S^-T r
@@ -326,12 +384,18 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
   each(D, [&](sem_ctx* c, int i) {
     launch_init_masked(c, 0, phiD[i], q[i], 0);
     launch_init_masked(c, 0, rhs.empty() ? nullptr : rhs[i], r[i], 2);
-    launch_apply(c, 0, q[i], r[i], AP_GATHER_ALL | AP_NEGATE);
-    CUDA_CHECK(cudaMemsetAsync(u[i], 0, sizeof(double) * c->L[0].n, c->stream));
-    if (o.outer != 0)  // PDC / MG: keep this rank's partial b_F (summed by every later exchange)
-      CUDA_CHECK(cudaMemcpyAsync(ro[i], r[i], sizeof(double) * c->L[0].n, cudaMemcpyDeviceToDevice, c->stream));
   });
-  exchange(D, 0, r);
+  // PDC / MG keep this rank's partial b_F (summed by every later exchange)
+  if (o.outer != 0) {
+    each(D, [&](sem_ctx* c, int i) { launch_apply(c, 0, q[i], r[i], AP_GATHER_ALL | AP_NEGATE); });
+    each(D, [&](sem_ctx* c, int i) {
+      CUDA_CHECK(cudaMemcpyAsync(ro[i], r[i], sizeof(double) * c->L[0].n, cudaMemcpyDeviceToDevice, c->stream));
+    });
+    exchange(D, 0, r);
+  } else {
+    apply_exchange(D, 0, q, r, AP_GATHER_ALL | AP_NEGATE);
+  }
+  each(D, [&](sem_ctx* c, int i) { CUDA_CHECK(cudaMemsetAsync(u[i], 0, sizeof(double) * c->L[0].n, c->stream)); });
   double h[4];
   dot(D, r, r, nullptr, nullptr, 4);
   read_scal(D, 4, 1, h);
@@ -350,11 +414,8 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
     int dcur = 8, dnew = 10;
     dot(D, p, r, nullptr, nullptr, dcur);
     while (R.iters < o.imax) {
-      each(D, [&](sem_ctx* c, int i) {
-        CUDA_CHECK(cudaMemsetAsync(q[i], 0, sizeof(double) * c->L[0].n, c->stream));
-        launch_apply(c, 0, p[i], q[i], 0);
-      });
-      exchange(D, 0, q);
+      each(D, [&](sem_ctx* c, int i) { CUDA_CHECK(cudaMemsetAsync(q[i], 0, sizeof(double) * c->L[0].n, c->stream)); });
+      apply_exchange(D, 0, p, q, 0);
       dot(D, p, q, nullptr, nullptr, 1);
       each(D, [&](sem_ctx* c, int i) {
         if (flex) CUDA_CHECK(cudaMemcpyAsync(ro[i], r[i], sizeof(double) * c->L[0].n, cudaMemcpyDeviceToDevice, c->stream));
@@ -392,9 +453,8 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
       each(D, [&](sem_ctx* c, int i) {
         launch_axpy(c, c->L[0].n, 1.0, z[i], u[i]);
         CUDA_CHECK(cudaMemcpyAsync(r[i], ro[i], sizeof(double) * c->L[0].n, cudaMemcpyDeviceToDevice, c->stream));
-        launch_apply(c, 0, u[i], r[i], AP_NEGATE);
       });
-      exchange(D, 0, r);
+      apply_exchange(D, 0, u, r, AP_NEGATE);
       R.iters++;
       dot(D, r, r, nullptr, nullptr, 3);
       read_scal(D, 3, 1, h);
@@ -437,6 +497,20 @@ static void setup_exchange(sem_ctx* c, const LocalPart& P) {
     L.xidx = upload(c, all);
     L.sendbuf = dalloc<double>(c, all.size());
     L.recvbuf = dalloc<double>(c, all.size());
+    // interface / interior owned elements (apply_exchange)
+    std::vector<uint8_t> shared(L.n, 0);
+    for (int32_t i : all) shared[i] = 1;
+    std::vector<int32_t> eif, ein;
+    const int N = L.N;
+    for (int e = 0; e < P.E_own; ++e) {
+      bool s = false;
+      for (int k = 0; k < N && !s; ++k) s = shared[LL.conn[(size_t)e * N + k]] != 0;
+      (s ? eif : ein).push_back(e);
+    }
+    L.n_if = (int)eif.size();
+    L.n_in = (int)ein.size();
+    L.e_if = upload(c, eif);
+    L.e_in = upload(c, ein);
   }
 }
 
@@ -589,6 +663,13 @@ void setup_distributed(sem_ctx* c, GlobalModel& gm) {
   D->cx = dalloc<double>(c, D->gn.back());
   D->cz = dalloc<double>(c, D->gn.back());
   CUDA_CHECK(cudaMallocHost(&D->hsum, 32 * sizeof(double)));
+  {
+    const char* ov = getenv("SEM_DIST_OVERLAP");
+    D->overlap = !(ov && atoi(ov) == 0);
+    CUDA_CHECK(cudaStreamCreateWithFlags(&D->comm_stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&D->ev_xfer, cudaEventDisableTiming));
+  }
   if (!D->emulated) {
     ncclUniqueId id;
     memcpy(&id, o.nccl_id, sizeof(id));
@@ -730,6 +811,9 @@ void dist_destroy(sem_ctx* c) {
   if (D->coarse) sem_destroy(D->coarse);
   if (D->comm) nccl().CommDestroy(D->comm);
   if (D->hsum) cudaFreeHost(D->hsum);
+  if (D->ev_pack) cudaEventDestroy(D->ev_pack);
+  if (D->ev_xfer) cudaEventDestroy(D->ev_xfer);
+  if (D->comm_stream) cudaStreamDestroy(D->comm_stream);
   delete D;
   c->dist = nullptr;
 }

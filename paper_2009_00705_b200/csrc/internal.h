@@ -135,6 +135,10 @@ struct DeviceLevel {
   int32_t* xidx = nullptr;           // concatenated local ids
   int32_t* xnbr = nullptr;           // neighbour slot of every entry (unused by NCCL path)
   double *sendbuf = nullptr, *recvbuf = nullptr;
+  // owned elements touching an exchanged node (interface, applied first) and the rest (interior,
+  // applied while the exchange of the interface sums is in flight; dist.cu)
+  int32_t *e_if = nullptr, *e_in = nullptr;
+  int n_if = 0, n_in = 0;
 };
 
 // deterministic mode (opts.deterministic): colour-ordered gather-scatter and
@@ -240,7 +244,8 @@ void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags);
 void launch_apply_dmma(sem_ctx* c, int level, const double* u, double* y, int flags);
 std::vector<double> dmma_fragments(const LevelRef& R);
 std::vector<double> warp_apply_mats(const LevelRef& R);
-bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags);
+bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int flags,
+                       const int32_t* elist = nullptr, int ne = 0);   // elist: apply only these elements
 std::vector<double> quad_apply_mats(const LevelRef& R);
 bool launch_apply_quad(sem_ctx* c, int level, const double* u, double* y, int flags);
 void build_g_tiles(sem_ctx* c, int level);

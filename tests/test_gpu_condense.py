@@ -52,7 +52,7 @@ def _to_orc(t, perm, n):
     (6, None, dict(outer=1)),
 ])
 def test_condensed_solve_parity(p, q, kw):
-    m, s, lev, perm = _case(p, q, **kw)
+    m, s, lev, perm = _case(p, q, nx=8 if p >= 6 else 16, **kw)
     ni, nb, by = s.condensed_info()
     qq = p if q is None else q
     assert ni == (p - 1) * (p - 2) // 2 * (qq - 1) and ni + nb == lev.conn.shape[1]

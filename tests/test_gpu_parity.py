@@ -294,7 +294,7 @@ def test_not_converged_flag(c1):
     assert not rep["converged"] and rep["iters"] == 1
 
 
-@pytest.mark.parametrize("agg", [0, 4, 16])
+@pytest.mark.parametrize("agg", [0, 16])
 def test_iterative_coarse_solver(c2, agg):
     """Reading O9 for large P=1 problems: line-Jacobi PCG coarse solve (coarse_solver=1),
     with and without the two-level aggregate correction (reading O44, coarse_agg
