@@ -280,14 +280,34 @@ static void residual(Dist& D, int li, const Vecs& f, const Vecs& u, const Vecs& 
   apply_exchange(D, li, u, r, AP_NEGATE);
 }
 
-// u += S^-1 r (transpose = 0) or u += S^-T r
+// u += S^-1 r (transpose = 0) or u += S^-T r.  Dense levels overlap the exchange like
+// apply_exchange: interface subdomains, pack, [transfer || interior subdomains], unpack-add.
 static void schwarz_update(Dist& D, int li, const Vecs& r, const Vecs& u, int transpose) {
   Vecs d = lvec(D, li, &DeviceLevel::d);
-  each(D, [&](sem_ctx* c, int i) {
-    CUDA_CHECK(cudaMemsetAsync(d[i], 0, sizeof(double) * c->L[li].n, c->stream));
-    launch_schwarz(c, li, r[i], d[i], transpose);
-  });
-  exchange(D, li, d);
+  bool ov = D.overlap;
+  for (auto* c : D.parts) ov = ov && c->L[li].s_if && !c->L[li].fdm && !c->det.on;
+  each(D, [&](sem_ctx* c, int i) { CUDA_CHECK(cudaMemsetAsync(d[i], 0, sizeof(double) * c->L[li].n, c->stream)); });
+  if (!ov) {
+    each(D, [&](sem_ctx* c, int i) { launch_schwarz(c, li, r[i], d[i], transpose); });
+    exchange(D, li, d);
+  } else {
+    sem_ctx* c0 = D.parts[0];
+    each(D, [&](sem_ctx* c, int i) {
+      const DeviceLevel& L = c->L[li];
+      if (!launch_schwarz_list(c, li, r[i], d[i], transpose, L.s_if, L.ns_if)) throw SemError(SEM_ECUDA, "schwarz");
+    });
+    pack_all(D, li, d);
+    CUDA_CHECK(cudaEventRecord(D.ev_pack, c0->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(D.comm_stream, D.ev_pack, 0));
+    transfer(D, li, D.comm_stream);
+    CUDA_CHECK(cudaEventRecord(D.ev_xfer, D.comm_stream));
+    each(D, [&](sem_ctx* c, int i) {
+      const DeviceLevel& L = c->L[li];
+      if (!launch_schwarz_list(c, li, r[i], d[i], transpose, L.s_in, L.ns_in)) throw SemError(SEM_ECUDA, "schwarz");
+    });
+    CUDA_CHECK(cudaStreamWaitEvent(c0->stream, D.ev_xfer, 0));
+    unpack_all(D, li, d);
+  }
   each(D, [&](sem_ctx* c, int i) { launch_axpy(c, c->L[li].n, 1.0, d[i], u[i]); });
 }
 
@@ -511,6 +531,18 @@ static void setup_exchange(sem_ctx* c, const LocalPart& P) {
     L.n_in = (int)ein.size();
     L.e_if = upload(c, eif);
     L.e_in = upload(c, ein);
+    if (li + 1 < c->L.size() && !L.fdm && L.nsub == (int)LL.S.off.size() - 1) {  // dense: subdomain k = owned element k
+      std::vector<int32_t> sif, sin;
+      for (int k = 0; k < L.nsub; ++k) {
+        bool s = false;
+        for (int64_t t = LL.S.off[k]; t < LL.S.off[k + 1] && !s; ++t) s = shared[LL.S.idx[t]] != 0;
+        (s ? sif : sin).push_back(k);
+      }
+      L.ns_if = (int)sif.size();
+      L.ns_in = (int)sin.size();
+      L.s_if = upload(c, sif);
+      L.s_in = upload(c, sin);
+    }
   }
 }
 

@@ -139,6 +139,8 @@ struct DeviceLevel {
   // applied while the exchange of the interface sums is in flight; dist.cu)
   int32_t *e_if = nullptr, *e_in = nullptr;
   int n_if = 0, n_in = 0;
+  int32_t *s_if = nullptr, *s_in = nullptr;   // the same split of the owned (dense) Schwarz subdomains
+  int ns_if = 0, ns_in = 0;
 };
 
 // deterministic mode (opts.deterministic): colour-ordered gather-scatter and
@@ -252,6 +254,8 @@ void build_g_tiles(sem_ctx* c, int level);
 void build_p1_matrices(sem_ctx* c, int level, const double* d_D);
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);
 void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose);
+bool launch_schwarz_list(sem_ctx* c, int level, const double* r, double* u, int transpose, const int32_t* slist,
+                         int nb);   // dense levels: sweep only subdomains slist[0..nb)
 void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose);
 int fdm_kernel_choice(const DeviceLevel& L);
 void launch_restrict(sem_ctx* c, int level, const double* rf, double* rc);

@@ -603,6 +603,30 @@ void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int trans
   c->launches++;
 }
 
+// dense Schwarz sweep over a subset of the subdomains (dist.cu: interface subdomains first)
+bool launch_schwarz_list(sem_ctx* c, int level, const double* r, double* u, int transpose, const int32_t* slist,
+                         int nb) {
+  const DeviceLevel& L = c->L[level];
+  if (L.fdm || c->det.on || L.nsub == 0) return false;
+  if (nb == 0) return true;
+  const int npad = 16 * L.max_tiles_1d;
+  const int smem = 9 * npad * (int)sizeof(double);
+  static int attr_set[kMaxDev] = {0}, attr_set32[kMaxDev] = {0};
+  if (smem > 48 * 1024) {
+    smem_opt_in(k_schwarz<float>, smem, attr_set32);
+    smem_opt_in(k_schwarz<double>, smem, attr_set);
+  }
+  if (L.tiles32)
+    k_schwarz<float><<<nb, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles32, L.W, r, u, transpose,
+                                                   npad, slist);
+  else
+    k_schwarz<double><<<nb, 256, smem, c->stream>>>(L.sidx, L.sidx_off, L.tile_off, L.tiles, L.W, r, u, transpose,
+                                                    npad, slist);
+  CUDA_CHECK(cudaGetLastError());
+  c->launches++;
+  return true;
+}
+
 // ============================================================== transfers
 // Prolongation u_f += P u_c with P evaluated element by element, each fine node
 // written only by its owner element (first element containing it): P[j][i] =
