@@ -536,7 +536,8 @@ def main():
             roof["traffic"] = tr["dram_bytes_per_launch"]
             roof["traffic_note"] = tr["source"]
     ach_a = b_a / (us_a * 1e-6) / 1e9
-    apply = {"kernel": "k_apply_warp<%d> (FP64 tensor cores, warp per element)" % m.p, "us": us_a,
+    apply = {"kernel": ("k_apply_qs<%d> (FP64 tensor cores, four elements per group of warps)" if m.p <= 5 else
+                        "k_apply_warp<%d> (FP64 tensor cores, warp per element)") % m.p, "us": us_a,
              "alg_bytes_per_launch": b_a,
              "achieved_GBs": ach_a, "frac": ach_a / peak,
              "MDOF_s": info["n_dof"] / us_a if world == 1 else None}

@@ -95,7 +95,9 @@ typedef struct {
                                  TMA-staged geometric factors (p <= 6; p = 7, 8 use variant 2);
                                  1 CUDA-core FMA sum factorisation (reference variant);
                                  2 DMMA with CTA-wide element batches; 3 DMMA with four elements per
-                                 warp (k_apply_quad, 3 <= p <= 5; the default (0) uses it at p = 3)    */
+                                 warp (k_apply_quad, 3 <= p <= 5); 4 DMMA with four elements per
+                                 group of warps, one warp per vertical row tile (k_apply_qs,
+                                 3 <= p <= 6; the default (0) uses it at 3 <= p <= 5)              */
   int coarse_solver;          /* P=1 solve (reading O9): 0 auto (dense inverse if <= 46,000 free
                                  nodes, else iterative), 1 iterative (Jacobi-PCG, the outer PCG becomes
                                  flexible), 2 dense                                                  */

@@ -6,7 +6,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsem_pmg.so")
+# SEM_PMG_LIB: an alternative build of the same library (A/B timing tools only)
+LIB_PATH = os.environ.get("SEM_PMG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsem_pmg.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build the CUDA library first "
                       "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")

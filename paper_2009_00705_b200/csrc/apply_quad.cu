@@ -72,7 +72,6 @@ struct AQ {
   static constexpr int SU = 4 * UST, SC = 4 * N;
   static constexpr int SMEM = (BMT + BT + W * R * TS + W * SU) * 8 + W * SC * 4 + W * R * 8;
   static_assert(TSE % 16 == 8 && LDA % 16 == 8, "bank layout");
-  static_assert(SMEM <= 227 * 1024, "apply_quad shared memory");
 };
 
 // host: Bm [3][ROWSA][LDM] (Br, Bs, B0 at [a][m]), BmT [3][8 NM][LDA] (the same at [m][a]),
@@ -98,6 +97,7 @@ std::vector<double> quad_apply_mats(const LevelRef& R) {
     case 3: return run(std::integral_constant<int, 3>{});
     case 4: return run(std::integral_constant<int, 4>{});
     case 5: return run(std::integral_constant<int, 5>{});
+    case 6: return run(std::integral_constant<int, 6>{});
   }
   return {};
 }
@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(32 * AQ<P>::W, 1)
     k_apply_quad(int E, const int32_t* __restrict__ conn, const double* __restrict__ Gw,
                  const double* __restrict__ mats, const double* __restrict__ u, double* __restrict__ y, int flags) {
   using D = AQ<P>;
+  static_assert(D::SMEM <= 227 * 1024, "apply_quad shared memory");
   extern __shared__ __align__(128) double sm[];
   double* BmT = sm;                       // [3][8 NM][LDA]  B_c[a][m] at [m][a] (both triangle stages)
   double* sBt = BmT + D::BMT;             // [QV][N1]
@@ -420,6 +421,350 @@ bool launch_apply_quad(sem_ctx* c, int level, const double* u, double* y, int fl
     case 3: apply_quad_P<3>(c, L, u, y, flags); break;
     case 4: apply_quad_P<4>(c, L, u, y, flags); break;
     case 5: apply_quad_P<5>(c, L, u, y, flags); break;
+    default: return false;
+  }
+  c->launches++;
+  return true;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// k_apply_qs<P>: the same four-element quad, split over MTQ warps (one per row tile mt of the
+// (q, e) rows, i.e. vertical points q = 2 mt, 2 mt + 1).  Same arithmetic as k_apply_quad per row
+// tile; what changes is the register footprint: a warp holds only its tile's stage-A fragments
+// and stage-B^T accumulators (~130 registers instead of 242), so 15-16 warps fit per SM (4 per
+// scheduler instead of 2) and the DMMA / shared-memory latencies of one warp hide behind the
+// others.  The quad's data are shared by its group of warps:
+//   * u gathered once per quad into shared memory (cp.async, all the group's threads);
+//   * the geometric factors of the quad's current a-tile: one ring of R slots per group, filled
+//     by four TMA bulk copies (one per element) issued by the group's first warp, "full" mbarrier
+//     (tx bytes) waited on by every warp, "empty" mbarrier (one arrival per warp) waited on by the
+//     producer before it refills a slot;
+//   * stage A^T writes each warp's partial y (its two q values summed by one xor-16 shuffle) to a
+//     per-warp shared buffer; after a group barrier the group sums the MTQ partials in a fixed
+//     order and scatters with FP64 atomics, element-major (coalesced connectivity reads).
+// Group barriers are named barriers (bar.sync 1 + group, 32 MTQ threads).
+template <int P>
+struct AS {
+  using B = AQ<P>;
+  static constexpr int N1 = B::N1, NT = B::NT, QT = B::QT, QV = B::QV, Q = B::Q, N = B::N;
+  static constexpr int MW = B::MTQ;             // warps per quad group (row tiles)
+  static constexpr int NG = P == 3 ? 8 : P == 6 ? 3 : 5;   // groups per CTA
+  static constexpr int W = MW * NG;
+  static constexpr int R = 2;
+  static constexpr int KM = B::KM, MTA = B::MTA, NM = B::NM, NALAST = B::NALAST, QE = B::QE, LDA = B::LDA;
+  static constexpr int TSE = B::TSE, TS = B::TS, UST = B::UST, NYL = B::NYL;
+  static constexpr int BT = B::BT, BM = B::BM;
+  // B_c[a][m] at [m][a] in shared memory with row offsets ro(m) = m LDB + 4 ((m >> 1) & 1), LDB = 8 mod 16:
+  // conflict-free for both the 8-byte stage-B loads (half-warp: m = 4 ks + c4, a = 8 na + r4) and the
+  // 16-byte stage-B^T loads (quarter-warp: m = 8 nm + r4, a pair 8 na + 2 c4)
+  static constexpr int LDB = ((8 * MTA + 4 + 7) / 16) * 16 + 8;
+  static constexpr int CSB = 8 * NM * LDB + 8;  // component stride
+  static constexpr int BMT = 3 * CSB;
+  static constexpr int SU = 4 * UST, SY = MW * 4 * N, SC = 4 * N;
+  static constexpr int NGQ = (4 * N + 32 * MW - 1) / (32 * MW);   // scatter entries per thread
+  static constexpr int GD = R * TS + SU + SY;   // doubles per group
+  static constexpr int SMEM = (BMT + BT + NG * GD) * 8 + NG * SC * 4 + NG * 2 * R * 8;
+  static_assert(LDB % 16 == 8 && LDB >= 8 * MTA + 4, "qs operand layout");
+  static_assert(SMEM <= 227 * 1024, "apply_qs shared memory");
+};
+
+__device__ __forceinline__ void qs_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void qs_wait(uint32_t mb, uint32_t par) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(mb), "r"(par)
+        : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * AS<P>::W, 1)
+    k_apply_qs(int E, const int32_t* __restrict__ conn, const double* __restrict__ Gw,
+               const double* __restrict__ mats, const double* __restrict__ u, double* __restrict__ y, int flags,
+               const int32_t* __restrict__ elist) {
+  using D = AS<P>;
+  extern __shared__ __align__(128) double sm[];
+  double* BmT = sm;
+  double* sBt = BmT + D::BMT;
+  double* sDt = sBt + D::QV * D::N1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / D::MW, mt = warp % D::MW, gt = tid - grp * 32 * D::MW;
+  const int r4 = lane >> 2, c4 = lane & 3, el = r4 & 3, h = r4 >> 2, q = 2 * mt + h;
+  double* gbase = sBt + D::BT + grp * D::GD;
+  double* ring = gbase;                       // [R][4][TSE]
+  double* su = ring + D::R * D::TS;           // [4][UST]
+  double* yb = su + D::SU;                    // [MW][4][N]
+  int32_t* scn = reinterpret_cast<int32_t*>(sBt + D::BT + D::NG * D::GD) + grp * D::SC;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<int32_t*>(sBt + D::BT + D::NG * D::GD) +
+                                               D::NG * D::SC) + grp * 2 * D::R;   // full[R], empty[R]
+  {  // BmT (global: [3][8 NM][LDA]) -> shared rows at ro(m); then Bt, Dt
+    constexpr int RW = 8 * D::MTA, CW = 8 * D::NM * RW;
+    for (int i = tid; i < 3 * CW; i += 32 * D::W) {
+      const int c = i / CW, m = (i - c * CW) / RW, a = i - c * CW - m * RW;
+      sm[c * D::CSB + m * D::LDB + 4 * ((m >> 1) & 1) + a] = __ldg(mats + D::BM + (c * 8 * D::NM + m) * D::LDA + a);
+    }
+    for (int i = tid; i < D::BT; i += 32 * D::W) sBt[i] = __ldg(mats + D::BM + AQ<P>::BMT + i);
+  }
+  if (gt == 0) {
+    for (int b = 0; b < D::R; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(aq_smem(mbar + b)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(aq_smem(mbar + D::R + b)), "r"(D::MW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int gbar = 1 + grp, gthr = 32 * D::MW;
+  const double sgn = (flags & AP_NEGATE) ? -1.0 : 1.0;
+  const int nquad = (E + 3) >> 2;
+  const int qstride = gridDim.x * D::NG;
+  const int q0 = blockIdx.x * D::NG + grp;
+  auto elem = [&](int i) { return elist ? __ldg(elist + i) : i; };
+  // copy t of this group: quad q0 + (t / MTA) qstride, a-tile t % MTA, slot t % R
+  auto issue = [&](int t) {
+    const int qd = q0 + (t / D::MTA) * qstride, ma = t % D::MTA;
+    if (qd >= nquad) return;
+    if (t >= D::R) qs_wait(aq_smem(mbar + D::R + t % D::R), (uint32_t)((t / D::R) - 1) & 1u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const int ne = min(4, E - 4 * qd);
+    const uint32_t one = (uint32_t)(6 * D::QV * (ma < D::MTA - 1 ? 8 : D::NALAST)) * 8u;
+    const uint32_t mb = aq_smem(mbar + t % D::R);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(one * ne) : "memory");
+    for (int k = 0; k < ne; ++k)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              aq_smem(ring + (t % D::R) * D::TS + k * D::TSE)),
+          "l"(Gw + (size_t)elem(4 * qd + k) * 6 * D::Q + (size_t)ma * 48 * D::QV), "r"(one), "r"(mb)
+          : "memory");
+  };
+  // the gather of the next quad is staged by the group's last warp alone (its own cp.async
+  // groups and __syncwarp: no group barrier), the producer of the G ring is the first warp
+  const bool stager = mt == D::MW - 1;
+  auto stage_conn = [&](int qd) {
+    const int ne = min(4, E - 4 * qd);
+    for (int i = lane; i < ne * D::N; i += 32) {
+      const int k = i / D::N;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(aq_smem(scn + i)),
+                   "l"(conn + (size_t)elem(4 * qd + k) * D::N + (i - k * D::N))
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto stage_u = [&](int qd) {
+    const int nval = min(4, E - 4 * qd) * D::N;
+    for (int i = lane; i < D::SC; i += 32) {
+      const int g = i < nval ? scn[i] : INT_MIN;
+      const bool take = g >= 0 || (g != INT_MIN && (flags & AP_GATHER_ALL));
+      const double* src = u + (take ? (g >= 0 ? g : ~g) : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(aq_smem(su + (i / D::N) * D::UST + i % D::N)),
+                   "l"(src), "r"(take ? 8 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (q0 < nquad) {
+    if (gt == 0)
+      for (int t = 0; t < D::R; ++t) issue(t);
+    if (stager) {
+      stage_conn(q0);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      stage_u(q0);
+    }
+  }
+  int tk = 0;
+  for (int qd = q0; qd < nquad; qd += qstride, tk += D::MTA) {
+    const bool ev = 4 * qd + el < E;
+    // ---- stage A (FMA): this warp's A fragments, m = 4 ks + c4, q = 2 mt + h
+    double Ua[D::KM], Ud[D::KM];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    qs_bar(gbar, gthr);   // u of this quad visible; the previous quad's yb consumed
+    const int ne = min(4, E - 4 * qd);
+    int gq[D::NGQ];       // scatter targets of this thread (scn is refilled for the next quad below)
+#pragma unroll
+    for (int k = 0; k < D::NGQ; ++k) {
+      const int i = gt + k * gthr;
+      gq[k] = i < ne * D::N ? scn[i] : INT_MIN;
+    }
+#pragma unroll
+    for (int ks = 0; ks < D::KM; ++ks) Ua[ks] = Ud[ks] = 0.0;
+    if (q < D::QV) {
+#pragma unroll
+      for (int l = 0; l < D::N1; ++l) {
+        const double bt = sBt[q * D::N1 + l], dt = sDt[q * D::N1 + l];
+#pragma unroll
+        for (int ks = 0; ks < D::KM; ++ks) {
+          const int m = 4 * ks + c4;
+          const double uu = (ev && m < D::NT) ? su[el * D::UST + m + D::NT * l] : 0.0;
+          Ua[ks] = fma(uu, bt, Ua[ks]);
+          Ud[ks] = fma(uu, dt, Ud[ks]);
+        }
+      }
+    }
+    qs_bar(gbar, gthr);   // su and scn free
+    const int qn = qd + qstride;
+    if (stager && qn < nquad) stage_conn(qn);
+    double Vt[D::NM][2], Vd[D::NM][2];
+#pragma unroll
+    for (int nm = 0; nm < D::NM; ++nm) Vt[nm][0] = Vt[nm][1] = Vd[nm][0] = Vd[nm][1] = 0.0;
+#pragma unroll 1
+    for (int na = 0; na < D::MTA; ++na) {
+      const int t = tk + na;
+      if (stager && na == D::MTA / 2 && qn < nquad) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        stage_u(qn);
+      }
+      qs_wait(aq_smem(mbar + t % D::R), (uint32_t)(t / D::R) & 1u);
+      // ---- stage B: g_c^T[(q,e)][a] of this warp's row tile
+      double g[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int ks = 0; ks < D::KM; ++ks) {
+        const int m = 4 * ks + c4, off = m * D::LDB + 4 * ((m >> 1) & 1) + 8 * na + r4;
+        const double br = BmT[off], bs = BmT[D::CSB + off], b0 = BmT[2 * D::CSB + off];
+        aq_dmma(g[0][0], g[0][1], Ua[ks], br);
+        aq_dmma(g[1][0], g[1][1], Ua[ks], bs);
+        aq_dmma(g[2][0], g[2][1], Ud[ks], b0);
+      }
+      // ---- w = G g at (a = 8 na + 2 c4 + i, q)
+      const int nat = (na < D::MTA - 1) ? 8 : D::NALAST;
+      const double* Gt = ring + (t % D::R) * D::TS + el * D::TSE;
+      const int cs = D::QV * nat;
+      const int qp = (q & 1) ? D::QE + (q >> 1) : (q >> 1);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int al = 2 * c4 + i;
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+        if (ev && q < D::QV && al < nat) {
+          const double* gp = Gt + qp * nat + al;
+          double gxx, gxy, gxz, gyy, gyz, gzz;
+          if ((D::NALAST & 1) == 0 || na < D::MTA - 1) {
+            const double2 v0 = *reinterpret_cast<const double2*>(gp - i);
+            const double2 v1 = *reinterpret_cast<const double2*>(gp - i + cs);
+            const double2 v2 = *reinterpret_cast<const double2*>(gp - i + 2 * cs);
+            const double2 v3 = *reinterpret_cast<const double2*>(gp - i + 3 * cs);
+            const double2 v4 = *reinterpret_cast<const double2*>(gp - i + 4 * cs);
+            const double2 v5 = *reinterpret_cast<const double2*>(gp - i + 5 * cs);
+            gxx = i ? v0.y : v0.x;
+            gxy = i ? v1.y : v1.x;
+            gxz = i ? v2.y : v2.x;
+            gyy = i ? v3.y : v3.x;
+            gyz = i ? v4.y : v4.x;
+            gzz = i ? v5.y : v5.x;
+          } else {
+            gxx = gp[0];
+            gxy = gp[cs];
+            gxz = gp[2 * cs];
+            gyy = gp[3 * cs];
+            gyz = gp[4 * cs];
+            gzz = gp[5 * cs];
+          }
+          const double x0 = g[0][i], x1 = g[1][i], x2 = g[2][i];
+          w0 = gxx * x0 + gxy * x1 + gxz * x2;
+          w1 = gxy * x0 + gyy * x1 + gyz * x2;
+          w2 = gxz * x0 + gyz * x1 + gzz * x2;
+        }
+        g[0][i] = w0;
+        g[1][i] = w1;
+        g[2][i] = w2;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(aq_smem(mbar + D::R + t % D::R)) : "memory");
+      if (mt == 0 && lane == 0) issue(t + D::R);
+      // ---- stage B^T: V^T[(q,e)][m] += w^T[(q,e)][a] B_c[a][m]; k-step i <-> a = 8 na + 2 c4 + i
+      double2 bo[3][D::NM];
+#pragma unroll
+      for (int nm = 0; nm < D::NM; ++nm) {
+        const int m = 8 * nm + r4, off = m * D::LDB + 4 * ((m >> 1) & 1) + 8 * na + 2 * c4;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) bo[c][nm] = *reinterpret_cast<const double2*>(BmT + c * D::CSB + off);
+      }
+      // component order r, 0, s: the two updates of a Vt accumulator per k-step are 2 NM apart
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+          for (int nm = 0; nm < D::NM; ++nm) {
+            const int c = cc == 0 ? 0 : (cc == 1 ? 2 : 1);
+            const double b = i ? bo[c][nm].y : bo[c][nm].x;
+            if (c < 2) aq_dmma(Vt[nm][0], Vt[nm][1], g[c][i], b);
+            else aq_dmma(Vd[nm][0], Vd[nm][1], g[2][i], b);
+          }
+    }
+    // ---- stage A^T (FMA): partial y of this warp's two q values -> yb[mt]
+    double* ybw = yb + mt * 4 * D::N + el * D::N;
+#pragma unroll
+    for (int l = 0; l < D::N1; ++l) {
+      const double bt = q < D::QV ? sBt[q * D::N1 + l] : 0.0, dt = q < D::QV ? sDt[q * D::N1 + l] : 0.0;
+      double yl[D::NM][2];
+#pragma unroll
+      for (int nm = 0; nm < D::NM; ++nm)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double v = fma(Vt[nm][i], bt, Vd[nm][i] * dt);
+          yl[nm][i] = v + __shfl_xor_sync(0xffffffffu, v, 16);
+        }
+      if ((l < D::NYL) == (h == 0)) {
+#pragma unroll
+        for (int nm = 0; nm < D::NM; ++nm)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int m = 8 * nm + 2 * c4 + i;
+            if (m < D::NT) ybw[m + D::NT * l] = yl[nm][i];
+          }
+      }
+    }
+    qs_bar(gbar, gthr);
+    // ---- sum the MW partials (fixed order) and scatter, element-major
+#pragma unroll
+    for (int k = 0; k < D::NGQ; ++k) {
+      const int i = gt + k * gthr, g = gq[k];
+      if (g == INT_MIN) continue;
+      double acc = yb[i];
+#pragma unroll
+      for (int w = 1; w < D::MW; ++w) acc += yb[w * 4 * D::N + i];
+      if (g >= 0) atomicAdd(y + g, sgn * acc);
+      else if (flags & AP_SCATTER_ALL) atomicAdd(y + ~g, sgn * acc);
+    }
+  }
+}
+
+template <int P>
+static void apply_qs_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags,
+                       const int32_t* elist, int ne) {
+  using D = AS<P>;
+  static int grid_maxes[kMaxDev] = {0};
+  const int dev = cur_device();
+  int& grid_max = grid_maxes[dev];
+  if (!grid_max) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_apply_qs<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
+    int per_sm = 0, sms = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_qs<P>, 32 * D::W, D::SMEM));
+    grid_max = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int E = elist ? ne : c->E_own;
+  if (E == 0) return;
+  const int nquad = (E + 3) / 4;
+  const int need = (nquad + D::NG - 1) / D::NG;
+  const int grid = need < grid_max ? need : grid_max;
+  k_apply_qs<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(E, L.conn, L.Gw, L.qmats, u, y, flags, elist);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+bool launch_apply_qs(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne) {
+  const DeviceLevel& L = c->L[level];
+  if (!L.qmats || !L.Gw) return false;
+  switch (L.p) {
+    case 3: apply_qs_P<3>(c, L, u, y, flags, elist, ne); break;
+    case 4: apply_qs_P<4>(c, L, u, y, flags, elist, ne); break;
+    case 5: apply_qs_P<5>(c, L, u, y, flags, elist, ne); break;
+    case 6: apply_qs_P<6>(c, L, u, y, flags, elist, ne); break;
     default: return false;
   }
   c->launches++;

@@ -396,7 +396,7 @@ __global__ void k_g_tiles(int64_t E, int QT, int QV, const double* __restrict__ 
 void build_g_tiles(sem_ctx* c, int level) {
   DeviceLevel& L = c->L[level];
   const int QT = L.ref.qt, QV = L.ref.qv;
-  if (L.p > 6 || (c->opts.apply_kernel != 0 && c->opts.apply_kernel != 3)) return;
+  if (L.p > 6 || (c->opts.apply_kernel != 0 && c->opts.apply_kernel != 3 && c->opts.apply_kernel != 4)) return;
   if (!L.Gw) {  // refreshed in place by sem_update_geometry
     CUDA_CHECK(cudaMalloc(&L.Gw, (size_t)c->E * 6 * L.Q * sizeof(double)));
     c->allocs.push_back(L.Gw);

@@ -394,7 +394,7 @@ void check_opts(const sem_opts& o) {
   if (o.pz < 0 || o.pz > 8) throw SemError(SEM_EINVAL, "bad options: pz");
   if (o.coarse_agg < -1 || o.coarse_agg > 8192) throw SemError(SEM_EINVAL, "bad options: coarse_agg (-1..8192)");
   if (o.nu1 < 0 || o.nu2 < 0 || o.overlap < -1 || o.outer < 0 || o.outer > 2 || o.apply_kernel < 0 ||
-      o.apply_kernel > 3 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
+      o.apply_kernel > 4 || o.coarse_solver < 0 || o.coarse_solver > 2 || !(o.coarse_rtol > 0) ||
       o.coarse_maxit < 1 || o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks)
     throw SemError(SEM_EINVAL, "bad options");
 }
@@ -582,7 +582,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
     if (L.p == L.q) {  // the tensor-core kernels are isotropic; (P_xy, P_z) levels use k_apply_pq
       L.frag = upload(c, dmma_fragments(R));
       if (L.p <= 6) L.wmats = upload(c, warp_apply_mats(R));
-      if (L.p >= 3 && L.p <= 5) L.qmats = upload(c, quad_apply_mats(R));
+      if (L.p >= 3 && L.p <= 6) L.qmats = upload(c, quad_apply_mats(R));
     }
     // geometric factors from the finest nodal map (all held elements)
     L.G = dalloc<double>(c, (size_t)E * 6 * L.Q);
@@ -616,7 +616,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
     Scratch s2;
     double* d_D = s2.put(c->L[li].ref.Dfull);
     const int lid = lids[li];
-    if ((o.apply_kernel == 0 || o.apply_kernel == 3) && c->L[li].p == c->L[li].q) build_p1_matrices(c, li, d_D);
+    if ((o.apply_kernel == 0 || o.apply_kernel >= 3) && c->L[li].p == c->L[li].q) build_p1_matrices(c, li, d_D);
     if (li + 1 < nl) {
       double t0 = now_ms();
       if (part && o.local_solve == 1) {  // partitioned FDM / exact-dense hybrid (O33, O35)
@@ -1343,7 +1343,7 @@ int sem_bench_kernel(sem_ctx* c, int kernel, int level, int reps, double* mean_u
                      (L.nsub ? 4.0 * L.nk_sum : 0.0);
       else if (kernel == 0)
         *alg_bytes = (L.tiles32 ? 4.0 : 8.0) * L.packed + 4.0 * L.nk_sum + 32.0 * L.n;
-      else if (L.Ae1 && (t->opts.apply_kernel == 0 || t->opts.apply_kernel == 3))  // element-matrix path (p <= 2)
+      else if (L.Ae1 && (t->opts.apply_kernel == 0 || t->opts.apply_kernel >= 3))  // element-matrix path (p <= 2)
         *alg_bytes = (double)t->E_own * (8.0 * L.N * (L.N + 1) / 2 + 4.0 * L.N) + 16.0 * L.n;
       else
         *alg_bytes = (double)t->E_own * (48.0 * L.Q + 4.0 * L.N) + 16.0 * L.n;

@@ -133,6 +133,13 @@ struct Dist {
   bool overlap = true;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_xfer = nullptr;
+  // PCG's z = V(r) on fixed buffers (r = bw, z = pw / zw of every part) replayed from a CUDA
+  // graph (vcycle_pcg below): kernels, exchanges (comm-stream fork/join, NCCL send/recv or the
+  // emulated copies), the coarse all-reduce and solve
+  cudaGraphExec_t vc_exec[2] = {nullptr, nullptr};
+  std::vector<int64_t> vc_dl[2];   // kernel launches of one replay per part, coarse ctx last
+  cudaStream_t cap_stream = nullptr;
+  int vc_eager = 0;
 };
 
 template <class F>
@@ -199,14 +206,14 @@ static void exchange(Dist& D, int li, const std::vector<double*>& v) {
 }
 
 // y (+)= A u on level li (each part's owned elements), then the exchange that completes y.
-// Overlapped when every part can apply element subsets (k_apply_warp, p <= 6): interface
+// Overlapped when every part can apply element subsets (k_apply_qs / k_apply_warp, p <= 6): interface
 // elements -> pack -> [transfer on the comm stream || interior elements] -> unpack-add.
 // Correct because interior elements write no exchanged node, so the packed partial sums
 // are final once the interface elements are done.
 static void apply_exchange(Dist& D, int li, const std::vector<double*>& u, const std::vector<double*>& y, int flags) {
   bool ov = D.overlap;
   for (auto* c : D.parts) ov = ov && c->L[li].e_if && c->L[li].wmats && c->L[li].Gw && !c->det.on &&
-                               (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3);
+                               (c->opts.apply_kernel == 0 || c->opts.apply_kernel >= 3);
   if (!ov) {
     each(D, [&](sem_ctx* c, int i) { launch_apply(c, li, u[i], y[i], flags); });
     exchange(D, li, y);
@@ -215,7 +222,7 @@ static void apply_exchange(Dist& D, int li, const std::vector<double*>& u, const
   sem_ctx* c0 = D.parts[0];
   each(D, [&](sem_ctx* c, int i) {
     DeviceLevel& L = c->L[li];
-    if (L.n_if && !launch_apply_warp(c, li, u[i], y[i], flags, L.e_if, L.n_if))
+    if (L.n_if && !launch_apply_subset(c, li, u[i], y[i], flags, L.e_if, L.n_if))
       throw SemError(SEM_ECUDA, "interface apply");
   });
   pack_all(D, li, y);
@@ -225,7 +232,7 @@ static void apply_exchange(Dist& D, int li, const std::vector<double*>& u, const
   CUDA_CHECK(cudaEventRecord(D.ev_xfer, D.comm_stream));
   each(D, [&](sem_ctx* c, int i) {
     DeviceLevel& L = c->L[li];
-    if (L.n_in && !launch_apply_warp(c, li, u[i], y[i], flags, L.e_in, L.n_in))
+    if (L.n_in && !launch_apply_subset(c, li, u[i], y[i], flags, L.e_in, L.n_in))
       throw SemError(SEM_ECUDA, "interior apply");
   });
   CUDA_CHECK(cudaStreamWaitEvent(c0->stream, D.ev_xfer, 0));
@@ -368,6 +375,62 @@ static void vcycle(Dist& D, int li, const Vecs& f, const Vecs& u) {
   }
 }
 
+// z = V(r) for the PCG / MG loops, replayed from a CUDA graph after one eager V-cycle (function
+// attributes and lazily sized buffers settled).  Every part and the coarse ctx must run on one
+// stream (NCCL: one part per process; emulated: the parts share the caller's stream), else
+// eager.  SEM_NO_GRAPHS=1 or SEM_DIST_GRAPHS=0 turn it off.
+static void vcycle_pcg(Dist& D, const Vecs& r, const Vecs& z, int slot) {
+  static const int off = [] {
+    const char* e = getenv("SEM_NO_GRAPHS");
+    const char* f = getenv("SEM_DIST_GRAPHS");
+    return ((e && atoi(e)) || (f && !atoi(f))) ? 1 : 0;
+  }();
+  sem_ctx* c0 = D.parts[0];
+  bool same = D.coarse->stream == c0->stream;
+  for (auto* c : D.parts) same = same && c->stream == c0->stream;
+  if (off || !same || D.vc_eager < 1) {
+    vcycle(D, 0, r, z);
+    D.vc_eager++;
+    return;
+  }
+  const int R = (int)D.parts.size();
+  if (!D.vc_exec[slot]) {
+    if (!D.cap_stream) CUDA_CHECK(cudaStreamCreateWithFlags(&D.cap_stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamSynchronize(c0->stream));
+    CUDA_CHECK(cudaStreamSynchronize(D.comm_stream));
+    const cudaStream_t keep = c0->stream;
+    std::vector<int64_t> l0;
+    for (auto* c : D.parts) l0.push_back(c->launches), c->stream = D.cap_stream;
+    l0.push_back(D.coarse->launches);
+    D.coarse->stream = D.cap_stream;
+    auto restore = [&] {
+      for (auto* c : D.parts) c->stream = keep;
+      D.coarse->stream = keep;
+    };
+    cudaGraph_t g = nullptr;
+    CUDA_CHECK(cudaStreamBeginCapture(D.cap_stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      vcycle(D, 0, r, z);
+    } catch (...) {
+      cudaStreamEndCapture(D.cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+      restore();
+      throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(D.cap_stream, &g));
+    restore();
+    D.vc_dl[slot].assign(R + 1, 0);
+    for (int i = 0; i < R; ++i) D.vc_dl[slot][i] = D.parts[i]->launches - l0[i], D.parts[i]->launches = l0[i];
+    D.vc_dl[slot][R] = D.coarse->launches - l0[R];
+    D.coarse->launches = l0[R];
+    CUDA_CHECK(cudaGraphInstantiate(&D.vc_exec[slot], g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+  }
+  CUDA_CHECK(cudaGraphLaunch(D.vc_exec[slot], c0->stream));
+  for (int i = 0; i < R; ++i) D.parts[i]->launches += D.vc_dl[slot][i];
+  D.coarse->launches += D.vc_dl[slot][R];
+}
+
 static void read_scal(Dist& D, int s, int k, double* out) {
   sem_ctx* c = D.parts[0];
   CUDA_CHECK(cudaMemcpyAsync(c->hscal, c->scal + s, k * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -429,7 +492,7 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
   if (rn <= thresh) {
     R.converged = 1;
   } else if (o.outer == 0) {
-    vcycle(D, 0, r, p);
+    vcycle_pcg(D, r, p, 0);
     R.vcycles++;
     int dcur = 8, dnew = 10;
     dot(D, p, r, nullptr, nullptr, dcur);
@@ -455,7 +518,7 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
         R.converged = 1;
         break;
       }
-      vcycle(D, 0, r, z);
+      vcycle_pcg(D, r, z, 1);
       R.vcycles++;
       if (flex) {
         dot(D, z, r, &z, &ro, dnew);
@@ -468,7 +531,7 @@ static int solve(Dist& D, const Vecs& rhs, const Vecs& phiD, double tol, const V
     }
   } else {
     while (R.iters < o.imax) {
-      vcycle(D, 0, r, z);
+      vcycle_pcg(D, r, z, 1);
       R.vcycles++;
       each(D, [&](sem_ctx* c, int i) {
         launch_axpy(c, c->L[0].n, 1.0, z[i], u[i]);
@@ -846,6 +909,9 @@ void dist_destroy(sem_ctx* c) {
   if (D->ev_pack) cudaEventDestroy(D->ev_pack);
   if (D->ev_xfer) cudaEventDestroy(D->ev_xfer);
   if (D->comm_stream) cudaStreamDestroy(D->comm_stream);
+  for (auto& e : D->vc_exec)
+    if (e) cudaGraphExecDestroy(e);
+  if (D->cap_stream) cudaStreamDestroy(D->cap_stream);
   delete D;
   c->dist = nullptr;
 }

@@ -682,14 +682,19 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
   double yk[MT][NVT][2];
   if (active) {
     const int e = eid[j];
-    // T = S_h^T B1
+    // T = S_h^T B1 over the unit's mtu = ceil(n_h / 8) tiles (S_h is zero beyond n_h: the
+    // skipped tiles are exact zeros); for MT >= 5 only (the guards cost more than they save at
+    // the small tile counts of p <= 3: measured on config 5's p = 2, 3 levels)
+    const int mtu = MT >= 5 ? (nh + 7) / 8 : MT, ktu = 2 * mtu;
     double T[MT][NVT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
       for (int n = 0; n < NVT; ++n) T[mt][n][0] = T[mt][n][1] = 0.0;
+      if (mt >= mtu) continue;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
+        if (kt >= ktu) break;
         const double af = Ss[(kt * 4 + (lane & 3)) * LDS + mt * 8 + (lane >> 2)];
 #pragma unroll
         for (int n = 0; n < NVT; ++n) fdm_dmma(T[mt][n][0], T[mt][n][1], af, b1[kt][n]);
@@ -713,6 +718,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
     const double* Lh = lh + ho;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
+      if (mt >= mtu) break;
       double v[NVT][2];
 #pragma unroll
       for (int n = 0; n < NVT; ++n) v[n][0] = v[n][1] = 0.0;
@@ -763,8 +769,10 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
     for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
       for (int n = 0; n < NVT; ++n) yk[mt][n][0] = yk[mt][n][1] = 0.0;
+      if (mt >= mtu) continue;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
+        if (kt >= ktu) break;
         const double af = Ss[(mt * 8 + (lane >> 2)) * LDS + kt * 4 + (lane & 3)];
 #pragma unroll
         for (int n = 0; n < NVT; ++n) fdm_dmma(yk[mt][n][0], yk[mt][n][1], af, b2[kt][n]);
@@ -821,17 +829,19 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
 //   Ys = S_h Zs                   CTA-wide over the stacked columns
 //   u += sum_j Ys[:, box j]       summed per column node, scattered once (x W for S^-1)
 // Same arithmetic per box as k_fdm_warp; ~40 % fewer DMMAs at p = 6.
-// C[ROWS][ncol] = A B on the CTA's 8 warps, jobs of 2 m-tiles x 2 n-tiles (four independent
-// accumulator chains); A fragment a0 = A[m][k] read through (m, k) -> aidx, B from Bs[k][n] (ld ldb)
+// C[8 mtu][ncol] = A B on the CTA's 8 warps, jobs of 2 m-tiles x 2 n-tiles (four independent
+// accumulator chains); A fragment a0 = A[m][k] read through (m, k) -> aidx, B from Bs[k][n] (ld ldb).
+// Only the unit's mtu = ceil(n_h / 8) row / contraction tiles: S_h is zero beyond n_h, so the
+// skipped tiles contribute exact zeros (and later steps read no row >= 8 mtu)
 template <int MT, bool AT>
 __device__ __forceinline__ void fdm_cta_gemm(const double* __restrict__ Ss, const double* __restrict__ Bs,
-                                             double* __restrict__ Cs, int ldb, int ncol, int warp, int lane) {
-  constexpr int ROWS = 8 * MT, KT = 2 * MT, LDS = ROWS + 4, MP = (MT + 1) / 2;
+                                             double* __restrict__ Cs, int ldb, int ncol, int warp, int lane, int mtu) {
+  constexpr int ROWS = 8 * MT, LDS = ROWS + 4;
   const int r4 = lane >> 2, c4 = lane & 3;
-  const int nt = (ncol + 7) / 8, np = (nt + 1) / 2;
+  const int nt = (ncol + 7) / 8, np = (nt + 1) / 2, MP = (mtu + 1) / 2, KT = 2 * mtu;
   for (int job = warp; job < MP * np; job += 8) {
     const int m0 = 2 * (job % MP), n0 = 2 * (job / MP);
-    const bool m2 = m0 + 1 < MT, n2 = n0 + 1 < nt;
+    const bool m2 = m0 + 1 < mtu, n2 = n0 + 1 < nt;
     double cc[2][2][2] = {};
 #pragma unroll 4
     for (int kt = 0; kt < KT; ++kt) {
@@ -895,6 +905,15 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     }
     soff[cnt] = acc;
   }
+  const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
+  const int nval = nh * nzu;
+  // node ids of the first gather chunk, in flight together with the S_h loads
+  int gid0[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int t = tid + 256 * k, h = t / nzu, zz = t - h * nzu;
+    gid0[k] = t < nval ? __ldg(ci + h * nz + zlo + zz) : -1;
+  }
   {  // S_h -> shared
     constexpr int IS = (ROWS * ROWS + 255) / 256;
     double tmp[IS];
@@ -929,18 +948,16 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) lav[mt] = mt * 8 + r4 < nh ? __ldg(lh + ho + mt * 8 + r4) : 1.0;
   }
-  const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
   // column block (x W for S^-T): the n_h x n_zu valid entries; rows >= n_h zeroed (they meet the
   // zero columns of S_h^T: stale shared memory there could hold non-finite values), columns
   // >= n_zu only reach output columns no later step reads
-  const int nval = nh * nzu;
   for (int base = 0; base < nval; base += 256 * 8) {
     int gid[8], pos[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int t = base + tid + 256 * k, h = t / nzu, zz = t - h * nzu;
       pos[k] = t < nval ? h * ldb + zz : -1;
-      gid[k] = t < nval ? __ldg(ci + h * nz + zlo + zz) : -1;
+      gid[k] = base == 0 ? gid0[k] : (t < nval ? __ldg(ci + h * nz + zlo + zz) : -1);
     }
     double val[8];
 #pragma unroll
@@ -957,13 +974,15 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   for (int t = nh * ldb + tid; t < ROWS * ldb; t += 256) B1[t] = 0.0;
   __syncthreads();
   // 1. Tall = S_h^T Rc -> B2
-  fdm_cta_gemm<MT, true>(Ss, B1, B2, ldb, nzu, warp, lane);
+  const int mtu = (nh + 7) / 8;
+  fdm_cta_gemm<MT, true>(Ss, B1, B2, ldb, nzu, warp, lane, mtu);
   __syncthreads();
   // 2. warp j: vertical transform and scaling of box j, stored compactly into Zs (B1)
   if (warp < cnt && !sk[warp]) {
     const int j = warp, zb = ez0[j] - zlo, nvj = env[j], so = soff[j];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
+      if (mt >= mtu) break;
       double v[NVT][2];
 #pragma unroll
       for (int n = 0; n < NVT; ++n) v[n][0] = v[n][1] = 0.0;
@@ -1005,34 +1024,57 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   }
   __syncthreads();
   // 3. Ys = S_h Zs -> B2 over the stacked columns
-  fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, soff[cnt], warp, lane);
+  fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, soff[cnt], warp, lane, mtu);
   __syncthreads();
   // 4. every column node of the unit: sum of the boxes holding it, scatter (x W for S^-1).
   // The boxes are ordered by layer and their z ranges increase with j: the boxes holding z form
-  // a contiguous run [jlo, jhi], found per z from the unit's box table (fixed summation order j)
-  __shared__ short zj[2 * 8 * 16 + 2][2];
+  // a contiguous run; per z the stacked-column offsets of its (non-skipped) boxes are tabulated
+  // once (ascending j: fixed summation order), then the column nodes are processed in chunks of
+  // 8 per thread with independent connectivity and weight loads (two global round trips per
+  // chunk instead of two per node)
+  constexpr int ZO = 4;
+  __shared__ short zo[2 * 8 * 16 + 2][ZO];
+  __shared__ unsigned char zn[2 * 8 * 16 + 2];
   for (int z = tid; z < nzu; z += 256) {
-    int jlo = cnt, jhi = -1;
+    int k = 0;
     for (int j = 0; j < cnt; ++j) {
       const int zz = z - (ez0[j] - zlo);
-      if (zz >= 0 && zz < env[j]) {
-        jlo = min(jlo, j);
-        jhi = max(jhi, j);
+      if (zz >= 0 && zz < env[j] && !sk[j]) {
+        if (k < ZO) zo[z][k] = (short)(soff[j] + zz);
+        ++k;
       }
     }
-    zj[z][0] = (short)jlo;
-    zj[z][1] = (short)jhi;
+    zn[z] = (unsigned char)k;
   }
   __syncthreads();
-  for (int t = tid; t < nh * nzu; t += 256) {
-    const int h = t / nzu, z = t - h * nzu;
-    const int g = __ldg(ci + h * nz + zlo + z);
-    if (g < 0) continue;
-    double acc = 0.0;
-    for (int j = zj[z][0]; j <= zj[z][1]; ++j)
-      if (!sk[j]) acc += B2[h * ldb + soff[j] + z - (ez0[j] - zlo)];
-    if (!transpose) acc *= __ldg(W + g);
-    atomicAdd(u + g, acc);
+  const int ntot = nh * nzu;
+  for (int base = 0; base < ntot; base += 256 * 8) {
+    int g[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = base + tid + 256 * k, h = t / nzu, z = t - h * nzu;
+      g[k] = t < ntot ? __ldg(ci + h * nz + zlo + z) : -1;
+    }
+    double wv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wv[k] = (!transpose && g[k] >= 0) ? __ldg(W + g[k]) : 1.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (g[k] < 0) continue;
+      const int t = base + tid + 256 * k, h = t / nzu, z = t - h * nzu;
+      const double* row = B2 + h * ldb;
+      const int nk = zn[z];
+      double acc = 0.0;
+      if (nk <= ZO) {
+        for (int q = 0; q < nk; ++q) acc += row[zo[z][q]];
+      } else {  // more boxes than tabulated (not met for the box sizes of this kernel): walk the run
+        for (int j = 0; j < cnt; ++j) {
+          const int zz = z - (ez0[j] - zlo);
+          if (zz >= 0 && zz < env[j] && !sk[j]) acc += row[soff[j] + zz];
+        }
+      }
+      atomicAdd(u + g[k], acc * wv[k]);
+    }
   }
 }
 

@@ -251,6 +251,8 @@ bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int fl
 std::vector<double> quad_apply_mats(const LevelRef& R);
 bool launch_apply_quad(sem_ctx* c, int level, const double* u, double* y, int flags);
 void build_g_tiles(sem_ctx* c, int level);
+bool launch_apply_subset(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne);
+bool launch_apply_qs(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne);
 void build_p1_matrices(sem_ctx* c, int level, const double* d_D);
 void launch_init_masked(sem_ctx* c, int level, const double* src, double* dst, int mode);
 void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int transpose);

@@ -381,6 +381,16 @@ void build_p1_matrices(sem_ctx* c, int level, const double* d_D) {
   CUDA_CHECK(cudaFree(Ae));
 }
 
+// operator over an element subset (partitioned overlap, dist.cu): the same kernel choice as
+// launch_apply for the kernels that take element lists; false if none applies
+bool launch_apply_subset(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne) {
+  if (c->det.on || !(c->opts.apply_kernel == 0 || c->opts.apply_kernel >= 3)) return false;
+  if ((c->opts.apply_kernel == 4 || (c->opts.apply_kernel == 0 && c->L[level].p <= 5)) &&
+      launch_apply_qs(c, level, u, y, flags, elist, ne))
+    return true;
+  return launch_apply_warp(c, level, u, y, flags, elist, ne);
+}
+
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
   if (c->L[level].p != c->L[level].q) {  // anisotropic level
     apply_pq(c, c->L[level], u, y, flags);
@@ -389,7 +399,7 @@ void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) 
   }
   if (!c->det.on) {
     const DeviceLevel& L = c->L[level];
-    if (L.p <= 2 && L.Ae1 && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3)) {
+    if (L.p <= 2 && L.Ae1 && (c->opts.apply_kernel == 0 || c->opts.apply_kernel >= 3)) {
       if (c->E_own > 0) {
         if (L.p == 1)
           k_apply_em<6><<<(c->E_own + 127) / 128, 128, 0, c->stream>>>(c->E_own, (int64_t)c->E, L.conn, L.Ae1, u,
@@ -403,12 +413,14 @@ void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) 
       return;
     }
   }
-  // default (0): the four-elements-per-warp kernel at p = 3 (measured 80 vs 97 us on config 3's p = 3
-  // level), the warp-per-element kernel at p = 4..6 (quad: 427 vs 299 us at p = 5)
-  if (!c->det.on && (c->opts.apply_kernel == 3 || (c->opts.apply_kernel == 0 && c->L[level].p == 3)) &&
-      launch_apply_quad(c, level, u, y, flags))
+  // default (0): four elements per group of warps (k_apply_qs) at p = 3..5 (config 3 p = 5: 289 vs
+  // 312 us for k_apply_warp; config 4 p = 3: 683 vs 800 us for k_apply_quad), the warp-per-element
+  // kernel at p = 6 (699 vs 938 us)
+  if (!c->det.on && (c->opts.apply_kernel == 4 || (c->opts.apply_kernel == 0 && c->L[level].p <= 5)) &&
+      launch_apply_qs(c, level, u, y, flags, nullptr, 0))
     return;
-  if (!c->det.on && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 3) && launch_apply_warp(c, level, u, y, flags))
+  if (!c->det.on && c->opts.apply_kernel == 3 && launch_apply_quad(c, level, u, y, flags)) return;
+  if (!c->det.on && (c->opts.apply_kernel == 0 || c->opts.apply_kernel >= 3) && launch_apply_warp(c, level, u, y, flags))
     return;
   if (!c->det.on && c->opts.apply_kernel != 1) {
     launch_apply_dmma(c, level, u, y, flags);

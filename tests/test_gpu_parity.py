@@ -224,11 +224,12 @@ def test_literal_smoother_option(c1):
     assert rel(out[lev.free], mg.vcycle(r)) <= STEP_TOL
 
 
-@pytest.mark.parametrize("apply_kernel", [0, 1, 2, 3])
+@pytest.mark.parametrize("apply_kernel", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("p", range(1, 9))
 def test_config4_construction_every_order(p, apply_kernel):
     """Config-4 construction (scaled replica) at every order p = 1..8, both operator
-    kernels (0 = warp-per-element DMMA, 1 = FMA, 2 = batched DMMA, 3 = four elements per warp): apply and solve parity; p = 1 is the
+    kernels (0 = default, 1 = FMA, 2 = batched DMMA, 3 = four elements per warp, 4 = four elements per
+    group of warps): apply and solve parity; p = 1 is the
     single-level coarse solve (O26).  3x3 (p <= 5) or 2x2 quads x 2 layers = 36 / 16
     prisms: several element batches with a ragged last batch for every p."""
     m, lev, phiD, phi_direct = _c4_oracle(p)      # the oracle side, shared by the four kernel variants
@@ -242,6 +243,31 @@ def test_config4_construction_every_order(p, apply_kernel):
     phi, rep = s.solve(torch.from_numpy(phiD[perm]).cuda(), tol=1e-13)
     out[perm] = phi.cpu().numpy()
     assert rel(out, phi_direct) <= SOLVE_TOL
+
+
+@pytest.mark.parametrize("apply_kernel", [3, 4])
+@pytest.mark.parametrize("p", [3, 4, 5, 6])
+@pytest.mark.parametrize("nx,ny,nz", [(1, 1, 3), (5, 3, 3)])
+def test_quad_kernels_ragged(p, apply_kernel, nx, ny, nz):
+    """The four-element kernels on element counts that are not a multiple of four (6 and 90
+    prisms: a ragged last quad, one or several CTAs), masked and raw operator, against the
+    assembled oracle matrix (eq 3.8)."""
+    m = config1(p=p, nx=nx, ny=ny, nz=nz)
+    lev = sem.build_system(m, p)
+    s = make_solver(m, apply_kernel=apply_kernel)
+    perm = lib_to_oracle(s.node_xyz(0), lev.xyz)
+    u = random_vector(lev.n, seed=11 + p)
+    for masked in (False, True):
+        y = s.apply(torch.from_numpy(u[perm]).cuda(), masked=masked)
+        out = np.zeros(lev.n)
+        out[perm] = y.cpu().numpy()
+        if masked:   # y_F = A_FF u_F, y_D = u_D
+            F = lev.free
+            assert rel(out[F], lev.A[F][:, F] @ u[F]) <= APPLY_TOL
+            np.testing.assert_array_equal(out[lev.dirichlet], u[lev.dirichlet])
+        else:
+            assert rel(out, lev.A @ u) <= APPLY_TOL
+    s.close()
 
 
 @functools.lru_cache(maxsize=None)

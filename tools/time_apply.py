@@ -26,7 +26,7 @@ else:
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 nodes = m.node_xyz(lib.reference_nodes(m.p))
-VARIANTS = {0: "warp-dmma", 1: "fma", 2: "batched-dmma"}
+VARIANTS = {0: "default", 1: "fma", 2: "batched-dmma", 3: "quad", 4: "quad-split"}
 for variant in [int(v) for v in os.environ.get("VARIANTS", "0,2").split(",")]:
     kw = dict(apply_kernel=variant, local_solve=1)
     if a.levels:
