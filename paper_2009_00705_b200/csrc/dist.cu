@@ -23,7 +23,9 @@
 // elements touching an exchanged node (interface) are applied first, their partial
 // sums packed and sent on a communication stream, and the interior elements -- which
 // touch no exchanged node -- are applied on the compute stream while the transfer is
-// in flight; the received sums are added after both.  SEM_DIST_OVERLAP=0 turns it off.
+// in flight; the received sums are added after both.  Dense Schwarz sweeps and FDM
+// sweeps split the same way over subdomains / column units.  On by default for the NCCL
+// transport, off for emulated ranks (SEM_DIST_OVERLAP, see dist_setup).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -131,6 +133,7 @@ struct Dist {
   double* hsum = nullptr;        // pinned host [32] (emulated all-reduce)
   // overlap of operator applies with their exchange (apply_exchange)
   bool overlap = true;
+  int fdm_ov_min = 0;            // least interface FDM units per part for the split sweep
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_xfer = nullptr;
   // PCG's z = V(r) on fixed buffers (r = bw, z = pw / zw of every part) replayed from a CUDA
@@ -291,10 +294,31 @@ static void residual(Dist& D, int li, const Vecs& f, const Vecs& u, const Vecs& 
 // apply_exchange: interface subdomains, pack, [transfer || interior subdomains], unpack-add.
 static void schwarz_update(Dist& D, int li, const Vecs& r, const Vecs& u, int transpose) {
   Vecs d = lvec(D, li, &DeviceLevel::d);
-  bool ov = D.overlap;
-  for (auto* c : D.parts) ov = ov && c->L[li].s_if && !c->L[li].fdm && !c->det.on;
+  bool ov = D.overlap, fov = D.overlap;
+  for (auto* c : D.parts) {
+    ov = ov && c->L[li].s_if && !c->L[li].fdm && !c->det.on;
+    fov = fov && c->L[li].fdm && c->L[li].fu_if && !c->det.on && c->L[li].nfu_if >= D.fdm_ov_min;
+  }
   each(D, [&](sem_ctx* c, int i) { CUDA_CHECK(cudaMemsetAsync(d[i], 0, sizeof(double) * c->L[li].n, c->stream)); });
-  if (!ov) {
+  if (fov) {  // FDM level: interface column units (+ the whole O35 dense subset), then the rest
+    sem_ctx* c0 = D.parts[0];
+    each(D, [&](sem_ctx* c, int i) {
+      const DeviceLevel& L = c->L[li];
+      if (!launch_fdm_list(c, li, r[i], d[i], transpose, L.fu_if, L.nfu_if)) throw SemError(SEM_ECUDA, "fdm");
+      if (L.nsub) launch_schwarz_dense(c, li, r[i], d[i], transpose);
+    });
+    pack_all(D, li, d);
+    CUDA_CHECK(cudaEventRecord(D.ev_pack, c0->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(D.comm_stream, D.ev_pack, 0));
+    transfer(D, li, D.comm_stream);
+    CUDA_CHECK(cudaEventRecord(D.ev_xfer, D.comm_stream));
+    each(D, [&](sem_ctx* c, int i) {
+      const DeviceLevel& L = c->L[li];
+      if (!launch_fdm_list(c, li, r[i], d[i], transpose, L.fu_in, L.nfu_in)) throw SemError(SEM_ECUDA, "fdm");
+    });
+    CUDA_CHECK(cudaStreamWaitEvent(c0->stream, D.ev_xfer, 0));
+    unpack_all(D, li, d);
+  } else if (!ov) {
     each(D, [&](sem_ctx* c, int i) { launch_schwarz(c, li, r[i], d[i], transpose); });
     exchange(D, li, d);
   } else {
@@ -606,6 +630,32 @@ static void setup_exchange(sem_ctx* c, const LocalPart& P) {
       L.s_if = upload(c, sif);
       L.s_in = upload(c, sin);
     }
+    // FDM level on the column-unit kernels: a unit is on the interface if any node of its column
+    // range (the nodes its scatter writes) is exchanged
+    const int fk = li + 1 < c->L.size() ? fdm_kernel_choice(L) : SEM_SMOOTHER_DENSE;
+    if (L.fdm && li < P.F.size() &&
+        (fk == SEM_SMOOTHER_FDM_WARP1 || fk == SEM_SMOOTHER_FDM_WARP2 || fk == SEM_SMOOTHER_FDM_CTA)) {
+      const FdmTopo& F = P.F[li];
+      std::vector<int4> hu(L.f_nunits);
+      CUDA_CHECK(cudaMemcpy(hu.data(), L.f_units, hu.size() * sizeof(int4), cudaMemcpyDeviceToHost));
+      std::vector<int32_t> uif, uin;
+      for (int i = 0; i < L.f_nunits; ++i) {
+        const int q = hu[i].x, e0 = F.colel[hu[i].y], e1 = F.colel[hu[i].y + hu[i].z - 1];
+        const int nh = (int)(F.hoff[q + 1] - F.hoff[q]), nz = F.nzc[q];
+        const int zlo = F.z0[e0], zhi = F.z0[e1] + F.nv[e1];
+        bool s = false;
+        for (int h = 0; h < nh && !s; ++h)
+          for (int z = zlo; z < zhi && !s; ++z) {
+            const int32_t g = F.cidx[F.cioff[q] + (int64_t)h * nz + z];
+            s = g >= 0 && shared[g] != 0;
+          }
+        (s ? uif : uin).push_back(i);
+      }
+      L.nfu_if = (int)uif.size();
+      L.nfu_in = (int)uin.size();
+      L.fu_if = upload(c, uif.empty() ? std::vector<int32_t>{0} : uif);
+      L.fu_in = upload(c, uin.empty() ? std::vector<int32_t>{0} : uin);
+    }
   }
 }
 
@@ -759,8 +809,18 @@ void setup_distributed(sem_ctx* c, GlobalModel& gm) {
   D->cz = dalloc<double>(c, D->gn.back());
   CUDA_CHECK(cudaMallocHost(&D->hsum, 32 * sizeof(double)));
   {
+    // SEM_DIST_OVERLAP: unset = on for the NCCL transport, off for emulated ranks (one GPU runs
+    // them one after another: there is no transfer to hide, only the split launches' tails);
+    // 0 = off; 1 = on; 2 = on with every FDM sweep split (below)
     const char* ov = getenv("SEM_DIST_OVERLAP");
-    D->overlap = !(ov && atoi(ov) == 0);
+    D->overlap = ov ? atoi(ov) != 0 : !D->emulated;
+    // FDM sweeps are split only when the interface units fill a few waves of the GPU by
+    // themselves: a small interface launch under-fills the SMs and the split sweep loses more
+    // to wave tails than the hidden transfer saves (emulated config 3, 4 ranks: 78.6 ms serial
+    // vs 87.9 ms always split).  SEM_DIST_OVERLAP=2 splits every FDM sweep (tests).
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device >= 0 ? c->device : 0);
+    D->fdm_ov_min = (ov && atoi(ov) == 2) ? 0 : 8 * sms;
     CUDA_CHECK(cudaStreamCreateWithFlags(&D->comm_stream, cudaStreamNonBlocking));
     CUDA_CHECK(cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&D->ev_xfer, cudaEventDisableTiming));

@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
                                                   const double* __restrict__ lvp, const double* __restrict__ W,
                                                   const double* __restrict__ r, double* __restrict__ u, int transpose,
                                                   int ldr, const uint8_t* __restrict__ skip, int nph,
-                                                  const int* __restrict__ udesc) {
+                                                  const int* __restrict__ udesc, const int* __restrict__ ulist) {
   constexpr int ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
   extern __shared__ __align__(16) double sm[];
   double* Ss = sm;                  // [ROWS][LDS]  S_h (row i node, col a mode), zero padded
@@ -606,7 +606,8 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
   // [10..17] element ids, [18..25] z0, [26..33] n_v
   __shared__ int ud[FDM_UD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < FDM_UD) ud[tid] = __ldg(udesc + (size_t)blockIdx.x * FDM_UD + tid);
+  const int ub = ulist ? __ldg(ulist + blockIdx.x) : (int)blockIdx.x;   // unit (or the listed subset's)
+  if (tid < FDM_UD) ud[tid] = __ldg(udesc + (size_t)ub * FDM_UD + tid);
   __syncthreads();
   const int c = ud[0], cnt = ud[1], nh = ud[2], nz = ud[3];
   const int64_t mo = (int64_t)(uint32_t)ud[4] | ((int64_t)ud[5] << 32);
@@ -875,7 +876,7 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
                                                    const double* __restrict__ lvp, const double* __restrict__ W,
                                                    const double* __restrict__ r, double* __restrict__ u, int transpose,
                                                    int ldb, const uint8_t* __restrict__ skip,
-                                                   const int* __restrict__ udesc) {
+                                                   const int* __restrict__ udesc, const int* __restrict__ ulist) {
   constexpr int NVT = 2, ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
   extern __shared__ __align__(16) double sm[];
   double* Ss = sm;                  // [ROWS][LDS]  S_h (row i node, col a mode), zero padded
@@ -885,7 +886,8 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   __shared__ int soff[9];
   __shared__ int sk[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, r4 = lane >> 2, c4 = lane & 3;
-  if (tid < FDM_UD) ud[tid] = __ldg(udesc + (size_t)blockIdx.x * FDM_UD + tid);
+  const int ub = ulist ? __ldg(ulist + blockIdx.x) : (int)blockIdx.x;   // unit (or the listed subset's)
+  if (tid < FDM_UD) ud[tid] = __ldg(udesc + (size_t)ub * FDM_UD + tid);
   __syncthreads();
   const int cnt = ud[1], nh = ud[2], nz = ud[3];
   const int64_t mo = (int64_t)(uint32_t)ud[4] | ((int64_t)ud[5] << 32);
@@ -1079,14 +1081,17 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
 }
 
 template <int MT>
-static void fdm_cta_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
+static void fdm_cta_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose,
+                           const int* ulist = nullptr, int nu = -1) {
   const int ldz0 = 8 * L.f_nv_max, ldz = ldz0 + ((4 - ldz0 % 8) + 8) % 8;
   const int ldb = std::max(L.f_ldr, ldz);
   const int smem = (8 * MT * (8 * MT + 4) + 2 * 8 * MT * ldb) * (int)sizeof(double);
   static int attr[kMaxDev] = {0};
   smem_opt_in(k_fdm_cta<MT>, smem, attr);
-  k_fdm_cta<MT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_cidx, L.f_Sh, L.f_lh, L.f_Svp, L.f_lvp, L.W, r, u,
-                                                       transpose, ldb, L.f_skip, L.f_udesc);
+  const int nb = ulist ? nu : L.f_nunits;
+  if (nb == 0) return;
+  k_fdm_cta<MT><<<nb, 256, smem, c->stream>>>(L.f_cidx, L.f_Sh, L.f_lh, L.f_Svp, L.f_lvp, L.W, r, u, transpose, ldb,
+                                              L.f_skip, L.f_udesc, ulist);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -1100,28 +1105,31 @@ static bool fdm_cta_enabled() {
 }
 
 template <int MT, int NVT>
-static void fdm_warp_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
+static void fdm_warp_launch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose,
+                            const int* ulist, int nu) {
   const int smem = (8 * MT * (8 * MT + 4) + 8 * MT * L.f_ldr) * (int)sizeof(double);
   static int attr[kMaxDev] = {0};
   smem_opt_in(k_fdm_warp<MT, NVT>, smem, attr);
-  k_fdm_warp<MT, NVT><<<L.f_nunits, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff,
-                                                             L.f_nzc, L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh,
-                                                             L.f_Svp, L.f_lvp, L.W, r, u, transpose, L.f_ldr,
-                                                             L.f_skip, L.f_nph, L.f_udesc);
+  const int nb = ulist ? nu : L.f_nunits;
+  if (nb == 0) return;
+  k_fdm_warp<MT, NVT><<<nb, 256, smem, c->stream>>>(L.f_units, L.f_colel, L.f_hoff, L.f_moff, L.f_cioff, L.f_nzc,
+                                                     L.f_cidx, L.f_z0, L.f_nv, L.f_Sh, L.f_lh, L.f_Svp, L.f_lvp, L.W,
+                                                     r, u, transpose, L.f_ldr, L.f_skip, L.f_nph, L.f_udesc, ulist);
   CUDA_CHECK(cudaGetLastError());
 }
 
 template <int NVT>
-static void fdm_warp_dispatch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose) {
+static void fdm_warp_dispatch(sem_ctx* c, const DeviceLevel& L, const double* r, double* u, int transpose,
+                              const int* ulist = nullptr, int nu = -1) {
   switch (L.f_mt) {
-    case 1: fdm_warp_launch<1, NVT>(c, L, r, u, transpose); break;
-    case 2: fdm_warp_launch<2, NVT>(c, L, r, u, transpose); break;
-    case 3: fdm_warp_launch<3, NVT>(c, L, r, u, transpose); break;
-    case 4: fdm_warp_launch<4, NVT>(c, L, r, u, transpose); break;
-    case 5: fdm_warp_launch<5, NVT>(c, L, r, u, transpose); break;
-    case 6: fdm_warp_launch<6, NVT>(c, L, r, u, transpose); break;
-    case 7: fdm_warp_launch<7, NVT>(c, L, r, u, transpose); break;
-    default: fdm_warp_launch<8, NVT>(c, L, r, u, transpose); break;
+    case 1: fdm_warp_launch<1, NVT>(c, L, r, u, transpose, ulist, nu); break;
+    case 2: fdm_warp_launch<2, NVT>(c, L, r, u, transpose, ulist, nu); break;
+    case 3: fdm_warp_launch<3, NVT>(c, L, r, u, transpose, ulist, nu); break;
+    case 4: fdm_warp_launch<4, NVT>(c, L, r, u, transpose, ulist, nu); break;
+    case 5: fdm_warp_launch<5, NVT>(c, L, r, u, transpose, ulist, nu); break;
+    case 6: fdm_warp_launch<6, NVT>(c, L, r, u, transpose, ulist, nu); break;
+    case 7: fdm_warp_launch<7, NVT>(c, L, r, u, transpose, ulist, nu); break;
+    default: fdm_warp_launch<8, NVT>(c, L, r, u, transpose, ulist, nu); break;
   }
 }
 
@@ -1183,6 +1191,25 @@ int fdm_kernel_choice(const DeviceLevel& L) {
   }
   if (!fdm_simple() && L.f_mt <= 16 && L.f_nvt <= 3) return SEM_SMOOTHER_FDM_COL;
   return SEM_SMOOTHER_FDM_GENERIC;
+}
+
+// FDM sweep over a subset of the column units (dist.cu: interface units first, the rest while the
+// exchange is in flight); the column-unit kernels only, false for the others
+bool launch_fdm_list(sem_ctx* c, int level, const double* r, double* u, int transpose, const int* ulist, int nu) {
+  const DeviceLevel& L = c->L[level];
+  const int kind = fdm_kernel_choice(L);
+  if (kind == SEM_SMOOTHER_FDM_WARP1) fdm_warp_dispatch<1>(c, L, r, u, transpose, ulist, nu);
+  else if (kind == SEM_SMOOTHER_FDM_WARP2) fdm_warp_dispatch<2>(c, L, r, u, transpose, ulist, nu);
+  else if (kind == SEM_SMOOTHER_FDM_CTA) {
+    switch (L.f_mt) {
+      case 5: fdm_cta_launch<5>(c, L, r, u, transpose, ulist, nu); break;
+      case 6: fdm_cta_launch<6>(c, L, r, u, transpose, ulist, nu); break;
+      case 7: fdm_cta_launch<7>(c, L, r, u, transpose, ulist, nu); break;
+      default: fdm_cta_launch<8>(c, L, r, u, transpose, ulist, nu); break;
+    }
+  } else return false;
+  c->launches++;
+  return true;
 }
 
 void launch_fdm(sem_ctx* c, int level, const double* r, double* u, int transpose) {

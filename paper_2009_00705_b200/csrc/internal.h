@@ -141,6 +141,8 @@ struct DeviceLevel {
   int n_if = 0, n_in = 0;
   int32_t *s_if = nullptr, *s_in = nullptr;   // the same split of the owned (dense) Schwarz subdomains
   int ns_if = 0, ns_in = 0;
+  int32_t *fu_if = nullptr, *fu_in = nullptr;  // the same split of the FDM column units (column-unit kernels)
+  int nfu_if = 0, nfu_in = 0;
 };
 
 // deterministic mode (opts.deterministic): colour-ordered gather-scatter and
@@ -251,6 +253,8 @@ bool launch_apply_warp(sem_ctx* c, int level, const double* u, double* y, int fl
 std::vector<double> quad_apply_mats(const LevelRef& R);
 bool launch_apply_quad(sem_ctx* c, int level, const double* u, double* y, int flags);
 void build_g_tiles(sem_ctx* c, int level);
+void launch_schwarz_dense(sem_ctx* c, int level, const double* r, double* u, int transpose);
+bool launch_fdm_list(sem_ctx* c, int level, const double* r, double* u, int transpose, const int* ulist, int nu);
 bool launch_apply_subset(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne);
 bool launch_apply_qs(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne);
 void build_p1_matrices(sem_ctx* c, int level, const double* d_D);

@@ -590,6 +590,13 @@ void launch_schwarz(sem_ctx* c, int level, const double* r, double* u, int trans
     launch_fdm(c, level, r, u, transpose);
     if (L.nsub == 0) return;  // else: the dense subdomains of an O35 hybrid follow
   }
+  launch_schwarz_dense(c, level, r, u, transpose);
+}
+
+// the dense (exact local inverse) subdomains of a level: all of them, or the O35 subset of an
+// FDM level
+void launch_schwarz_dense(sem_ctx* c, int level, const double* r, double* u, int transpose) {
+  const DeviceLevel& L = c->L[level];
   const int npad = 16 * L.max_tiles_1d;
   const int smem = 9 * npad * (int)sizeof(double);
   static int attr_set[kMaxDev] = {0}, attr_set32[kMaxDev] = {0};

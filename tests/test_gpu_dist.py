@@ -38,9 +38,19 @@ def pair(request):
     return m, mk(m)
 
 
+@pytest.fixture(autouse=True)
+def _overlap_forced(monkeypatch):
+    """Every partitioned ctx of this module splits its applies and sweeps into interface /
+    interior parts with the exchange in flight (the NCCL default; emulated ranks default to the
+    serial path, which has no transfer to hide).  SEM_DIST_OVERLAP is read at setup."""
+    monkeypatch.setenv("SEM_DIST_OVERLAP", "2")
+
+
+@pytest.mark.parametrize("overlap", ["2", "0"])
 @pytest.mark.parametrize("nranks", [2, 3, 4])
-def test_partitioned_matches_single_domain(pair, nranks):
+def test_partitioned_matches_single_domain(pair, nranks, overlap, monkeypatch):
     m, s1 = pair
+    monkeypatch.setenv("SEM_DIST_OVERLAP", overlap)
     sd = mk(m, nranks=nranks)
     assert sd.info["n_dof"] == s1.info["n_dof"] and sd.info["level_p"] == s1.info["level_p"]
     np.testing.assert_array_equal(sd.node_xyz(0), s1.node_xyz(0))
@@ -89,9 +99,11 @@ FDM_MESHES = {
 
 @pytest.mark.parametrize("name", list(FDM_MESHES))
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_partitioned_fdm_matches_single_domain(name, nranks):
+def test_partitioned_fdm_matches_single_domain(name, nranks, monkeypatch):
     """Partitioned FDM / exact-dense hybrid (O33, O35): smoother sweep, V-cycle and
-    solve equal the single-domain FDM solver (hull replica included)."""
+    solve equal the single-domain FDM solver (hull replica included).  Every FDM sweep
+    split into interface / interior column units (SEM_DIST_OVERLAP=2)."""
+    monkeypatch.setenv("SEM_DIST_OVERLAP", "2")
     m = FDM_MESHES[name]()
     s1 = mk(m, local_solve=1)
     sd = mk(m, local_solve=1, nranks=nranks)
@@ -107,6 +119,25 @@ def test_partitioned_fdm_matches_single_domain(name, nranks):
     pd, rd = sd.solve(phiD, 1e-12)
     assert rd["converged"] and abs(rd["iters"] - r1["iters"]) <= 1
     assert rel(pd.cpu().numpy(), p1.cpu().numpy()) <= 1e-10
+    sd.close()
+    s1.close()
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_partitioned_fdm_cta_overlap(nranks, monkeypatch):
+    """p = 6 Delaunay basin whose level-0 sweep runs k_fdm_cta<8>: the partitioned sweep
+    (interface column units, exchange in flight, interior units; FDM unit lists) and the
+    V-cycle equal the single domain."""
+    from workloads.configs import delaunay_basin
+    monkeypatch.setenv("SEM_DIST_OVERLAP", "2")
+    m = delaunay_basin("fdm_cta8", 6, n_in=16, nz=3, seed=1)
+    s1 = mk(m, local_solve=1)
+    assert s1.info["smoother_kernel"][0] == "k_fdm_cta<MT>"
+    sd = mk(m, local_solve=1, nranks=nranks)
+    n = s1.info["n_dof"]
+    mask = torch.from_numpy(s1.dirichlet_mask(0)).cuda()
+    r = torch.from_numpy(random_vector(n, seed=7)).cuda().masked_fill(mask, 0.0)
+    assert rel(sd.vcycle(r).cpu().numpy(), s1.vcycle(r).cpu().numpy()) <= 1e-12
     sd.close()
     s1.close()
 
