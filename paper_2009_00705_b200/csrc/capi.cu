@@ -682,6 +682,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
 }
 
 void do_setup(const sem_mesh* mesh, int p, const sem_opts* opts, sem_ctx* c) {
+  NvtxRange nv("sem_setup");
   const double t_start = now_ms();
   if (opts) c->opts = *opts;
   else sem_default_opts(&c->opts);
@@ -738,6 +739,7 @@ void coarse_solve(sem_ctx* c, const double* f, double* u) {
 
 // ------------------------------------------------------------------ V-cycle (Alg 4.1)
 void vcycle(sem_ctx* c, int li, const double* f, double* u) {
+  NvtxRange nv(nvtx_level_name(li));
   const int nl = (int)c->L.size();
   if (li == nl - 1) {  // coarsest: exact solve (O10, O26)
     coarse_solve(c, f, u);
@@ -825,6 +827,7 @@ void read_scalars(sem_ctx* c, int n) {
 // ------------------------------------------------------------------ solve
 int do_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep,
              int guess = 0, int cond = 0) {
+  NvtxRange nv(cond ? "laplace_solve_condensed" : "laplace_solve");
   if (!phiD || !phi) throw SemError(SEM_EINVAL, "dirichlet_phi and phi are required");
   if (!(tol >= 0.0)) throw SemError(SEM_EINVAL, "tol must be >= 0");
   DeviceLevel& L = c->L[0];

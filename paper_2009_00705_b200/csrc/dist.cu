@@ -863,6 +863,7 @@ static void gather_global(Dist& D, int li, const Vecs& l, double* g) {
 }
 
 int dist_solve(sem_ctx* c, const double* rhs, const double* phiD, double tol, double* phi, sem_report* rep) {
+  NvtxRange nv("laplace_solve (partitioned)");
   Dist& D = *c->dist;
   Vecs vr = scatter_global(D, 0, rhs, &sem_ctx::host_in2);
   Vecs vd = scatter_global(D, 0, phiD, &sem_ctx::host_in);

@@ -627,21 +627,21 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
   (void)nzc;
   (void)z0;
   (void)nvv;
-  {  // S_h -> shared (all loads in flight before the stores)
+  {  // S_h -> shared by cp.async (zero-filled padding), in flight during the column-block gather
     constexpr int IS = (ROWS * ROWS + 255) / 256;
-    double tmp[IS];
 #pragma unroll
     for (int k = 0; k < IS; ++k) {
       const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
-      tmp[k] = (t < ROWS * ROWS && i < nh && a < nh) ? __ldg(S + i * nh + a) : 0.0;
+      if (t < ROWS * ROWS) {
+        const bool v = i < nh && a < nh;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(Ss + i * LDS + a))),
+                     "l"(S + (v ? i * nh + a : 0)), "r"(v ? 8 : 0)
+                     : "memory");
+      }
     }
-#pragma unroll
-    for (int k = 0; k < IS; ++k) {
-      const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
-      if (t < ROWS * ROWS) Ss[i * LDS + a] = tmp[k];
-    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  __syncthreads();
   const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
   // column block gather in batches of 8 items per thread: node ids, values (x W), stores
   for (int base = 0; base < ROWS * ldr; base += 256 * 8) {
@@ -665,6 +665,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
       if (t < ROWS * ldr) Rc[t] = val[k];
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const bool active = warp < cnt && !skip[eid[warp < cnt ? warp : 0]];
   const int j = warp < cnt ? warp : 0;
@@ -916,19 +917,21 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     const int t = tid + 256 * k, h = t / nzu, zz = t - h * nzu;
     gid0[k] = t < nval ? __ldg(ci + h * nz + zlo + zz) : -1;
   }
-  {  // S_h -> shared
+  {  // S_h -> shared by cp.async (zero-filled padding), completed with the column block below:
+     // the S_h bytes stream in while the gather's dependent loads are in flight
     constexpr int IS = (ROWS * ROWS + 255) / 256;
-    double tmp[IS];
 #pragma unroll
     for (int k = 0; k < IS; ++k) {
       const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
-      tmp[k] = (t < ROWS * ROWS && i < nh && a < nh) ? __ldg(S + i * nh + a) : 0.0;
+      if (t < ROWS * ROWS) {
+        const bool v = i < nh && a < nh;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(Ss + i * LDS + a))),
+                     "l"(S + (v ? i * nh + a : 0)), "r"(v ? 8 : 0)
+                     : "memory");
+      }
     }
-#pragma unroll
-    for (int k = 0; k < IS; ++k) {
-      const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
-      if (t < ROWS * ROWS) Ss[i * LDS + a] = tmp[k];
-    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   // per-box vertical modes of warp j, loaded before step 1 (latency hidden behind it)
   double s1[4][2], s2[4][2], lvv[2][2], lav[MT];
@@ -974,6 +977,7 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
       if (pos[k] >= 0) B1[pos[k]] = val[k];
   }
   for (int t = nh * ldb + tid; t < ROWS * ldb; t += 256) B1[t] = 0.0;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // 1. Tall = S_h^T Rc -> B2
   const int mtu = (nh + 7) / 8;

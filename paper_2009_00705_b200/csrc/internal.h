@@ -1,6 +1,7 @@
 // Internal structures of the C-ABI library (not installed).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -42,6 +43,22 @@ struct DeviceGuard {
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
+
+// NVTX range for the timeline of nsys / ncu (--nvtx): header-only nvtx3, no-ops unless a tool
+// injects itself (SURVEY §5 tracing).  Host-side only: kernels replayed from CUDA graphs carry
+// the range of the call that launched the graph.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+inline const char* nvtx_level_name(int li) {
+  static const char* names[] = {"V-cycle level 0", "V-cycle level 1", "V-cycle level 2", "V-cycle level 3",
+                                "V-cycle level 4", "V-cycle level 5", "V-cycle level 6", "V-cycle level 7",
+                                "V-cycle level 8"};
+  return (li >= 0 && li < 9) ? names[li] : "V-cycle level";
+}
 
 inline int cur_device() {
   int d = 0;
