@@ -373,6 +373,15 @@ def sweep_one(args, p, variant):
     s = lib.Solver(m.vertices, m.prisms, m.face_tag, p, node_xyz=nodes, **(extra if p > 1 else {}))
     setup_s = time.perf_counter() - t0
     del nodes
+    apply = None
+    if variant == SWEEP[0][0]:  # the finest operator apply of this p (the same kernel for every variant)
+        us_a, b_a = s.bench_kernel("apply", 0, 20)
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        pk = json.load(open(peaks_path))["hbm_gbs"] if os.path.exists(peaks_path) else 6470.8
+        kern = ("k_apply_em<%d>" % (6 if p == 1 else 18)) if p <= 2 else (
+            "k_apply_qs<%d>" % p if p <= 5 else ("k_apply_warp<6>" if p == 6 else "k_apply_dmma<%d>" % p))
+        apply = {"kernel": kern, "us": us_a, "alg_bytes_per_launch": b_a,
+                 "achieved_GBs": b_a / (us_a * 1e-6) / 1e9, "frac": b_a / (us_a * 1e-6) / 1e9 / pk}
     xyz = s.node_xyz(0)
     phiD = torch.from_numpy(m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])).cuda()
     phi = s.empty(0)
@@ -396,6 +405,8 @@ def sweep_one(args, p, variant):
            "MDOF_s": i["n_free"] / (ms * 1e-3) / 1e6, "setup_s": setup_s, "device_GB": i["device_bytes"] / 1e9,
            "smoother_kernels": i["smoother_kernel"],
            "solve_roofline": solve_roofline(s, rep, ms, peak) if p > 1 else None}
+    if apply:
+        out["apply"] = apply
     if p >= 3:  # the same solve on the statically condensed system (NEXT-3): same ctx, same stop test
         out["condensed"] = timed_condensed(args, s, phiD, phi)
     print("SWEEP " + json.dumps(out), flush=True)

@@ -983,6 +983,15 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   const int mtu = (nh + 7) / 8;
   fdm_cta_gemm<MT, true>(Ss, B1, B2, ldb, nzu, warp, lane, mtu);
   __syncthreads();
+  // the scatter's first chunk (step 4): node ids now, weights before step 3, both in flight
+  // behind the vertical step and the second GEMM (the same (h, z) <- t map as the gather)
+  const int ntot = nh * nzu;
+  int g4[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int t = tid + 256 * k, h = t / nzu, z = t - h * nzu;
+    g4[k] = t < ntot ? __ldg(ci + h * nz + zlo + z) : -1;
+  }
   // 2. warp j: vertical transform and scaling of box j, stored compactly into Zs (B1)
   if (warp < cnt && !sk[warp]) {
     const int j = warp, zb = ez0[j] - zlo, nvj = env[j], so = soff[j];
@@ -1029,6 +1038,9 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     }
   }
   __syncthreads();
+  double w4[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w4[k] = (!transpose && g4[k] >= 0) ? __ldg(W + g4[k]) : 1.0;
   // 3. Ys = S_h Zs -> B2 over the stacked columns
   fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, soff[cnt], warp, lane, mtu);
   __syncthreads();
@@ -1053,17 +1065,21 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     zn[z] = (unsigned char)k;
   }
   __syncthreads();
-  const int ntot = nh * nzu;
   for (int base = 0; base < ntot; base += 256 * 8) {
     int g[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = base + tid + 256 * k, h = t / nzu, z = t - h * nzu;
-      g[k] = t < ntot ? __ldg(ci + h * nz + zlo + z) : -1;
-    }
     double wv[8];
+    if (base == 0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) wv[k] = (!transpose && g[k] >= 0) ? __ldg(W + g[k]) : 1.0;
+      for (int k = 0; k < 8; ++k) g[k] = g4[k], wv[k] = w4[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = base + tid + 256 * k, h = t / nzu, z = t - h * nzu;
+        g[k] = t < ntot ? __ldg(ci + h * nz + zlo + z) : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) wv[k] = (!transpose && g[k] >= 0) ? __ldg(W + g[k]) : 1.0;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (g[k] < 0) continue;
