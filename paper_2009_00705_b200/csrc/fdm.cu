@@ -688,21 +688,8 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
     // skipped tiles are exact zeros); for MT >= 5 only (the guards cost more than they save at
     // the small tile counts of p <= 3: measured on config 5's p = 2, 3 levels)
     const int mtu = MT >= 5 ? (nh + 7) / 8 : MT, ktu = 2 * mtu;
-    double T[MT][NVT][2];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll
-      for (int n = 0; n < NVT; ++n) T[mt][n][0] = T[mt][n][1] = 0.0;
-      if (mt >= mtu) continue;
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        if (kt >= ktu) break;
-        const double af = Ss[(kt * 4 + (lane & 3)) * LDS + mt * 8 + (lane >> 2)];
-#pragma unroll
-        for (int n = 0; n < NVT; ++n) fdm_dmma(T[mt][n][0], T[mt][n][1], af, b1[kt][n]);
-      }
-    }
-    // vertical: T <- ((T S_v) ./ (l_h + l_v)) S_v^T, per m-tile
+    // the element's vertical modes and the first horizontal eigenvalue: loads in flight behind
+    // the first GEMM (their latency sat on the vertical step's first use)
     const double* sv = Svp + (size_t)e * NVP * NVP;
     const double* lv = lvp + (size_t)e * NVP;
     double s1[2 * NVT][NVT], s2[2 * NVT][NVT], lvv[NVT][2];
@@ -718,6 +705,22 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
 #pragma unroll
       for (int i = 0; i < 2; ++i) lvv[n][i] = __ldg(lv + n * 8 + 2 * (lane & 3) + i);
     const double* Lh = lh + ho;
+    double la_next = (lane >> 2) < nh ? __ldg(Lh + (lane >> 2)) : 1.0;
+    double T[MT][NVT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+      for (int n = 0; n < NVT; ++n) T[mt][n][0] = T[mt][n][1] = 0.0;
+      if (mt >= mtu) continue;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        if (kt >= ktu) break;
+        const double af = Ss[(kt * 4 + (lane & 3)) * LDS + mt * 8 + (lane >> 2)];
+#pragma unroll
+        for (int n = 0; n < NVT; ++n) fdm_dmma(T[mt][n][0], T[mt][n][1], af, b1[kt][n]);
+      }
+    }
+    // vertical: T <- ((T S_v) ./ (l_h + l_v)) S_v^T, per m-tile
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       if (mt >= mtu) break;
@@ -730,8 +733,11 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
 #pragma unroll
         for (int n = 0; n < NVT; ++n) fdm_dmma(v[n][0], v[n][1], a, s1[kt][n]);
       }
-      const int ah = mt * 8 + (lane >> 2);
-      const double la = ah < nh ? __ldg(Lh + ah) : 1.0;
+      const double la = la_next;   // this tile's l_h; the next tile's load issued now
+      if (mt + 1 < MT) {
+        const int an = (mt + 1) * 8 + (lane >> 2);
+        la_next = an < nh ? __ldg(Lh + an) : 1.0;
+      }
 #pragma unroll
       for (int n = 0; n < NVT; ++n)
 #pragma unroll

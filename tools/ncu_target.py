@@ -2,6 +2,7 @@
   schwarz3        one level-0 k_schwarz<double> sweep of config 3 (exact dense ASM)
   apply3 <v>      one level-0 operator apply of config 3 with apply_kernel v
   apply <cfg> <v> one level-0 apply of config2/config3/config4p<P> with apply_kernel v
+  fdm3            one level-0 FDM sweep of config 3
   fdm5            one level-0 FDM sweep of config 5
 Prints the library's algorithmic bytes per launch (sem_bench_kernel) as JSON."""
 import json, os, sys
@@ -13,6 +14,8 @@ from workloads import config2, config3, config4  # noqa
 what = sys.argv[1]
 if what == "schwarz3":
     m, kw, kern = config3(), {}, "schwarz"
+elif what == "fdm3":
+    m, kw, kern = config3(), dict(local_solve=1), "schwarz"
 elif what == "fdm5":
     from workloads.config5 import config5
     m, kw, kern = config5(), dict(local_solve=1), "schwarz"
