@@ -237,6 +237,45 @@ def run_variants(args, lib, m, phiD_h, peak, base_kw):
     return out
 
 
+def run_aniso(args, lib, peak):
+    """SURVEY NEXT-2 at full config-3 size: the same basin with (P_xy, P_z) = (5, 3) elements and the
+    paper's Table 5.4 schedule (5,3) -> (3,3) -> (1,1), exact dense local inverses, the
+    headline's stop test; a different discretisation (fewer vertical nodes), so not the headline."""
+    import torch
+    from workloads import config3
+    m = config3()
+    m.pz = 3
+    t0 = time.perf_counter()
+    s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p, 3)), pz=3,
+                   levels=[(5, 3), (3, 3), (1, 1)])
+    setup_s = time.perf_counter() - t0
+    xyz = s.node_xyz(0)
+    phiD = torch.from_numpy(m.phi(xyz[:, 0], xyz[:, 1], xyz[:, 2])).cuda()
+    phi = s.empty(0)
+    for _ in range(args.warmup):
+        s.solve(phiD, args.tol, out=phi)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s.stream)
+    for _ in range(args.steps):
+        _, rep = s.solve(phiD, args.tol, out=phi)
+    e1.record(s.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    us_a, b_a = s.bench_kernel("apply", 0, 20)
+    out = {"name": "aniso_table5.4", "workload": "config3 basin, P_5(triangle) x P_3(t) prisms (NEXT-2)",
+           "smoother": "exact dense local inverses, levels (5,3) -> (3,3) -> (1,1) (Table 5.4)",
+           "value": s.info["n_free"] / (ms * 1e-3) / 1e6, "unit": "MDOF/s", "ms_per_step": ms,
+           "iters": rep["iters"], "vcycles": rep["vcycles"], "rel_res": rep["rel_res"], "n_dof": s.info["n_dof"],
+           "setup_s": setup_s,
+           "apply": {"kernel": "k_apply_qs<5, 3>", "us": us_a, "alg_bytes_per_launch": b_a,
+                     "achieved_GBs": b_a / (us_a * 1e-6) / 1e9, "frac": b_a / (us_a * 1e-6) / 1e9 / peak}}
+    s.close()
+    del s
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_config5(args, lib, peak):
     """BASELINE.json config 5 (52.8 M DOF, hull) on one GPU: its exact dense
     Schwarz inverses would need ~400 GB, so it runs with the FDM / exact-dense
@@ -576,6 +615,7 @@ def main():
             s.close()
             del s
             torch.cuda.empty_cache()
+            variants.append(run_aniso(args, lib, peak))
             variants.append(run_config5(args, lib, peak))
     fnpf_block = None
     if world == 1 and args.emulate_ranks <= 1 and not args.no_variants and args.config == "config3":

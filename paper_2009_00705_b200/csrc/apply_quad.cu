@@ -43,10 +43,13 @@ namespace aq {
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 }  // namespace aq
 
-template <int P>
+// P: triangle order, PZ: vertical order (anisotropic P_P x P_PZ levels of SURVEY NEXT-2; PZ = P
+// for the isotropic kernels): N1 = P + 1 triangle-edge nodes, NV = PZ + 1 vertical nodes and points
+template <int P, int PZ = P>
 struct AQ {
-  static constexpr int N1 = P + 1, NT = N1 * (N1 + 1) / 2, QT = N1 * N1, QV = N1, Q = QT * QV, N = NT * N1;
-  static constexpr int MTQ = aq::cdiv(N1, 2);   // row tiles over (q, e)
+  static constexpr int N1 = P + 1, NT = N1 * (N1 + 1) / 2, QT = N1 * N1, NV = PZ + 1, QV = NV, Q = QT * QV,
+                       N = NT * NV;
+  static constexpr int MTQ = aq::cdiv(QV, 2);   // row tiles over (q, e)
   static constexpr int KM = aq::cdiv(NT, 4);    // k-steps over triangle nodes (stage B)
   static constexpr int MTA = aq::cdiv(QT, 8);   // a-tiles
   static constexpr int NM = aq::cdiv(NT, 8);    // n-tiles over triangle nodes (stage B^T)
@@ -59,13 +62,13 @@ struct AQ {
   // 16-byte loads of the (a, a+1) pairs of a quarter-warp (two m rows x four a pairs) hit distinct banks
   static constexpr int LDA = 8 * MTA + ((8 * MTA) % 16 == 0 ? 8 : 0);
   static constexpr int BMT = 3 * 8 * NM * LDA;
-  static constexpr int BT = 2 * QV * N1;        // Bt, Dt [q][l]
+  static constexpr int BT = 2 * QV * NV;        // Bt, Dt [q][l]
   static constexpr int W = 8;                   // warps per CTA
   static constexpr int R = 2;                   // ring slots per warp
   static constexpr int TSE0 = 6 * QV * 8;       // doubles of one element's a-tile (full tile)
   static constexpr int TSE = TSE0 + 8;          // slot stride per element: = 8 mod 16 (bank spread of the 4 elements)
   static constexpr int TS = 4 * TSE;            // doubles of one slot (four elements)
-  static constexpr int NYL = aq::cdiv(N1, 2);   // vertical output nodes scattered per lane
+  static constexpr int NYL = aq::cdiv(NV, 2);   // vertical output nodes scattered per lane
   // next quad's gather staged in shared memory by cp.async: u [4][UST] (UST = 4 mod 16: the four
   // elements' rows in distinct banks) and the connectivity [4 N]
   static constexpr int UST = (N + 11) / 16 * 16 + 4;
@@ -77,8 +80,8 @@ struct AQ {
 // host: Bm [3][ROWSA][LDM] (Br, Bs, B0 at [a][m]), BmT [3][8 NM][LDA] (the same at [m][a]),
 // then Bt, Dt [q][l]
 std::vector<double> quad_apply_mats(const LevelRef& R) {
-  auto run = [&](auto tag) {
-    using D = AQ<decltype(tag)::value>;
+  auto run = [&](auto tp, auto tq) {
+    using D = AQ<decltype(tp)::value, decltype(tq)::value>;
     std::vector<double> v(D::BM + D::BMT + D::BT, 0.0);
     const double* B[3] = {R.Br.data(), R.Bs.data(), R.B0.data()};
     for (int c = 0; c < 3; ++c)
@@ -87,18 +90,20 @@ std::vector<double> quad_apply_mats(const LevelRef& R) {
           v[(c * D::ROWSA + a) * D::LDM + m] = B[c][a * D::NT + m];
           v[D::BM + (c * 8 * D::NM + m) * D::LDA + a] = B[c][a * D::NT + m];
         }
-    for (int i = 0; i < D::QV * D::N1; ++i) {
+    for (int i = 0; i < D::QV * D::NV; ++i) {
       v[D::BM + D::BMT + i] = R.Bt[i];
-      v[D::BM + D::BMT + D::QV * D::N1 + i] = R.Dt[i];
+      v[D::BM + D::BMT + D::QV * D::NV + i] = R.Dt[i];
     }
     return v;
   };
-  switch (R.p) {
-    case 3: return run(std::integral_constant<int, 3>{});
-    case 4: return run(std::integral_constant<int, 4>{});
-    case 5: return run(std::integral_constant<int, 5>{});
-    case 6: return run(std::integral_constant<int, 6>{});
-  }
+  using std::integral_constant;
+#define AQ_CASE(P_, Q_) \
+  if (R.p == P_ && R.q == Q_) return run(integral_constant<int, P_>{}, integral_constant<int, Q_>{});
+  AQ_CASE(3, 3) AQ_CASE(4, 4) AQ_CASE(5, 5) AQ_CASE(6, 6)
+  AQ_CASE(3, 1) AQ_CASE(3, 2) AQ_CASE(3, 4) AQ_CASE(3, 5)
+  AQ_CASE(4, 1) AQ_CASE(4, 2) AQ_CASE(4, 3) AQ_CASE(4, 5)
+  AQ_CASE(5, 1) AQ_CASE(5, 2) AQ_CASE(5, 3) AQ_CASE(5, 4)
+#undef AQ_CASE
   return {};
 }
 
@@ -444,13 +449,11 @@ bool launch_apply_quad(sem_ctx* c, int level, const double* u, double* y, int fl
 //     per-warp shared buffer; after a group barrier the group sums the MTQ partials in a fixed
 //     order and scatters with FP64 atomics, element-major (coalesced connectivity reads).
 // Group barriers are named barriers (bar.sync 1 + group, 32 MTQ threads).
-template <int P>
+template <int P, int PZ = P>
 struct AS {
-  using B = AQ<P>;
-  static constexpr int N1 = B::N1, NT = B::NT, QT = B::QT, QV = B::QV, Q = B::Q, N = B::N;
+  using B = AQ<P, PZ>;
+  static constexpr int N1 = B::N1, NV = B::NV, NT = B::NT, QT = B::QT, QV = B::QV, Q = B::Q, N = B::N;
   static constexpr int MW = B::MTQ;             // warps per quad group (row tiles)
-  static constexpr int NG = P == 3 ? 8 : P == 6 ? 3 : 5;   // groups per CTA
-  static constexpr int W = MW * NG;
   static constexpr int R = 2;
   static constexpr int KM = B::KM, MTA = B::MTA, NM = B::NM, NALAST = B::NALAST, QE = B::QE, LDA = B::LDA;
   static constexpr int TSE = B::TSE, TS = B::TS, UST = B::UST, NYL = B::NYL;
@@ -464,6 +467,12 @@ struct AS {
   static constexpr int SU = 4 * UST, SY = MW * 4 * N, SC = 4 * N;
   static constexpr int NGQ = (4 * N + 32 * MW - 1) / (32 * MW);   // scatter entries per thread
   static constexpr int GD = R * TS + SU + SY;   // doubles per group
+  // groups per CTA: measured for the isotropic orders; anisotropic levels take as many as fit in
+  // 227 KB of shared memory and 16 warps (<= 128 registers per thread)
+  static constexpr int GB = GD * 8 + SC * 4 + 2 * R * 8;
+  static constexpr int NGS = (227 * 1024 - (BMT + BT) * 8) / GB, NGW = 16 / MW;
+  static constexpr int NG = P == PZ ? (P == 3 ? 8 : P == 6 ? 3 : 5) : (NGS < NGW ? (NGS < 8 ? NGS : 8) : (NGW < 8 ? NGW : 8));
+  static constexpr int W = MW * NG;
   static constexpr int SMEM = (BMT + BT + NG * GD) * 8 + NG * SC * 4 + NG * 2 * R * 8;
   static_assert(LDB % 16 == 8 && LDB >= 8 * MTA + 4, "qs operand layout");
   static_assert(SMEM <= 227 * 1024, "apply_qs shared memory");
@@ -482,16 +491,16 @@ __device__ __forceinline__ void qs_wait(uint32_t mb, uint32_t par) {
         : "memory");
 }
 
-template <int P>
-__global__ void __launch_bounds__(32 * AS<P>::W, 1)
+template <int P, int PZ>
+__global__ void __launch_bounds__(32 * AS<P, PZ>::W, 1)
     k_apply_qs(int E, const int32_t* __restrict__ conn, const double* __restrict__ Gw,
                const double* __restrict__ mats, const double* __restrict__ u, double* __restrict__ y, int flags,
                const int32_t* __restrict__ elist) {
-  using D = AS<P>;
+  using D = AS<P, PZ>;
   extern __shared__ __align__(128) double sm[];
   double* BmT = sm;
   double* sBt = BmT + D::BMT;
-  double* sDt = sBt + D::QV * D::N1;
+  double* sDt = sBt + D::QV * D::NV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp / D::MW, mt = warp % D::MW, gt = tid - grp * 32 * D::MW;
   const int r4 = lane >> 2, c4 = lane & 3, el = r4 & 3, h = r4 >> 2, q = 2 * mt + h;
@@ -508,7 +517,7 @@ __global__ void __launch_bounds__(32 * AS<P>::W, 1)
       const int c = i / CW, m = (i - c * CW) / RW, a = i - c * CW - m * RW;
       sm[c * D::CSB + m * D::LDB + 4 * ((m >> 1) & 1) + a] = __ldg(mats + D::BM + (c * 8 * D::NM + m) * D::LDA + a);
     }
-    for (int i = tid; i < D::BT; i += 32 * D::W) sBt[i] = __ldg(mats + D::BM + AQ<P>::BMT + i);
+    for (int i = tid; i < D::BT; i += 32 * D::W) sBt[i] = __ldg(mats + D::BM + AQ<P, PZ>::BMT + i);
   }
   if (gt == 0) {
     for (int b = 0; b < D::R; ++b) {
@@ -594,8 +603,8 @@ __global__ void __launch_bounds__(32 * AS<P>::W, 1)
     for (int ks = 0; ks < D::KM; ++ks) Ua[ks] = Ud[ks] = 0.0;
     if (q < D::QV) {
 #pragma unroll
-      for (int l = 0; l < D::N1; ++l) {
-        const double bt = sBt[q * D::N1 + l], dt = sDt[q * D::N1 + l];
+      for (int l = 0; l < D::NV; ++l) {
+        const double bt = sBt[q * D::NV + l], dt = sDt[q * D::NV + l];
 #pragma unroll
         for (int ks = 0; ks < D::KM; ++ks) {
           const int m = 4 * ks + c4;
@@ -699,8 +708,8 @@ __global__ void __launch_bounds__(32 * AS<P>::W, 1)
     // ---- stage A^T (FMA): partial y of this warp's two q values -> yb[mt]
     double* ybw = yb + mt * 4 * D::N + el * D::N;
 #pragma unroll
-    for (int l = 0; l < D::N1; ++l) {
-      const double bt = q < D::QV ? sBt[q * D::N1 + l] : 0.0, dt = q < D::QV ? sDt[q * D::N1 + l] : 0.0;
+    for (int l = 0; l < D::NV; ++l) {
+      const double bt = q < D::QV ? sBt[q * D::NV + l] : 0.0, dt = q < D::QV ? sDt[q * D::NV + l] : 0.0;
       double yl[D::NM][2];
 #pragma unroll
       for (int nm = 0; nm < D::NM; ++nm)
@@ -734,18 +743,18 @@ __global__ void __launch_bounds__(32 * AS<P>::W, 1)
   }
 }
 
-template <int P>
+template <int P, int PZ>
 static void apply_qs_P(sem_ctx* c, const DeviceLevel& L, const double* u, double* y, int flags,
                        const int32_t* elist, int ne) {
-  using D = AS<P>;
+  using D = AS<P, PZ>;
   static int grid_maxes[kMaxDev] = {0};
   const int dev = cur_device();
   int& grid_max = grid_maxes[dev];
   if (!grid_max) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_apply_qs<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
+    CUDA_CHECK(cudaFuncSetAttribute(k_apply_qs<P, PZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM));
     int per_sm = 0, sms = 0;
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_qs<P>, 32 * D::W, D::SMEM));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_qs<P, PZ>, 32 * D::W, D::SMEM));
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int E = elist ? ne : c->E_own;
@@ -753,20 +762,23 @@ static void apply_qs_P(sem_ctx* c, const DeviceLevel& L, const double* u, double
   const int nquad = (E + 3) / 4;
   const int need = (nquad + D::NG - 1) / D::NG;
   const int grid = need < grid_max ? need : grid_max;
-  k_apply_qs<P><<<grid, 32 * D::W, D::SMEM, c->stream>>>(E, L.conn, L.Gw, L.qmats, u, y, flags, elist);
+  k_apply_qs<P, PZ><<<grid, 32 * D::W, D::SMEM, c->stream>>>(E, L.conn, L.Gw, L.qmats, u, y, flags, elist);
   CUDA_CHECK(cudaGetLastError());
 }
 
 bool launch_apply_qs(sem_ctx* c, int level, const double* u, double* y, int flags, const int32_t* elist, int ne) {
   const DeviceLevel& L = c->L[level];
   if (!L.qmats || !L.Gw) return false;
-  switch (L.p) {
-    case 3: apply_qs_P<3>(c, L, u, y, flags, elist, ne); break;
-    case 4: apply_qs_P<4>(c, L, u, y, flags, elist, ne); break;
-    case 5: apply_qs_P<5>(c, L, u, y, flags, elist, ne); break;
-    case 6: apply_qs_P<6>(c, L, u, y, flags, elist, ne); break;
-    default: return false;
+#define QS_CASE(P_, Q_) \
+  else if (L.p == P_ && L.q == Q_) apply_qs_P<P_, Q_>(c, L, u, y, flags, elist, ne);
+  if (false) {
   }
+  QS_CASE(3, 3) QS_CASE(4, 4) QS_CASE(5, 5) QS_CASE(6, 6)
+  QS_CASE(3, 1) QS_CASE(3, 2) QS_CASE(3, 4) QS_CASE(3, 5)
+  QS_CASE(4, 1) QS_CASE(4, 2) QS_CASE(4, 3) QS_CASE(4, 5)
+  QS_CASE(5, 1) QS_CASE(5, 2) QS_CASE(5, 3) QS_CASE(5, 4)
+  else return false;
+#undef QS_CASE
   c->launches++;
   return true;
 }

@@ -579,10 +579,13 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
       mats[(size_t)3 * R.qt * ntp + R.n1 * R.n1 + i] = R.Dt[i];
     }
     L.mats = upload(c, mats);
-    if (L.p == L.q) {  // the tensor-core kernels are isotropic; (P_xy, P_z) levels use k_apply_pq
+    if (L.p == L.q) {
       L.frag = upload(c, dmma_fragments(R));
       if (L.p <= 6) L.wmats = upload(c, warp_apply_mats(R));
       if (L.p >= 3 && L.p <= 6) L.qmats = upload(c, quad_apply_mats(R));
+    } else if (L.p >= 3 && L.p <= 5 && L.q >= 1 && L.q <= 5) {  // (P_xy, P_z) levels: k_apply_qs<p, q>
+      const std::vector<double> qm = quad_apply_mats(R);
+      if (!qm.empty()) L.qmats = upload(c, qm);
     }
     // geometric factors from the finest nodal map (all held elements)
     L.G = dalloc<double>(c, (size_t)E * 6 * L.Q);

@@ -393,6 +393,9 @@ bool launch_apply_subset(sem_ctx* c, int level, const double* u, double* y, int 
 
 void launch_apply(sem_ctx* c, int level, const double* u, double* y, int flags) {
   if (c->L[level].p != c->L[level].q) {  // anisotropic level
+    if (!c->det.on && (c->opts.apply_kernel == 0 || c->opts.apply_kernel == 4) &&
+        launch_apply_qs(c, level, u, y, flags, nullptr, 0))
+      return;   // tensor-core kernel for P_p x P_q, 3 <= p <= 5, 1 <= q <= 5
     apply_pq(c, c->L[level], u, y, flags);
     c->launches++;
     return;

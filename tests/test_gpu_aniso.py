@@ -129,3 +129,31 @@ def test_aniso_solve(case):
     A, b = sem.dirichlet_lift(lev, phiD)
     _, info = pmg.pcg(C.mg, b, rtol=1e-13)
     assert abs(rep["iters"] - info["iters"]) <= 1
+
+
+ANISO_PAIRS = [(p, q) for p in (3, 4, 5) for q in range(1, 6) if q != p]
+
+
+@pytest.mark.parametrize("p,q", ANISO_PAIRS)
+def test_aniso_tensor_core_kernel_every_pair(p, q):
+    """k_apply_qs<p, q> (the default for 3 <= p <= 5, 1 <= q <= 5) and the generic k_apply_pq
+    (apply_kernel = 1) on the finest P_p x P_q level against the assembled oracle matrix, raw
+    and masked, on 30 prisms (a ragged last quad of four elements)."""
+    m = config2(p=p, nx=5, ny=1, nz=3)
+    m.pz = q
+    lev = sem.build_system(m, p, q=q)
+    u = random_vector(lev.n, seed=300 + 10 * p + q)
+    F = lev.free
+    for kernel in (0, 1):
+        s = lib.Solver(m.vertices, m.prisms, m.face_tag, p, node_xyz=m.node_xyz(lib.reference_nodes(p, q)), pz=q,
+                       levels=[(p, q), (1, 1)], apply_kernel=kernel)
+        perm = lib_to_oracle(s.node_xyz(0), lev.xyz)
+        for masked in (False, True):
+            y = s.apply(torch.from_numpy(np.ascontiguousarray(u[perm])).cuda(), masked=masked)
+            out = np.zeros(lev.n)
+            out[perm] = y.cpu().numpy()
+            if masked:
+                assert rel(out[F], lev.A[F][:, F] @ u[F]) <= APPLY_TOL, (kernel, masked)
+            else:
+                assert rel(out, lev.A @ u) <= APPLY_TOL, (kernel, masked)
+        s.close()
