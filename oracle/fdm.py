@@ -12,8 +12,10 @@ horizontal node patch H_k and a vertical node range V_k, and
 
 where K_h, M_h are the 2D stiffness and mass matrices of the P_p triangle
 space on the footprint mesh (x, y affine per triangle) and K_v, M_v the 1D
-GLL P_p stiffness and mass matrices of element k's column, layer j having the
-mean thickness d_j of its three vertical edges.  B~_k = B_k exactly when the
+GLL P_q stiffness and mass matrices of element k's column (q = the vertical
+order: q = p on isotropic levels, the P_z of the paper's (P_xy, P_z) pairs,
+P:450, otherwise), layer j having the mean thickness d_j of its three vertical
+edges.  B~_k = B_k exactly when the
 prisms are straight with flat layers (config 1: A = K_h (x) M_v + M_h (x) K_v).
 
 Definitions written out here (the library computes the same operator by a
@@ -23,12 +25,12 @@ numpy.linalg.inv):
 * line structure: 3D nodes with equal (x, y) form one vertical line h (2D
   node); the z-index of a node is its rank by z on its line;
 * column of element k: its footprint triangle (2D labels of its bottom nodes);
-  layer j: its lowest z-index / p;
+  layer j: its lowest z-index / q;
 * H_k: 2D nodes within 2D lattice-graph distance `overlap` of the triangle's
   nodes (reading O15 restricted to one level: lattice neighbours inside a
   common triangle);
-* V_k: z-indices [max(0, jp - o), min(Z_c, jp + p + o)] of the column (Z_c =
-  p x layers), without the z-levels at which all of the column's own nodes
+* V_k: z-indices [max(0, jq - o), min(Z_c, jq + q + o)] of the column (Z_c =
+  q x layers), without the z-levels at which all of the column's own nodes
   are Dirichlet (the free surface);
 * local solve: (B~_k^{-1}) restricted to the box entries that exist and are
   free; W from the subdomain counts (eq 4.6).
@@ -100,16 +102,16 @@ class Columns:
     """Footprint triangles, element layers and the 2D / 1D operators of a level."""
 
     def __init__(self, mesh, level: sem.Level):
-        p = level.p
+        p, q = level.p, level.pz          # horizontal / vertical order (SURVEY NEXT-2; q = p isotropic)
         Nt = R.n_tri(p)
-        self.p = p
+        self.p, self.q = p, q
         self.hl, self.zi, self.xy, self.node_at = line_structure(level)
         E = level.conn.shape[0]
         elem_h = self.hl[level.conn[:, :Nt]]            # [E][Nt] labels of the bottom-level nodes
         z_lo = self.zi[level.conn].min(axis=1)
-        if np.any(z_lo % p):
+        if np.any(z_lo % q):
             raise ValueError("mesh is not layered")
-        self.layer = z_lo // p
+        self.layer = z_lo // q
         keys = {}
         self.col = np.empty(E, dtype=np.int64)
         for e in range(E):
@@ -149,17 +151,17 @@ class Columns:
         ar = self.tri_h[:, a].ravel()
         br = self.tri_h[:, b].ravel()
         self.adj = sp.csr_matrix((np.ones(ar.size), (ar, br)), shape=(nh, nh))
-        self.Kref, self.Mref = line_matrices(p)
+        self.Kref, self.Mref = line_matrices(q)
 
     def column_line_matrices(self, c: int):
         """K_v, M_v [Z_c+1][Z_c+1] of column c (layers of mean thickness d_j)."""
-        p = self.p
+        q = self.q
         el = self.col_elems[c]
-        Z = p * len(el)
+        Z = q * len(el)
         Kv = np.zeros((Z + 1, Z + 1))
         Mv = np.zeros((Z + 1, Z + 1))
         for j, e in enumerate(el):
-            s = slice(j * p, j * p + p + 1)
+            s = slice(j * q, j * q + q + 1)
             Kv[s, s] += (2.0 / self.d[e]) * self.Kref
             Mv[s, s] += (self.d[e] / 2.0) * self.Mref
         return Kv, Mv
@@ -197,7 +199,7 @@ def fdm_blocks(mesh, level: sem.Level, overlap: int, cols: Columns | None = None
     free nodes, dense local inverse (B~_k^{-1}) restricted to them, or None when
     inverses=False)."""
     cols = cols or Columns(mesh, level)
-    p = level.p
+    q = level.pz
     out = []
     cache = {}
     for k in (range(level.conn.shape[0]) if elems is None else elems):
@@ -211,7 +213,7 @@ def fdm_blocks(mesh, level: sem.Level, overlap: int, cols: Columns | None = None
             cache[c] = (H, Kv, Mv, Zc, set(dz), cols.K2[H][:, H].toarray(), cols.M2[H][:, H].toarray())
         H, Kv, Mv, Zc, dz, Kh, Mh = cache[c]
         j = int(cols.layer[k])
-        V = [z for z in range(max(0, j * p - overlap), min(Zc, j * p + p + overlap) + 1) if z not in dz]
+        V = [z for z in range(max(0, j * q - overlap), min(Zc, j * q + q + overlap) + 1) if z not in dz]
         V = np.array(V)
         ids = cols.node_at[np.repeat(H, len(V)), np.tile(V, len(H))]    # box order (h outer, z inner)
         keep = ids >= 0

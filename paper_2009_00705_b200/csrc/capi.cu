@@ -417,8 +417,8 @@ void prepare_global(const sem_mesh* mesh, int p, const sem_opts& o, GlobalModel&
   if (gm.PZ > 8) throw SemError(SEM_EINVAL, "vertical order pz must be in 1..8");
   schedule_pq(p, gm.PZ, o, gm.sched, gm.schedz);
   if (gm.PZ != p || gm.sched != gm.schedz) {
-    if (o.nranks > 1 || o.local_solve != 0)
-      throw SemError(SEM_EUNSUPPORTED, "anisotropic (P_xy, P_z) levels: single domain, dense local solves only");
+    if (o.nranks > 1)
+      throw SemError(SEM_EUNSUPPORTED, "anisotropic (P_xy, P_z) levels: single domain only");
   }
   gm.user_part.clear();
   if (mesh->part && o.nranks > 1) {
@@ -634,7 +634,7 @@ void build_levels(sem_ctx* c, const GlobalModel& gm, const std::vector<int>& lid
         setup_schwarz(c, li, (*gsch)[lid], blas, sol, d_D, o.verbose);
       } else if (o.local_solve == 1) {
         const int ov = o.overlap >= 0 ? o.overlap : (c->L[li].p + 2) / 2;  // refined: ceil((P+1)/2)
-        FdmTopo F = fdm_topology(gm.hm, gm.topo[lid], gm.X, p, ov);
+        FdmTopo F = fdm_topology(gm.hm, gm.topo[lid], gm.X, p, ov, gm.PZ);
         if (o.verbose) fprintf(stderr, "[sem] level p=%d FDM topology %.0f ms\n", c->L[li].p, now_ms() - t0);
         int64_t nirr = 0;
         for (uint8_t r : F.regular) nirr += !r;
@@ -1200,6 +1200,8 @@ int sem_update_geometry(sem_ctx* c, const double* node_xyz, int strategy) {
     if (strategy == 4 && c->L.size() > 1 && (!c->L[0].fdm || !c->C.iterative))
       throw SemError(SEM_EUNSUPPORTED, "strategy III (4) re-forms smoothers and coarse preconditioner every stage: "
                                        "needs local_solve = 1 and coarse_solver = 1");
+    if (strategy == 4 && c->PZ != c->P)
+      throw SemError(SEM_EUNSUPPORTED, "strategy III (4): isotropic orders only");
     condense_destroy(c);   // the interior factorisations follow the geometry (re-formed on the next condensed solve)
     const int p = c->P, Nf = n_prism(p, c->PZ), E = c->E;
     std::vector<double> X(node_xyz, node_xyz + (size_t)E * Nf * 3);

@@ -727,7 +727,7 @@ void setup_distributed(sem_ctx* c, GlobalModel& gm) {
   if (o.local_solve == 1) {
     for (int l = 0; l + 1 < nl; ++l) {
       const int ov = o.overlap >= 0 ? o.overlap : (gm.sched[l] + 2) / 2;
-      Fg.push_back(fdm_topology(gm.hm, gm.topo[l], gm.X, gm.P, ov));
+      Fg.push_back(fdm_topology(gm.hm, gm.topo[l], gm.X, gm.P, ov, gm.PZ));
       const FdmTopo& F = Fg.back();
       std::vector<double> cnt(gm.topo[l].n, 0.0);
       for (int e = 0; e < E; ++e)

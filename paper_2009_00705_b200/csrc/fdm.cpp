@@ -22,10 +22,14 @@ namespace {
 }
 }  // namespace
 
-FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<double>& X, int pg, int overlap) {
+FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<double>& X, int pg, int overlap,
+                     int qg) {
   FdmTopo F;
-  const int p = L.p, Nt = n_tri(p), N = L.N, E = m.E;
+  // p: horizontal order (triangle patches, 2D operators); q: vertical order (node lines, 1D operators)
+  const int p = L.p, q = L.q > 0 ? L.q : L.p, Nt = n_tri(p), N = L.N, E = m.E;
+  if (qg < 0) qg = pg;
   F.p = p;
+  F.q = q;
   F.overlap = overlap;
   // ---- 1. stacking: columns and layers
   struct KE {
@@ -89,18 +93,18 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
         const int32_t g = L.conn[(size_t)y * N + mm];
         int found = -1;
         for (int m2 = 0; m2 < Nt; ++m2)
-          if (L.conn[(size_t)x * N + m2 + (size_t)Nt * p] == g) found = m2;
+          if (L.conn[(size_t)x * N + m2 + (size_t)Nt * q] == g) found = m2;
         if (found < 0) unsupported("stacked prisms do not share their nodes");
         eh[(size_t)y * Nt + mm] = eh[(size_t)x * Nt + found];
       }
     }
   }
-  // ---- 3. vertical lines: node (h, z) with z = layer * p + l
+  // ---- 3. vertical lines: node (h, z) with z = layer * q + l
   std::vector<int32_t> linelen(nh2, 0);
   for (int e = 0; e < E; ++e)
     for (int mm = 0; mm < Nt; ++mm) {
       int32_t& ll = linelen[eh[(size_t)e * Nt + mm]];
-      ll = std::max(ll, (F.layer[e] + 1) * p + 1);
+      ll = std::max(ll, (F.layer[e] + 1) * q + 1);
     }
   std::vector<int64_t> lineoff(nh2 + 1, 0);
   for (int h = 0; h < nh2; ++h) lineoff[h + 1] = lineoff[h] + linelen[h];
@@ -109,7 +113,7 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
   for (int e = 0; e < E; ++e)
     for (int n = 0; n < N; ++n) {
       const int mm = n % Nt, l = n / Nt;
-      const int64_t s = lineoff[eh[(size_t)e * Nt + mm]] + F.layer[e] * p + l;
+      const int64_t s = lineoff[eh[(size_t)e * Nt + mm]] + F.layer[e] * q + l;
       const int32_t g = L.conn[(size_t)e * N + n];
       if ((vline[s] != -1 && vline[s] != g) || (pos[g] != -1 && pos[g] != s)) unsupported("nodes off their lines");
       vline[s] = g;
@@ -142,20 +146,20 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
     }
   }
   // ---- 5. reference data: 2D collapsed cubature, 1D GLL operators
-  const LevelRef R = make_level_ref(p);
+  const LevelRef R = make_level_ref(p, q);
   std::vector<double> wt(R.qt, 0.0);
   for (int a = 0; a < R.qt; ++a)
-    for (int q = 0; q < R.qv; ++q) wt[a] += R.wq[a + R.qt * q];
+    for (int k = 0; k < R.qv; ++k) wt[a] += R.wq[a + R.qt * k];
   for (auto& w : wt) w *= 0.5;  // sum of the vertical GL weights is 2
-  const Rule1D gv = gauss_legendre_rule(p + 1);
+  const Rule1D gv = gauss_legendre_rule(q + 1);
   std::vector<double> Kref(R.n1 * R.n1, 0.0), Mref(R.n1 * R.n1, 0.0);
   for (int a = 0; a < R.n1; ++a)
     for (int b = 0; b < R.n1; ++b)
-      for (int q = 0; q < R.qv; ++q) {
-        Kref[a * R.n1 + b] += gv.w[q] * R.Dt[q * R.n1 + a] * R.Dt[q * R.n1 + b];
-        Mref[a * R.n1 + b] += gv.w[q] * R.Bt[q * R.n1 + a] * R.Bt[q * R.n1 + b];
+      for (int k = 0; k < R.qv; ++k) {
+        Kref[a * R.n1 + b] += gv.w[k] * R.Dt[k * R.n1 + a] * R.Dt[k * R.n1 + b];
+        Mref[a * R.n1 + b] += gv.w[k] * R.Bt[k * R.n1 + a] * R.Bt[k * R.n1 + b];
       }
-  const int Ntg = n_tri(pg), Ng = Ntg * (pg + 1);
+  const int Ntg = n_tri(pg), Ng = Ntg * (qg + 1);
   const int corner[3] = {0, pg, Ntg - 1};  // lattice (0,0), (pg,0), (0,pg) = v0, v1, v2
   auto xyz = [&](int e, int n, int i) { return X[((size_t)e * Ng + n) * 3 + i]; };
   // 2D element operators of every column [ncol][Nt][Nt]
@@ -260,14 +264,14 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
   F.z0.assign(E, 0);
   F.nv.assign(E, 0);
   for (int e = 0; e < E; ++e) {
-    const int c = F.col[e], j = F.layer[e], Zc = nlay[c] * p;
+    const int c = F.col[e], j = F.layer[e], Zc = nlay[c] * q;
     const int32_t* t = &eh[(size_t)colbot[c] * Nt];
     auto dlev = [&](int z) {  // z-level of the column made of Dirichlet nodes only
       for (int mm = 0; mm < Nt; ++mm)
         if (!L.dir[vline[lineoff[t[mm]] + z]]) return false;
       return true;
     };
-    int lo = std::max(0, j * p - overlap), hi = std::min(Zc, j * p + p + overlap);
+    int lo = std::max(0, j * q - overlap), hi = std::min(Zc, j * q + q + overlap);
     while (lo <= hi && dlev(lo)) ++lo;
     while (hi >= lo && dlev(hi)) --hi;
     for (int z = lo; z <= hi; ++z)
@@ -292,15 +296,15 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
     double* Kv = &F.Kv[F.voff[e]];
     double* Mv = &F.Mv[F.voff[e]];
     for (int jj = 0; jj < nlay[c]; ++jj) {  // layers overlapping [lo, lo+nv)
-      const int zb = jj * p;
-      if (zb + p < lo || zb > lo + nv - 1) continue;
+      const int zb = jj * q;
+      if (zb + q < lo || zb > lo + nv - 1) continue;
       const int x = colel[cfirst[c] + jj];
       double d = 0.0;
       for (int v = 0; v < 3; ++v)
-        d += xyz(x, corner[v] + Ntg * pg, 2) - xyz(x, corner[v], 2);
+        d += xyz(x, corner[v] + Ntg * qg, 2) - xyz(x, corner[v], 2);
       d /= 3.0;
-      for (int a = 0; a <= p; ++a)
-        for (int b = 0; b <= p; ++b) {
+      for (int a = 0; a <= q; ++a)
+        for (int b = 0; b <= q; ++b) {
           const int za = zb + a - lo, zb2 = zb + b - lo;
           if (za < 0 || za >= nv || zb2 < 0 || zb2 >= nv) continue;
           Kv[za * nv + zb2] += (2.0 / d) * Kref[a * R.n1 + b];
@@ -324,7 +328,7 @@ FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<do
   F.nzc.resize(ncol);
   F.cioff.assign(ncol + 1, 0);
   for (int c = 0; c < ncol; ++c) {
-    F.nzc[c] = nlay[c] * p + 1;
+    F.nzc[c] = nlay[c] * q + 1;
     F.cioff[c + 1] = F.cioff[c] + (F.hoff[c + 1] - F.hoff[c]) * F.nzc[c];
   }
   F.cidx.resize(F.cioff[ncol]);
@@ -390,6 +394,7 @@ FdmTopo fdm_local(const FdmTopo& G, const std::vector<int32_t>& elems, int E_own
                   int64_t n_global, const std::vector<double>& Wg) {
   FdmTopo F;
   F.p = G.p;
+  F.q = G.q;
   F.overlap = G.overlap;
   std::vector<int32_t> gloc(n_global, -1);
   for (size_t i = 0; i < gid.size(); ++i) gloc[gid[i]] = (int32_t)i;

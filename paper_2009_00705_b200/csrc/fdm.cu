@@ -219,8 +219,8 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
   L.f_col = upload(c, F.col);
   L.f_cfirst = upload(c, F.cfirst);
   {  // 1D GLL stiffness / mass of the reference layer (per-stage vertical re-formation, stage.cu)
-    const LevelRef R = make_level_ref(F.p);
-    const Rule1D gv = gauss_legendre_rule(F.p + 1);
+    const LevelRef R = make_level_ref(F.p, F.q > 0 ? F.q : F.p);
+    const Rule1D gv = gauss_legendre_rule((F.q > 0 ? F.q : F.p) + 1);
     std::vector<double> km(2 * R.n1 * R.n1, 0.0);
     for (int a = 0; a < R.n1; ++a)
       for (int b = 0; b < R.n1; ++b)
@@ -250,7 +250,7 @@ void setup_fdm(sem_ctx* c, int li, const FdmTopo& F, cusolverDnHandle_t sol, cub
     L.f_mt = (F.nh_max + 7) / 8;
     std::vector<int4> units;
     L.f_warp = (L.f_mt <= 8 && nvt <= 2) ? 1 : 0;
-    L.f_nph = 2 + (2 * F.overlap) / F.p;  // boxes j, j + k of a column overlap iff k p <= p + 2 o
+    L.f_nph = 2 + (2 * F.overlap) / (F.q > 0 ? F.q : F.p);  // boxes j, j + k overlap iff k q <= q + 2 o
     const int per = L.f_warp ? 8 : FDM_NT / nvt;
     for (int q = 0; q < ncol; ++q)
       for (int64_t j = F.cfirst[q]; j < F.cfirst[q + 1]; j += per)

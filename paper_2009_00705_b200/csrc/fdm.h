@@ -17,7 +17,7 @@
 namespace sem {
 
 struct FdmTopo {
-  int p = 0, overlap = 0;
+  int p = 0, q = 0, overlap = 0;        // horizontal / vertical order (q = p isotropic)
   int ncol = 0;
   int nh_max = 0, nv_max = 0;
   std::vector<int32_t> col, layer;      // [E] column and layer (0 = bottom) of every element
@@ -54,6 +54,8 @@ FdmTopo fdm_local(const FdmTopo& G, const std::vector<int32_t>& elems, int E_own
 // X: [E][N(pg)][3] nodal map of order pg (the finest order; x, y are taken as
 // affine per triangle from its corner nodes, z-thicknesses from the corners).
 // Throws SemError(SEM_EUNSUPPORTED) if the mesh is not a stack of prism layers.
-FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<double>& X, int pg, int overlap);
+// pg, qg: horizontal / vertical order of the fine nodal map X (qg < 0: qg = pg)
+FdmTopo fdm_topology(const HostMesh& m, const LevelTopo& L, const std::vector<double>& X, int pg, int overlap,
+                     int qg = -1);
 
 }  // namespace sem

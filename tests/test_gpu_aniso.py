@@ -34,15 +34,15 @@ def _fine_map_xyz(m, lev):
 
 
 class ACase:
-    def __init__(self, m, levels=None):
+    def __init__(self, m, levels=None, **kw):
         self.m = m
-        kw = {}
         if levels is not None:
             kw["levels"] = levels
         self.s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p, m.pz)),
                             pz=m.pz, **kw)
         self.sched = list(zip(self.s.info["level_p"], self.s.info["level_pz"]))
-        self.mg = pmg.PMG(m, schedule=self.sched)
+        self.mg = pmg.PMG(m, schedule=self.sched, local_solve="fdm" if kw.get("local_solve") == 1 else "dense",
+                          overlap=kw.get("overlap", 1))
         self.levels = []
         for li, ml in enumerate(self.mg.levels):
             lev = ml.level
@@ -157,3 +157,29 @@ def test_aniso_tensor_core_kernel_every_pair(p, q):
             else:
                 assert rel(out, lev.A @ u) <= APPLY_TOL, (kernel, masked)
         s.close()
+
+
+@pytest.mark.parametrize("pq", [(5, 3), (4, 2), (3, 1)])
+def test_aniso_fdm_smoother_vcycle_solve(pq):
+    """FDM local solves (reading O33) on P_p x P_q levels: the library's separable boxes built
+    from the order-q vertical operators (k_fdm_warp) against the oracle's Kronecker inverses on
+    every smoothed level (S^-1 and S^-T), the V-cycle and the solve (the oracle's direct
+    solution), on the curved wave channel."""
+    p, q = pq
+    C = ACase(_mesh(p, q), local_solve=1)
+    for li in range(len(C.levels) - 1):
+        sm = C.mg.levels[li].smoother
+        r = random_vector(len(sm.W), seed=400 + li)
+        for tr in (False, True):
+            u = C.s.empty(li)
+            C.s.schwarz(li, C.free_to_lib(li, r), u, transpose=tr)
+            assert rel(C.lib_to_free(li, u), sm.apply(r, transpose=tr)) <= STEP_TOL, (li, tr)
+    nF = C.mg.levels[0].A.shape[0]
+    r = random_vector(nF, seed=41)
+    assert rel(C.lib_to_free(0, C.s.vcycle(C.free_to_lib(0, r))), C.mg.vcycle(r)) <= STEP_TOL
+    lev = C.levels[0][0]
+    phiD = C.m.phi(*lev.xyz.T)
+    phi, rep = C.s.solve(C.to_lib(0, phiD), tol=1e-12)
+    assert rep["converged"]
+    assert rel(C.to_orc(0, phi), sem.solve_direct(lev, phiD)) <= SOLVE_TOL
+    C.s.close()

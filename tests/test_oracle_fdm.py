@@ -86,6 +86,27 @@ def test_fdm_is_exact_on_straight_flat_prisms(p, overlap):
         np.testing.assert_allclose(Bj[np.ix_(o, o)], Bi, atol=1e-12 * np.abs(Bi).max())
 
 
+@pytest.mark.parametrize("p,q,overlap", [(3, 2, 1), (4, 2, 1), (2, 3, 1), (3, 1, 0)])
+def test_fdm_is_exact_on_straight_flat_prisms_anisotropic(p, q, overlap):
+    """The same identity on P_p(triangle) x P_q(t) prisms: with straight prisms and
+    flat layers A = K_h(p) (x) M_v(q) + M_h(p) (x) K_v(q), so the FDM local inverse built from the
+    order-q vertical operators equals the exact inverse of the O15 block of eq 4.4 (a dropped or
+    misplaced q -- the order-p vertical rule, layer index z / p -- breaks either the sets or the
+    inverses)."""
+    m = config1(p=p, nx=3, ny=2, nz=3)
+    m.pz = q
+    lev = sem.build_system(m, p, q=q)
+    F = lev.free
+    AFF = lev.A[F][:, F].tocsr()
+    dense = pmg.build_smoother(lev, AFF, overlap)
+    fsm = pmg.build_fdm_smoother(m, lev, overlap)
+    np.testing.assert_allclose(fsm.W, dense.W, rtol=0, atol=0)
+    for I, Bi, J, Bj in zip(dense.sets, dense.inv, fsm.sets, fsm.inv):
+        o = np.argsort(J)
+        np.testing.assert_array_equal(J[o], I)
+        np.testing.assert_allclose(Bj[np.ix_(o, o)], Bi, atol=1e-12 * np.abs(Bi).max())
+
+
 def test_fdm_is_not_exact_on_curved_prisms():
     """Sanity of the pin above: on curved prisms the separable form is only an
     approximation (the pin would be vacuous if the two always agreed)."""
