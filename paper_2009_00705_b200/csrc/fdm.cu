@@ -643,26 +643,39 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
-  // column block gather in batches of 8 items per thread: node ids, values (x W), stores
-  for (int base = 0; base < ROWS * ldr; base += 256 * 8) {
-    int gid[8];
-    double val[8];
+  // column block gather: warp w owns the rows h = w + 8 i (i < MT), its lanes the z positions
+  // z = lane + 32 zi (coalesced connectivity reads, no index division); the next z block's node
+  // ids load behind this block's values.  Every entry of Rc is written (zeros outside the unit)
+  {
+    const int nzi = (ldr + 31) >> 5;
+    int gid[MT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = base + tid + 256 * k, h = t / ldr, zz = t - h * ldr;
-      gid[k] = (h < nh && zz < nzu) ? __ldg(ci + h * nz + zlo + zz) : -1;
+    for (int i = 0; i < MT; ++i) {
+      const int h = warp + 8 * i;
+      gid[i] = (h < nh && lane < nzu) ? __ldg(ci + h * nz + zlo + lane) : -1;
     }
+    for (int zi = 0; zi < nzi; ++zi) {
+      const int z = lane + 32 * zi, zn1 = z + 32;
+      double val[MT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) val[k] = gid[k] >= 0 ? r[gid[k]] : 0.0;
-    if (transpose) {
+      for (int i = 0; i < MT; ++i) val[i] = gid[i] >= 0 ? r[gid[i]] : 0.0;
+      if (transpose) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (gid[k] >= 0) val[k] *= __ldg(W + gid[k]);
-    }
+        for (int i = 0; i < MT; ++i)
+          if (gid[i] >= 0) val[i] *= __ldg(W + gid[i]);
+      }
+      int gn[MT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = base + tid + 256 * k;
-      if (t < ROWS * ldr) Rc[t] = val[k];
+      for (int i = 0; i < MT; ++i) {
+        const int h = warp + 8 * i;
+        gn[i] = (h < nh && zn1 < nzu) ? __ldg(ci + h * nz + zlo + zn1) : -1;
+      }
+      if (z < ldr) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i) Rc[(warp + 8 * i) * ldr + z] = val[i];
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i) gid[i] = gn[i];
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -808,24 +821,36 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
     __syncthreads();
   }
   __syncthreads();
-  for (int base = 0; base < nh * ldr; base += 256 * 8) {  // scatter every column node of the unit once
-    int gid[8];
-    double val[8];
+  {  // scatter every column node of the unit once (the gather's (row, z) map)
+    const int nzi = (nzu + 31) >> 5;
+    int gid[MT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = base + tid + 256 * k, h = t / ldr, zz = t - h * ldr;
-      gid[k] = (h < nh && zz < nzu) ? __ldg(ci + h * nz + zlo + zz) : -1;
+    for (int i = 0; i < MT; ++i) {
+      const int h = warp + 8 * i;
+      gid[i] = (h < nh && lane < nzu) ? __ldg(ci + h * nz + zlo + lane) : -1;
     }
+    for (int zi = 0; zi < nzi; ++zi) {
+      const int z = lane + 32 * zi, zn1 = z + 32;
+      double val[MT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) val[k] = gid[k] >= 0 ? Rc[base + tid + 256 * k] : 0.0;
-    if (!transpose) {
+      for (int i = 0; i < MT; ++i) val[i] = gid[i] >= 0 ? Rc[(warp + 8 * i) * ldr + z] : 0.0;
+      if (!transpose) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (gid[k] >= 0) val[k] *= __ldg(W + gid[k]);
+        for (int i = 0; i < MT; ++i)
+          if (gid[i] >= 0) val[i] *= __ldg(W + gid[i]);
+      }
+      int gn[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int h = warp + 8 * i;
+        gn[i] = (h < nh && zn1 < nzu) ? __ldg(ci + h * nz + zlo + zn1) : -1;
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+        if (gid[i] >= 0) atomicAdd(u + gid[i], val[i]);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) gid[i] = gn[i];
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (gid[k] >= 0) atomicAdd(u + gid[k], val[k]);
   }
 }
 
@@ -915,13 +940,15 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     soff[cnt] = acc;
   }
   const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
-  const int nval = nh * nzu;
-  // node ids of the first gather chunk, in flight together with the S_h loads
-  int gid0[8];
+  // gather / scatter map: warp w owns the column rows h = w + 8 i (i < MT), its lanes the z
+  // positions z = lane + 32 zi: coalesced connectivity reads, no index division.  Node ids of
+  // the first z block, in flight together with the S_h loads
+  const int nzi = (nzu + 31) >> 5;
+  int gid0[MT];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int t = tid + 256 * k, h = t / nzu, zz = t - h * nzu;
-    gid0[k] = t < nval ? __ldg(ci + h * nz + zlo + zz) : -1;
+  for (int i = 0; i < MT; ++i) {
+    const int h = warp + 8 * i;
+    gid0[i] = (h < nh && lane < nzu) ? __ldg(ci + h * nz + zlo + lane) : -1;
   }
   {  // S_h -> shared by cp.async (zero-filled padding), completed with the column block below:
      // the S_h bytes stream in while the gather's dependent loads are in flight
@@ -962,25 +989,35 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   // column block (x W for S^-T): the n_h x n_zu valid entries; rows >= n_h zeroed (they meet the
   // zero columns of S_h^T: stale shared memory there could hold non-finite values), columns
   // >= n_zu only reach output columns no later step reads
-  for (int base = 0; base < nval; base += 256 * 8) {
-    int gid[8], pos[8];
+  {
+    int gid[MT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = base + tid + 256 * k, h = t / nzu, zz = t - h * nzu;
-      pos[k] = t < nval ? h * ldb + zz : -1;
-      gid[k] = base == 0 ? gid0[k] : (t < nval ? __ldg(ci + h * nz + zlo + zz) : -1);
+    for (int i = 0; i < MT; ++i) gid[i] = gid0[i];
+    for (int zi = 0; zi < nzi; ++zi) {
+      const int z = lane + 32 * zi;
+      double val[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) val[i] = gid[i] >= 0 ? r[gid[i]] : 0.0;
+      if (transpose) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+          if (gid[i] >= 0) val[i] *= __ldg(W + gid[i]);
+      }
+      int gn[MT];   // the next z block's node ids, in flight behind this block's r loads
+      const int zn1 = z + 32;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int h = warp + 8 * i;
+        gn[i] = (zi + 1 < nzi && h < nh && zn1 < nzu) ? __ldg(ci + h * nz + zlo + zn1) : -1;
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int h = warp + 8 * i;
+        if (h < nh && z < nzu) B1[h * ldb + z] = val[i];
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i) gid[i] = gn[i];
     }
-    double val[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) val[k] = gid[k] >= 0 ? r[gid[k]] : 0.0;
-    if (transpose) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (gid[k] >= 0) val[k] *= __ldg(W + gid[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (pos[k] >= 0) B1[pos[k]] = val[k];
   }
   for (int t = nh * ldb + tid; t < ROWS * ldb; t += 256) B1[t] = 0.0;
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -991,12 +1028,29 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   __syncthreads();
   // the scatter's first chunk (step 4): node ids now, weights before step 3, both in flight
   // behind the vertical step and the second GEMM (the same (h, z) <- t map as the gather)
-  const int ntot = nh * nzu;
-  int g4[8];
+  int g4[MT];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int t = tid + 256 * k, h = t / nzu, z = t - h * nzu;
-    g4[k] = t < ntot ? __ldg(ci + h * nz + zlo + z) : -1;
+  for (int i = 0; i < MT; ++i) {
+    const int h = warp + 8 * i;
+    g4[i] = (h < nh && lane < nzu) ? __ldg(ci + h * nz + zlo + lane) : -1;
+  }
+  // step 4's table, built here (it depends on the unit descriptor only; the barrier after step 2
+  // publishes it).  The boxes are ordered by layer and their z ranges increase with j: per z the
+  // stacked-column offsets of its (non-skipped) boxes, ascending j (fixed summation order)
+  constexpr int ZO = 4;
+  __shared__ __align__(8) short zo[2 * 8 * 16 + 2][ZO];
+  __shared__ unsigned char zn[2 * 8 * 16 + 2];
+  for (int z = tid; z < nzu; z += 256) {
+    int k = 0;
+    for (int j = 0; j < cnt; ++j) {
+      const int zz = z - (ez0[j] - zlo);
+      if (zz >= 0 && zz < env[j] && !sk[j]) {
+        if (k < ZO) zo[z][k] = (short)(soff[j] + zz);
+        ++k;
+      }
+    }
+    for (int q = k; q < ZO; ++q) zo[z][q] = 0;
+    zn[z] = (unsigned char)k;
   }
   // 2. warp j: vertical transform and scaling of box j, stored compactly into Zs (B1)
   if (warp < cnt && !sk[warp]) {
@@ -1044,64 +1098,63 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     }
   }
   __syncthreads();
-  double w4[8];
+  double w4[MT];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) w4[k] = (!transpose && g4[k] >= 0) ? __ldg(W + g4[k]) : 1.0;
+  for (int i = 0; i < MT; ++i) w4[i] = (!transpose && g4[i] >= 0) ? __ldg(W + g4[i]) : 1.0;
   // 3. Ys = S_h Zs -> B2 over the stacked columns
   fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, soff[cnt], warp, lane, mtu);
   __syncthreads();
-  // 4. every column node of the unit: sum of the boxes holding it, scatter (x W for S^-1).
-  // The boxes are ordered by layer and their z ranges increase with j: the boxes holding z form
-  // a contiguous run; per z the stacked-column offsets of its (non-skipped) boxes are tabulated
-  // once (ascending j: fixed summation order), then the column nodes are processed in chunks of
-  // 8 per thread with independent connectivity and weight loads (two global round trips per
-  // chunk instead of two per node)
-  constexpr int ZO = 4;
-  __shared__ short zo[2 * 8 * 16 + 2][ZO];
-  __shared__ unsigned char zn[2 * 8 * 16 + 2];
-  for (int z = tid; z < nzu; z += 256) {
-    int k = 0;
-    for (int j = 0; j < cnt; ++j) {
-      const int zz = z - (ez0[j] - zlo);
-      if (zz >= 0 && zz < env[j] && !sk[j]) {
-        if (k < ZO) zo[z][k] = (short)(soff[j] + zz);
-        ++k;
-      }
+  // 4. every column node of the unit: sum of the boxes holding it (table of step 2), scatter
+  // (x W for S^-1).  Same (row, z) map as the gather; a lane's table entry is read once per z
+  // block and serves its MT rows; the next block's node ids and weights load behind this block's sums
+  for (int zi = 0; zi < nzi; ++zi) {
+    const int z = lane + 32 * zi;
+    const bool zv = z < nzu;
+    int gn[MT];
+    const int zn1 = z + 32;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int h = warp + 8 * i;
+      gn[i] = (zi + 1 < nzi && h < nh && zn1 < nzu) ? __ldg(ci + h * nz + zlo + zn1) : -1;
     }
-    zn[z] = (unsigned char)k;
-  }
-  __syncthreads();
-  for (int base = 0; base < ntot; base += 256 * 8) {
-    int g[8];
-    double wv[8];
-    if (base == 0) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) g[k] = g4[k], wv[k] = w4[k];
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int t = base + tid + 256 * k, h = t / nzu, z = t - h * nzu;
-        g[k] = t < ntot ? __ldg(ci + h * nz + zlo + z) : -1;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) wv[k] = (!transpose && g[k] >= 0) ? __ldg(W + g[k]) : 1.0;
+    const int nk = zv ? zn[z] : 0;
+    int o[ZO];
+    {
+      const short4 t4 = zv ? *reinterpret_cast<const short4*>(zo[z]) : make_short4(0, 0, 0, 0);
+      o[0] = t4.x, o[1] = t4.y, o[2] = t4.z, o[3] = t4.w;
     }
+    double acc[MT];
+    if (__all_sync(0xffffffffu, nk <= ZO)) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (g[k] < 0) continue;
-      const int t = base + tid + 256 * k, h = t / nzu, z = t - h * nzu;
-      const double* row = B2 + h * ldb;
-      const int nk = zn[z];
-      double acc = 0.0;
-      if (nk <= ZO) {
-        for (int q = 0; q < nk; ++q) acc += row[zo[z][q]];
-      } else {  // more boxes than tabulated (not met for the box sizes of this kernel): walk the run
+      for (int i = 0; i < MT; ++i) {
+        const double* row = B2 + (warp + 8 * i) * ldb;   // rows < 8 MT: inside B2 for every i
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < ZO; ++q) {
+          const double x = row[o[q]];
+          a += q < nk ? x : 0.0;
+        }
+        acc[i] = a;
+      }
+    } else {  // more boxes than tabulated (not met for the box sizes of this kernel): walk the run
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double* row = B2 + (warp + 8 * i) * ldb;
+        double a = 0.0;
         for (int j = 0; j < cnt; ++j) {
           const int zz = z - (ez0[j] - zlo);
-          if (zz >= 0 && zz < env[j] && !sk[j]) acc += row[soff[j] + zz];
+          if (zv && zz >= 0 && zz < env[j] && !sk[j]) a += row[soff[j] + zz];
         }
+        acc[i] = a;
       }
-      atomicAdd(u + g[k], acc * wv[k]);
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+      if (g4[i] >= 0) atomicAdd(u + g4[i], acc[i] * w4[i]);
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      g4[i] = gn[i];
+      w4[i] = (!transpose && gn[i] >= 0) ? __ldg(W + gn[i]) : 1.0;
     }
   }
 }
