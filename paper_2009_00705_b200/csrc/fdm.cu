@@ -406,6 +406,17 @@ __global__ void __launch_bounds__(256) k_fdm(const int32_t* __restrict__ col, co
 }
 
 
+// 1 / d for d = l_h + l_v > 0 (normal range): MUFU.RCP64H seed (~20 bits) + two Newton steps
+// (2^-40, 2^-80: FP64 accurate); replaces the float round trip (two conversions + the IEEE
+// float reciprocal's fix-up branch)
+__device__ __forceinline__ double fdm_rcp(double d) {
+  double rc;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(d));
+  rc = fma(rc, fma(-d, rc, 1.0), rc);
+  rc = fma(rc, fma(-d, rc, 1.0), rc);
+  return rc;
+}
+
 __device__ __forceinline__ void fdm_dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -754,12 +765,9 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
 #pragma unroll
       for (int n = 0; n < NVT; ++n)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {  // v /= (l_h + l_v): float reciprocal + two Newton steps (FP64 accurate)
+        for (int i = 0; i < 2; ++i) {  // v /= (l_h + l_v)
           const double d = la + lvv[n][i];
-          double rc = (double)__frcp_rn((float)d);
-          rc = fma(rc, fma(-d, rc, 1.0), rc);
-          rc = fma(rc, fma(-d, rc, 1.0), rc);
-          v[n][i] *= rc;
+          v[n][i] *= fdm_rcp(d);
         }
 #pragma unroll
       for (int n = 0; n < NVT; ++n) T[mt][n][0] = T[mt][n][1] = 0.0;
@@ -909,7 +917,7 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
                                                    const double* __restrict__ r, double* __restrict__ u, int transpose,
                                                    int ldb, const uint8_t* __restrict__ skip,
                                                    const int* __restrict__ udesc, const int* __restrict__ ulist) {
-  constexpr int NVT = 2, ROWS = 8 * MT, KT = 2 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
+  constexpr int NVT = 2, ROWS = 8 * MT, NVP = 8 * NVT, LDS = ROWS + 4;
   extern __shared__ __align__(16) double sm[];
   double* Ss = sm;                  // [ROWS][LDS]  S_h (row i node, col a mode), zero padded
   double* B1 = Ss + ROWS * LDS;     // [ROWS][ldb]  column block Rc, then the stacked boxes Zs
@@ -944,12 +952,14 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   // positions z = lane + 32 zi: coalesced connectivity reads, no index division.  Node ids of
   // the first z block, in flight together with the S_h loads
   const int nzi = (nzu + 31) >> 5;
-  int gid0[MT];
+  int gid0[2][MT];   // z blocks 0 and 1 (n_zu <= 64: the whole unit) in one batch of loads
 #pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int h = warp + 8 * i;
-    gid0[i] = (h < nh && lane < nzu) ? __ldg(ci + h * nz + zlo + lane) : -1;
-  }
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int h = warp + 8 * i, z = lane + 32 * b;
+      gid0[b][i] = (h < nh && z < nzu) ? __ldg(ci + h * nz + zlo + z) : -1;
+    }
   {  // S_h -> shared by cp.async (zero-filled padding), completed with the column block below:
      // the S_h bytes stream in while the gather's dependent loads are in flight
     constexpr int IS = (ROWS * ROWS + 255) / 256;
@@ -966,6 +976,37 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  // column block (x W for S^-T): the n_h x n_zu valid entries; rows >= n_h zeroed (they meet the
+  // zero columns of S_h^T: stale shared memory there could hold non-finite values), columns
+  // >= n_zu only reach output columns no later step reads
+  for (int zi = 0; zi < nzi; zi += 2) {
+    int gid[2][MT];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int h = warp + 8 * i, z = lane + 32 * (zi + b);
+        gid[b][i] = zi == 0 ? gid0[b][i] : ((h < nh && z < nzu) ? __ldg(ci + h * nz + zlo + z) : -1);
+      }
+    double val[2][MT];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int i = 0; i < MT; ++i) val[b][i] = gid[b][i] >= 0 ? r[gid[b][i]] : 0.0;
+    if (transpose) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+          if (gid[b][i] >= 0) val[b][i] *= __ldg(W + gid[b][i]);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+        if (gid[b][i] >= 0) B1[(warp + 8 * i) * ldb + lane + 32 * (zi + b)] = val[b][i];
+  }
+  for (int t = nh * ldb + tid; t < ROWS * ldb; t += 256) B1[t] = 0.0;
   // per-box vertical modes of warp j, loaded before step 1 (latency hidden behind it)
   double s1[4][2], s2[4][2], lvv[2][2], lav[MT];
   if (warp < cnt) {
@@ -986,40 +1027,6 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) lav[mt] = mt * 8 + r4 < nh ? __ldg(lh + ho + mt * 8 + r4) : 1.0;
   }
-  // column block (x W for S^-T): the n_h x n_zu valid entries; rows >= n_h zeroed (they meet the
-  // zero columns of S_h^T: stale shared memory there could hold non-finite values), columns
-  // >= n_zu only reach output columns no later step reads
-  {
-    int gid[MT];
-#pragma unroll
-    for (int i = 0; i < MT; ++i) gid[i] = gid0[i];
-    for (int zi = 0; zi < nzi; ++zi) {
-      const int z = lane + 32 * zi;
-      double val[MT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) val[i] = gid[i] >= 0 ? r[gid[i]] : 0.0;
-      if (transpose) {
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-          if (gid[i] >= 0) val[i] *= __ldg(W + gid[i]);
-      }
-      int gn[MT];   // the next z block's node ids, in flight behind this block's r loads
-      const int zn1 = z + 32;
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const int h = warp + 8 * i;
-        gn[i] = (zi + 1 < nzi && h < nh && zn1 < nzu) ? __ldg(ci + h * nz + zlo + zn1) : -1;
-      }
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const int h = warp + 8 * i;
-        if (h < nh && z < nzu) B1[h * ldb + z] = val[i];
-      }
-#pragma unroll
-      for (int i = 0; i < MT; ++i) gid[i] = gn[i];
-    }
-  }
-  for (int t = nh * ldb + tid; t < ROWS * ldb; t += 256) B1[t] = 0.0;
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // 1. Tall = S_h^T Rc -> B2
@@ -1028,11 +1035,11 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   __syncthreads();
   // the scatter's first chunk (step 4): node ids now, weights before step 3, both in flight
   // behind the vertical step and the second GEMM (the same (h, z) <- t map as the gather)
-  int g4[MT];
+  int g4[2][MT];   // block 0's ids behind step 2, block 1's behind step 3
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
     const int h = warp + 8 * i;
-    g4[i] = (h < nh && lane < nzu) ? __ldg(ci + h * nz + zlo + lane) : -1;
+    g4[0][i] = (h < nh && lane < nzu) ? __ldg(ci + h * nz + zlo + lane) : -1;
   }
   // step 4's table, built here (it depends on the unit descriptor only; the barrier after step 2
   // publishes it).  The boxes are ordered by layer and their z ranges increase with j: per z the
@@ -1063,6 +1070,7 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
       for (int n = 0; n < NVT; ++n) v[n][0] = v[n][1] = 0.0;
 #pragma unroll
       for (int kt = 0; kt < 2 * NVT; ++kt) {  // A[a][col] = T_j[a][col] (zero beyond the box)
+        if (NVT == 2 && kt * 4 >= nvj) continue;   // k-steps beyond the box: exact zeros (n_v = p + 3 <= 11 needs 3 of 4)
         const int col = kt * 4 + c4;
         const double a = col < nvj ? B2[(mt * 8 + r4) * ldb + zb + col] : 0.0;
 #pragma unroll
@@ -1072,18 +1080,16 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
 #pragma unroll
       for (int n = 0; n < NVT; ++n)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {  // v /= (l_h + l_v): float reciprocal + two Newton steps
+        for (int i = 0; i < 2; ++i) {  // v /= (l_h + l_v)
           const double d = la + lvv[n][i];
-          double rc = (double)__frcp_rn((float)d);
-          rc = fma(rc, fma(-d, rc, 1.0), rc);
-          rc = fma(rc, fma(-d, rc, 1.0), rc);
-          v[n][i] *= rc;
+          v[n][i] *= fdm_rcp(d);
         }
       double t2[NVT][2];
 #pragma unroll
       for (int n = 0; n < NVT; ++n) t2[n][0] = t2[n][1] = 0.0;
 #pragma unroll
       for (int kt = 0; kt < 2 * NVT; ++kt) {
+        if (NVT == 2 && kt * 4 >= nvj) continue;   // k-steps beyond the box: exact zeros (n_v = p + 3 <= 11 needs 3 of 4)
         const double a = c_to_a<NVT>(v, kt, lane);
 #pragma unroll
         for (int n = 0; n < NVT; ++n) fdm_dmma(t2[n][0], t2[n][1], a, s2[kt][n]);
@@ -1098,63 +1104,75 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     }
   }
   __syncthreads();
-  double w4[MT];
+  double w4[2][MT];   // block 0's weights behind step 3, block 1's behind block 0's sums (registers)
 #pragma unroll
-  for (int i = 0; i < MT; ++i) w4[i] = (!transpose && g4[i] >= 0) ? __ldg(W + g4[i]) : 1.0;
+  for (int i = 0; i < MT; ++i) w4[0][i] = (!transpose && g4[0][i] >= 0) ? __ldg(W + g4[0][i]) : 1.0;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int h = warp + 8 * i, z = lane + 32;
+    g4[1][i] = (h < nh && z < nzu) ? __ldg(ci + h * nz + zlo + z) : -1;
+  }
   // 3. Ys = S_h Zs -> B2 over the stacked columns
   fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, soff[cnt], warp, lane, mtu);
+#pragma unroll
+  for (int i = 0; i < MT; ++i) w4[1][i] = (!transpose && g4[1][i] >= 0) ? __ldg(W + g4[1][i]) : 1.0;
   __syncthreads();
   // 4. every column node of the unit: sum of the boxes holding it (table of step 2), scatter
-  // (x W for S^-1).  Same (row, z) map as the gather; a lane's table entry is read once per z
-  // block and serves its MT rows; the next block's node ids and weights load behind this block's sums
-  for (int zi = 0; zi < nzi; ++zi) {
-    const int z = lane + 32 * zi;
-    const bool zv = z < nzu;
-    int gn[MT];
-    const int zn1 = z + 32;
+  // (x W for S^-1).  Same (row, z) map as the gather, two z blocks per pass (node ids and
+  // weights of the first pass loaded behind steps 2 and 3); a lane's table entry is read once
+  // per z block and serves its MT rows
+  for (int zi = 0; zi < nzi; zi += 2) {
+    if (zi > 0) {
 #pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      const int h = warp + 8 * i;
-      gn[i] = (zi + 1 < nzi && h < nh && zn1 < nzu) ? __ldg(ci + h * nz + zlo + zn1) : -1;
-    }
-    const int nk = zv ? zn[z] : 0;
-    int o[ZO];
-    {
-      const short4 t4 = zv ? *reinterpret_cast<const short4*>(zo[z]) : make_short4(0, 0, 0, 0);
-      o[0] = t4.x, o[1] = t4.y, o[2] = t4.z, o[3] = t4.w;
-    }
-    double acc[MT];
-    if (__all_sync(0xffffffffu, nk <= ZO)) {
+      for (int b = 0; b < 2; ++b)
 #pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const double* row = B2 + (warp + 8 * i) * ldb;   // rows < 8 MT: inside B2 for every i
-        double a = 0.0;
-#pragma unroll
-        for (int q = 0; q < ZO; ++q) {
-          const double x = row[o[q]];
-          a += q < nk ? x : 0.0;
+        for (int i = 0; i < MT; ++i) {
+          const int h = warp + 8 * i, z = lane + 32 * (zi + b);
+          g4[b][i] = (h < nh && z < nzu) ? __ldg(ci + h * nz + zlo + z) : -1;
         }
-        acc[i] = a;
-      }
-    } else {  // more boxes than tabulated (not met for the box sizes of this kernel): walk the run
 #pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const double* row = B2 + (warp + 8 * i) * ldb;
-        double a = 0.0;
-        for (int j = 0; j < cnt; ++j) {
-          const int zz = z - (ez0[j] - zlo);
-          if (zv && zz >= 0 && zz < env[j] && !sk[j]) a += row[soff[j] + zz];
-        }
-        acc[i] = a;
-      }
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int i = 0; i < MT; ++i) w4[b][i] = (!transpose && g4[b][i] >= 0) ? __ldg(W + g4[b][i]) : 1.0;
     }
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
-      if (g4[i] >= 0) atomicAdd(u + g4[i], acc[i] * w4[i]);
+    for (int b = 0; b < 2; ++b) {
+      const int z = lane + 32 * (zi + b);
+      const bool zv = z < nzu;
+      const int nk = zv ? zn[z] : 0;
+      int o[ZO];
+      {
+        const short4 t4 = zv ? *reinterpret_cast<const short4*>(zo[z]) : make_short4(0, 0, 0, 0);
+        o[0] = t4.x, o[1] = t4.y, o[2] = t4.z, o[3] = t4.w;
+      }
+      double acc[MT];
+      if (__all_sync(0xffffffffu, nk <= ZO)) {
 #pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      g4[i] = gn[i];
-      w4[i] = (!transpose && gn[i] >= 0) ? __ldg(W + gn[i]) : 1.0;
+        for (int i = 0; i < MT; ++i) {
+          const double* row = B2 + (warp + 8 * i) * ldb;   // rows < 8 MT: inside B2 for every i
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < ZO; ++q) {
+            const double x = row[o[q]];
+            a += q < nk ? x : 0.0;
+          }
+          acc[i] = a;
+        }
+      } else {  // more boxes than tabulated (not met for the box sizes of this kernel): walk the run
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const double* row = B2 + (warp + 8 * i) * ldb;
+          double a = 0.0;
+          for (int j = 0; j < cnt; ++j) {
+            const int zz = z - (ez0[j] - zlo);
+            if (zv && zz >= 0 && zz < env[j] && !sk[j]) a += row[soff[j] + zz];
+          }
+          acc[i] = a;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+        if (g4[b][i] >= 0) atomicAdd(u + g4[b][i], acc[i] * w4[b][i]);
     }
   }
 }
