@@ -406,6 +406,36 @@ __global__ void __launch_bounds__(256) k_fdm(const int32_t* __restrict__ col, co
 }
 
 
+// S_h (n_h x n_h, row-major, global) -> Ss [ROWS][LDS] by 8-byte cp.async, zero-filled beyond n_h
+// (source size 0).  16 threads per row, 16 rows per pass: row base and validity once per row,
+// one compare + select per element (the flat t -> (t / ROWS, t % ROWS) map cost ~10 instructions
+// per element, 11 % of k_fdm_cta<8>'s instructions); 128-byte runs per row
+template <int ROWS, int LDS>
+__device__ __forceinline__ void fdm_stage_Sh(double* __restrict__ Ss, const double* __restrict__ S, int nh, int tid) {
+  const int ti = tid >> 4, ta = tid & 15;
+  constexpr int NP = (ROWS + 15) / 16;
+#pragma unroll
+  for (int pi = 0; pi < NP; ++pi) {
+    const int i = ti + 16 * pi;
+    if (i < ROWS) {
+      const bool rv = i < nh;
+      const double* src = S + (rv ? i * nh : 0);
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(Ss + i * LDS + ta));
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const int a = ta + 16 * k;
+        if (a < ROWS) {
+          const bool v = rv && a < nh;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + 128 * k), "l"(src + (v ? a : 0)),
+                       "r"(v ? 8 : 0)
+                       : "memory");
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // 1 / d for d = l_h + l_v > 0 (normal range): MUFU.RCP64H seed (~20 bits) + two Newton steps
 // (2^-40, 2^-80: FP64 accurate); replaces the float round trip (two conversions + the IEEE
 // float reciprocal's fix-up branch)
@@ -638,21 +668,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
   (void)nzc;
   (void)z0;
   (void)nvv;
-  {  // S_h -> shared by cp.async (zero-filled padding), in flight during the column-block gather
-    constexpr int IS = (ROWS * ROWS + 255) / 256;
-#pragma unroll
-    for (int k = 0; k < IS; ++k) {
-      const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
-      if (t < ROWS * ROWS) {
-        const bool v = i < nh && a < nh;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                         static_cast<uint32_t>(__cvta_generic_to_shared(Ss + i * LDS + a))),
-                     "l"(S + (v ? i * nh + a : 0)), "r"(v ? 8 : 0)
-                     : "memory");
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
+  fdm_stage_Sh<ROWS, LDS>(Ss, S, nh, tid);   // in flight during the column-block gather
   const int zlo = ez0[0], nzu = ez0[cnt - 1] + env[cnt - 1] - zlo;
   // column block gather: warp w owns the rows h = w + 8 i (i < MT), its lanes the z positions
   // z = lane + 32 zi (coalesced connectivity reads, no index division); the next z block's node
@@ -880,8 +896,9 @@ __device__ __forceinline__ void fdm_cta_gemm(const double* __restrict__ Ss, cons
   constexpr int ROWS = 8 * MT, LDS = ROWS + 4;
   const int r4 = lane >> 2, c4 = lane & 3;
   const int nt = (ncol + 7) / 8, np = (nt + 1) / 2, MP = (mtu + 1) / 2, KT = 2 * mtu;
+  const int minv = 65536 / MP + 1;   // job / MP for job < 2^10 (MP <= 4): one multiply instead of a division
   for (int job = warp; job < MP * np; job += 8) {
-    const int m0 = 2 * (job % MP), n0 = 2 * (job / MP);
+    const int jn = (job * minv) >> 16, m0 = 2 * (job - jn * MP), n0 = 2 * jn;
     const bool m2 = m0 + 1 < mtu, n2 = n0 + 1 < nt;
     double cc[2][2][2] = {};
 #pragma unroll 4
@@ -960,22 +977,9 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
       const int h = warp + 8 * i, z = lane + 32 * b;
       gid0[b][i] = (h < nh && z < nzu) ? __ldg(ci + h * nz + zlo + z) : -1;
     }
-  {  // S_h -> shared by cp.async (zero-filled padding), completed with the column block below:
-     // the S_h bytes stream in while the gather's dependent loads are in flight
-    constexpr int IS = (ROWS * ROWS + 255) / 256;
-#pragma unroll
-    for (int k = 0; k < IS; ++k) {
-      const int t = tid + 256 * k, i = t / ROWS, a = t - i * ROWS;
-      if (t < ROWS * ROWS) {
-        const bool v = i < nh && a < nh;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                         static_cast<uint32_t>(__cvta_generic_to_shared(Ss + i * LDS + a))),
-                     "l"(S + (v ? i * nh + a : 0)), "r"(v ? 8 : 0)
-                     : "memory");
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
+  // S_h -> shared, completed with the column block below: the bytes stream in while the gather's
+  // dependent loads are in flight
+  fdm_stage_Sh<ROWS, LDS>(Ss, S, nh, tid);
   // column block (x W for S^-T): the n_h x n_zu valid entries; rows >= n_h zeroed (they meet the
   // zero columns of S_h^T: stale shared memory there could hold non-finite values), columns
   // >= n_zu only reach output columns no later step reads
