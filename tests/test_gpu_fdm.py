@@ -2,6 +2,8 @@
 the oracle's FDM smoother (oracle/fdm.py: Kronecker box inverted by
 numpy.linalg.inv), element by element through the C ABI; V-cycle and solve
 parity; the FDM smoother equals the exact dense one on straight flat prisms."""
+import os
+
 import numpy as np
 import pytest
 
@@ -187,3 +189,42 @@ def test_fdm_cta8_on_p6_hull_replica():
         got[perm] = u.cpu().numpy()
         assert rel(got, zo) <= STEP_TOL
     s.close()
+
+
+def test_fdm_warp_nvt2_matches_cta():
+    """SEM_FDM_CTA=0 (read once per process, hence a subprocess) sends the p = 6 level-0 sweep of
+    the d6cta8 mesh through k_fdm_warp<8, 2>, the same arithmetic per box as k_fdm_cta<8> (whose
+    parity with the oracle is the d6cta8 case above): S^-1 r and S^-T r of both kernels agree to
+    rounding on every entry."""
+    import json
+    import subprocess
+    import sys
+    code = """
+import json, os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), 'tests'))
+import numpy as np, torch
+import paper_2009_00705_b200 as lib
+from workloads.configs import delaunay_basin
+m = delaunay_basin("fdm_cta8", 6, n_in=16, nz=3, seed=1)
+s = lib.Solver(m.vertices, m.prisms, m.face_tag, m.p, node_xyz=m.node_xyz(lib.reference_nodes(m.p)), local_solve=1)
+n = s.n_dof(0)
+r = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, n)).cuda()
+out = {"kernel": s.info["smoother_kernel"][0]}
+for tr in (0, 1):
+    u = torch.zeros(n, dtype=torch.float64, device="cuda")
+    s.schwarz(0, r, u, transpose=bool(tr))
+    out[str(tr)] = u.cpu().numpy().tolist()
+print("RESULT" + json.dumps(out))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for cta in ("1", "0"):
+        env = dict(os.environ, SEM_FDM_CTA=cta)
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+        assert p.returncode == 0, p.stderr[-2000:]
+        line = next(l for l in p.stdout.splitlines() if l.startswith("RESULT"))
+        res[cta] = json.loads(line[6:])
+    assert (res["1"]["kernel"], res["0"]["kernel"]) == ("k_fdm_cta<MT>", "k_fdm_warp<MT,2>")
+    for tr in ("0", "1"):
+        a, b = np.array(res["1"][tr]), np.array(res["0"][tr])
+        assert np.linalg.norm(a) > 0 and rel(b, a) <= STEP_TOL
