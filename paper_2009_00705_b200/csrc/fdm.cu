@@ -646,7 +646,9 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
   // [2] n_h, [3] Z_c + 1, [4..5] S_h offset, [6..7] node-id offset, [8..9] l_h offset,
   // [10..17] element ids, [18..25] z0, [26..33] n_v
   __shared__ int ud[FDM_UD];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp-uniform values go through a lane-0 broadcast: ptxas then sees the branches on them as
+  // uniform (no WARPSYNC.ALL + NOP in front of the mma.sync's they guard)
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int ub = ulist ? __ldg(ulist + blockIdx.x) : (int)blockIdx.x;   // unit (or the listed subset's)
   if (tid < FDM_UD) ud[tid] = __ldg(udesc + (size_t)ub * FDM_UD + tid);
   __syncthreads();
@@ -707,7 +709,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  const bool active = warp < cnt && !skip[eid[warp < cnt ? warp : 0]];
+  const bool active = __shfl_sync(0xffffffffu, (int)(warp < cnt && !skip[eid[warp < cnt ? warp : 0]]), 0) != 0;
   const int j = warp < cnt ? warp : 0;
   const int zb = ez0[j] - zlo, nvj = env[j];
   double b1[KT][NVT];
@@ -727,7 +729,7 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
     // T = S_h^T B1 over the unit's mtu = ceil(n_h / 8) tiles (S_h is zero beyond n_h: the
     // skipped tiles are exact zeros); for MT >= 5 only (the guards cost more than they save at
     // the small tile counts of p <= 3: measured on config 5's p = 2, 3 levels)
-    const int mtu = MT >= 5 ? (nh + 7) / 8 : MT, ktu = 2 * mtu;
+    const int mtu = MT >= 5 ? __shfl_sync(0xffffffffu, (nh + 7) / 8, 0) : MT, ktu = 2 * mtu;
     // the element's vertical modes and the first horizontal eigenvalue: loads in flight behind
     // the first GEMM (their latency sat on the vertical step's first use)
     const double* sv = Svp + (size_t)e * NVP * NVP;
@@ -890,40 +892,55 @@ __global__ void __launch_bounds__(256, NVT == 1 ? (MT <= 4 ? 4 : 3) : 2) k_fdm_w
 // accumulator chains); A fragment a0 = A[m][k] read through (m, k) -> aidx, B from Bs[k][n] (ld ldb).
 // Only the unit's mtu = ceil(n_h / 8) row / contraction tiles: S_h is zero beyond n_h, so the
 // skipped tiles contribute exact zeros (and later steps read no row >= 8 mtu)
+// one 2 x 2-tile job of fdm_cta_gemm with its tile validity at compile time: no branch inside the
+// k loop (with run-time `if (m2)` / `if (n2)` around the mma.sync, ptxas put a WARPSYNC.ALL + NOP
+// in front of every DMMA and a branch per m-tile: 3 issue slots per DMMA)
+template <int MT, bool AT, bool M2, bool N2>
+__device__ __forceinline__ void fdm_cta_job(const double* __restrict__ Ss, const double* __restrict__ Bs,
+                                            double* __restrict__ Cs, int ldb, int ncol, int m0, int n0, int KT,
+                                            int r4, int c4) {
+  constexpr int ROWS = 8 * MT, LDS = ROWS + 4;
+  double cc[2][2][2] = {};
+  const double* pa = AT ? Ss + c4 * LDS + m0 * 8 + r4 : Ss + (m0 * 8 + r4) * LDS + c4;
+  const double* pb = Bs + c4 * ldb + n0 * 8 + r4;
+#pragma unroll 4
+  for (int kt = 0; kt < KT; ++kt) {
+    double af[2], bf[2];
+    af[0] = pa[0];
+    if (M2) af[1] = AT ? pa[8] : pa[8 * LDS];
+    bf[0] = pb[0];
+    if (N2) bf[1] = pb[8];
+    pa += AT ? 4 * LDS : 4;
+    pb += 4 * ldb;
+    fdm_dmma(cc[0][0][0], cc[0][0][1], af[0], bf[0]);
+    if (N2) fdm_dmma(cc[0][1][0], cc[0][1][1], af[0], bf[1]);
+    if (M2) fdm_dmma(cc[1][0][0], cc[1][0][1], af[1], bf[0]);
+    if (M2 && N2) fdm_dmma(cc[1][1][0], cc[1][1][1], af[1], bf[1]);
+  }
+#pragma unroll
+  for (int x = 0; x < (M2 ? 2 : 1); ++x)
+#pragma unroll
+    for (int n = 0; n < (N2 ? 2 : 1); ++n)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int col = (n0 + n) * 8 + 2 * c4 + i;
+        if (col < ncol) Cs[((m0 + x) * 8 + r4) * ldb + col] = cc[x][n][i];
+      }
+}
+
 template <int MT, bool AT>
 __device__ __forceinline__ void fdm_cta_gemm(const double* __restrict__ Ss, const double* __restrict__ Bs,
                                              double* __restrict__ Cs, int ldb, int ncol, int warp, int lane, int mtu) {
-  constexpr int ROWS = 8 * MT, LDS = ROWS + 4;
   const int r4 = lane >> 2, c4 = lane & 3;
   const int nt = (ncol + 7) / 8, np = (nt + 1) / 2, MP = (mtu + 1) / 2, KT = 2 * mtu;
   const int minv = 65536 / MP + 1;   // job / MP for job < 2^10 (MP <= 4): one multiply instead of a division
   for (int job = warp; job < MP * np; job += 8) {
     const int jn = (job * minv) >> 16, m0 = 2 * (job - jn * MP), n0 = 2 * jn;
-    const bool m2 = m0 + 1 < mtu, n2 = n0 + 1 < nt;
-    double cc[2][2][2] = {};
-#pragma unroll 4
-    for (int kt = 0; kt < KT; ++kt) {
-      double af[2], bf[2];
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const int m = (m0 + x) * 8 + r4, kk = kt * 4 + c4;
-        af[x] = AT ? Ss[kk * LDS + m] : Ss[m * LDS + kk];
-        bf[x] = Bs[kk * ldb + (n0 + x) * 8 + r4];
-      }
-      fdm_dmma(cc[0][0][0], cc[0][0][1], af[0], bf[0]);
-      if (n2) fdm_dmma(cc[0][1][0], cc[0][1][1], af[0], bf[1]);
-      if (m2) fdm_dmma(cc[1][0][0], cc[1][0][1], af[1], bf[0]);
-      if (m2 && n2) fdm_dmma(cc[1][1][0], cc[1][1][1], af[1], bf[1]);
-    }
-#pragma unroll
-    for (int x = 0; x < 2; ++x)
-#pragma unroll
-      for (int n = 0; n < 2; ++n)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int col = (n0 + n) * 8 + 2 * c4 + i;
-          if ((x == 0 || m2) && col < ncol) Cs[((m0 + x) * 8 + r4) * ldb + col] = cc[x][n][i];
-        }
+    const bool m2 = m0 + 1 < mtu, n2 = n0 + 1 < nt;   // warp-uniform
+    if (m2 && n2) fdm_cta_job<MT, AT, true, true>(Ss, Bs, Cs, ldb, ncol, m0, n0, KT, r4, c4);
+    else if (m2) fdm_cta_job<MT, AT, true, false>(Ss, Bs, Cs, ldb, ncol, m0, n0, KT, r4, c4);
+    else if (n2) fdm_cta_job<MT, AT, false, true>(Ss, Bs, Cs, ldb, ncol, m0, n0, KT, r4, c4);
+    else fdm_cta_job<MT, AT, false, false>(Ss, Bs, Cs, ldb, ncol, m0, n0, KT, r4, c4);
   }
 }
 
@@ -942,7 +959,9 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   __shared__ int ud[FDM_UD];
   __shared__ int soff[9];
   __shared__ int sk[8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, r4 = lane >> 2, c4 = lane & 3;
+  // warp-uniform values go through a lane-0 broadcast: ptxas then sees the branches on them as
+  // uniform (no WARPSYNC.ALL + NOP in front of the mma.sync's they guard)
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), r4 = lane >> 2, c4 = lane & 3;
   const int ub = ulist ? __ldg(ulist + blockIdx.x) : (int)blockIdx.x;   // unit (or the listed subset's)
   if (tid < FDM_UD) ud[tid] = __ldg(udesc + (size_t)ub * FDM_UD + tid);
   __syncthreads();
@@ -1034,8 +1053,8 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // 1. Tall = S_h^T Rc -> B2
-  const int mtu = (nh + 7) / 8;
-  fdm_cta_gemm<MT, true>(Ss, B1, B2, ldb, nzu, warp, lane, mtu);
+  const int mtu = __shfl_sync(0xffffffffu, (nh + 7) / 8, 0);
+  fdm_cta_gemm<MT, true>(Ss, B1, B2, ldb, __shfl_sync(0xffffffffu, nzu, 0), warp, lane, mtu);
   __syncthreads();
   // the scatter's first chunk (step 4): node ids now, weights before step 3, both in flight
   // behind the vertical step and the second GEMM (the same (h, z) <- t map as the gather)
@@ -1064,8 +1083,8 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     zn[z] = (unsigned char)k;
   }
   // 2. warp j: vertical transform and scaling of box j, stored compactly into Zs (B1)
-  if (warp < cnt && !sk[warp]) {
-    const int j = warp, zb = ez0[j] - zlo, nvj = env[j], so = soff[j];
+  if (__shfl_sync(0xffffffffu, (int)(warp < cnt && !sk[warp < cnt ? warp : 0]), 0)) {
+    const int j = warp, zb = ez0[j] - zlo, nvj = __shfl_sync(0xffffffffu, env[j], 0), so = soff[j];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       if (mt >= mtu) break;
@@ -1074,7 +1093,7 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
       for (int n = 0; n < NVT; ++n) v[n][0] = v[n][1] = 0.0;
 #pragma unroll
       for (int kt = 0; kt < 2 * NVT; ++kt) {  // A[a][col] = T_j[a][col] (zero beyond the box)
-        if (NVT == 2 && kt * 4 >= nvj) continue;   // k-steps beyond the box: exact zeros (n_v = p + 3 <= 11 needs 3 of 4)
+        if (kt >= 2 && kt * 4 >= nvj) continue;   // k-steps beyond the box: exact zeros (n_v >= 8; n_v = p + 3 <= 11 needs 3 of 4)
         const int col = kt * 4 + c4;
         const double a = col < nvj ? B2[(mt * 8 + r4) * ldb + zb + col] : 0.0;
 #pragma unroll
@@ -1093,7 +1112,7 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
       for (int n = 0; n < NVT; ++n) t2[n][0] = t2[n][1] = 0.0;
 #pragma unroll
       for (int kt = 0; kt < 2 * NVT; ++kt) {
-        if (NVT == 2 && kt * 4 >= nvj) continue;   // k-steps beyond the box: exact zeros (n_v = p + 3 <= 11 needs 3 of 4)
+        if (kt >= 2 && kt * 4 >= nvj) continue;   // k-steps beyond the box: exact zeros (n_v >= 8; n_v = p + 3 <= 11 needs 3 of 4)
         const double a = c_to_a<NVT>(v, kt, lane);
 #pragma unroll
         for (int n = 0; n < NVT; ++n) fdm_dmma(t2[n][0], t2[n][1], a, s2[kt][n]);
@@ -1117,7 +1136,7 @@ __global__ void __launch_bounds__(256, 2) k_fdm_cta(const int32_t* __restrict__ 
     g4[1][i] = (h < nh && z < nzu) ? __ldg(ci + h * nz + zlo + z) : -1;
   }
   // 3. Ys = S_h Zs -> B2 over the stacked columns
-  fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, soff[cnt], warp, lane, mtu);
+  fdm_cta_gemm<MT, false>(Ss, B1, B2, ldb, __shfl_sync(0xffffffffu, soff[cnt], 0), warp, lane, mtu);
 #pragma unroll
   for (int i = 0; i < MT; ++i) w4[1][i] = (!transpose && g4[1][i] >= 0) ? __ldg(W + g4[1][i]) : 1.0;
   __syncthreads();
